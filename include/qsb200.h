@@ -1,0 +1,132 @@
+/*
+ * qsb200.h — C ABI of the B200-native state-vector backend (libqsb200.so).
+ *
+ * The reference (pairsim, /root/reference/pkg/src/pairsim) has no FFI: its
+ * boundary is a Python function API over a host numpy buffer.  This header is
+ * the native seam that the Python host layer (paper_1805_00988_b200/) binds
+ * with ctypes; every entry point below names the reference function whose
+ * semantics it reproduces.
+ *
+ * Conventions
+ *   - Amplitudes are complex64, interleaved (re, im) float32, qubit t = bit t
+ *     of the basis index (pkg/src/pairsim/state.py:3-5).
+ *   - A 2x2 gate [[a, b], [c, d]] is passed as float m[8] =
+ *     {a.re, a.im, b.re, b.im, c.re, c.im, d.re, d.im}, already rounded to
+ *     float32 exactly as `np.complex64(x)` rounds (pkg/src/pairsim/kernel.py:118-119).
+ *   - Every call returns an int status; 0 = QS_OK.  On failure the message is
+ *     available from qs_last_error() (thread-local).
+ *   - A handle owns one device buffer and one CUDA stream.  Mutating calls are
+ *     asynchronous on that stream (stream order is the sweep barrier of
+ *     pkg/src/pairsim/kernel.py:244-245); getters synchronize.  One host thread
+ *     per handle at a time.
+ */
+#ifndef QSB200_H
+#define QSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB200_ABI_VERSION 1
+
+/* Status codes.  The Python layer maps them onto the reference's exception
+ * taxonomy (pkg/src/pairsim/errors.py:4-37). */
+enum {
+    QS_OK = 0,
+    QS_ERR_INDEX = 1,      /* IndexError: qubit or basis index out of range   */
+    QS_ERR_VALUE = 2,      /* ValueError: control == target, n < 1, k < 1 ... */
+    QS_ERR_CAPACITY = 3,   /* CapacityError: register over the memory budget  */
+    QS_ERR_DEGENERATE = 4, /* DegenerateStateError: all probabilities zero    */
+    QS_ERR_CUDA = 5,       /* CUDA runtime failure (message has the details)  */
+    QS_ERR_NULL = 6        /* null handle or output pointer                   */
+};
+
+typedef struct qs_state qs_state;
+
+/* numpy PCG64 generator state (bit_generator.state["state"]), split into
+ * 64-bit halves.  Draws are (next64 >> 11) * 2^-53, exactly numpy's
+ * Generator.random() (pkg/src/pairsim/measure.py:81-82). */
+typedef struct {
+    uint64_t state_hi, state_lo;
+    uint64_t inc_hi, inc_lo;
+} qs_pcg64;
+
+/* One operation of a fused pass (qs_apply_fused). */
+enum {
+    QS_OP_PAIR = 0,  /* 2x2 pair update on `target` under `ctrl_mask`           */
+    QS_OP_PHASE = 1  /* amps with every bit of (1<<target | ctrl_mask) set are
+                        multiplied by d; requires a == 1, b == c == 0          */
+};
+
+typedef struct {
+    int32_t kind;       /* QS_OP_PAIR or QS_OP_PHASE                              */
+    int32_t target;     /* global qubit index                                     */
+    uint64_t ctrl_mask; /* global control qubits (all must be 1); excludes target */
+    float m[8];         /* gate entries, as for qs_apply_gate                      */
+} qs_op;
+
+/* ---- library ------------------------------------------------------------ */
+int qs_abi_version(void);
+const char *qs_last_error(void);
+int qs_device_count(int *out);
+
+/* ---- lifecycle: pkg/src/pairsim/state.py:122-143 (new_state) ------------ */
+/* Allocates 8 * 2^n bytes on `device` and initialises |0...0>.
+ * memory_budget == 0 selects the default budget: 75% of the device's free
+ * memory (the GPU analogue of default_memory_budget, state.py:114-119).
+ * Fails with QS_ERR_CAPACITY *before* allocating when over budget; a budget
+ * equal to the need is allowed (pkg/tests/test_state.py:45-52). */
+int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out);
+int qs_destroy(qs_state *s);
+int qs_num_qubits(const qs_state *s, int *out);
+int qs_device(const qs_state *s, int *out);
+/* Raw device pointer / cudaStream_t of the handle (for transports and
+ * device-side timing; the pointer stays owned by the handle). */
+int qs_device_pointer(qs_state *s, void **out);
+int qs_stream(qs_state *s, void **out);
+/* Overwrite the register with basis state |basis> (amps = e_basis). */
+int qs_reset(qs_state *s, uint64_t basis);
+int qs_synchronize(qs_state *s);
+
+/* ---- gates: pkg/src/pairsim/kernel.py:108-165 --------------------------- */
+/* apply_gate (kernel.py:108-132): per pair (a, b = a|1<<t):
+ *   v_a' = m_a v_a + m_b v_b ;  v_b' = m_d v_b + m_c v_a   (pre-update values) */
+int qs_apply_gate(qs_state *s, int target, const float m[8]);
+/* apply_controlled_gate (kernel.py:135-165): same update where bit `control`
+ * is 1; QS_ERR_INDEX out of range, QS_ERR_VALUE when control == target. */
+int qs_apply_controlled_gate(qs_state *s, int control, int target, const float m[8]);
+/* Doubly-controlled update (QCGPU's apply_controlled_controlled_gate; no
+ * pairsim counterpart): the update where bits c1 and c2 are both 1. */
+int qs_apply_controlled_controlled_gate(qs_state *s, int c1, int c2, int target, const float m[8]);
+/* Fused pass: one HBM read+write of the register applies `ops` in order,
+ * bit-identical to applying them one by one.  `tile_qubits` (ntile entries,
+ * must contain 0..5 when num_qubits >= 6) is the set of qubits held in each
+ * on-chip tile; every QS_OP_PAIR target must be in it (controls and phase
+ * bits may be anywhere). */
+int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile,
+                   const qs_op *ops, int nops);
+/* Swap qubits q1 and q2 (a basis permutation; used by the sharded layer). */
+int qs_swap_qubits(qs_state *s, int q1, int q2);
+
+/* ---- readout: state.py:146-161, measure.py:29-99 ------------------------- */
+int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, float *host);
+int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const float *host);
+/* probabilities (measure.py:29-34): p[j] = re^2 + im^2 in fp64, bit-exact. */
+int qs_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
+/* norm_squared (state.py:146-151): fp64 sum of |a|^2 (tree order). */
+int qs_norm_squared(qs_state *s, double *out);
+/* sample (measure.py:76-85): k draws from `rng` against the normalised
+ * sequential fp64 CDF, searchsorted(side="right"), clamped to dim-1.
+ * out[i] is the outcome of draw i.  Bit-exact with the reference for the
+ * same generator state.  QS_ERR_DEGENERATE when all probabilities are 0. */
+int qs_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
+/* measure_collapse (measure.py:88-99): one draw, then amps = e_outcome. */
+int qs_measure_collapse(qs_state *s, const qs_pcg64 *rng, int64_t *outcome);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSB200_H */

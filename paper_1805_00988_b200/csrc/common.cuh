@@ -1,0 +1,80 @@
+// Shared device helpers for libqsb200 (sm_100a).
+//
+// Arithmetic contract: every complex product is evaluated exactly as numpy's
+// complex64 SIMD multiply does on an FMA host (SURVEY.md Appendix A.1,
+// re-verified by oracle/ tests):
+//     (g * v).re = fma(g.re, v.re, -rn(g.im * v.im))
+//     (g * v).im = fma(g.re, v.im,  rn(g.im * v.re))
+// with the gate entry g as the left operand (pkg/src/pairsim/kernel.py:128-129),
+// and the two products of a pair update added component-wise in fp32.
+// Explicit __f*_rn intrinsics keep nvcc from re-contracting the expression.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qsb200.h"
+
+namespace qsb {
+
+struct Gate2 {
+    float2 a, b, c, d;
+};
+
+__host__ __device__ inline Gate2 gate_from(const float m[8]) {
+    Gate2 g;
+    g.a = make_float2(m[0], m[1]);
+    g.b = make_float2(m[2], m[3]);
+    g.c = make_float2(m[4], m[5]);
+    g.d = make_float2(m[6], m[7]);
+    return g;
+}
+
+__device__ __forceinline__ float2 cmul(float2 g, float2 v) {
+    float re = __fmaf_rn(g.x, v.x, -__fmul_rn(g.y, v.y));
+    float im = __fmaf_rn(g.x, v.y, __fmul_rn(g.y, v.x));
+    return make_float2(re, im);
+}
+
+__device__ __forceinline__ float2 cadd(float2 x, float2 y) {
+    return make_float2(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y));
+}
+
+// v_a' = a v_a + b v_b ; v_b' = d v_b + c v_a  (kernel.py:128-129)
+__device__ __forceinline__ void pair_update(const Gate2 &g, float2 &va, float2 &vb) {
+    float2 na = cadd(cmul(g.a, va), cmul(g.b, vb));
+    float2 nb = cadd(cmul(g.d, vb), cmul(g.c, va));
+    va = na;
+    vb = nb;
+}
+
+// Lane-uniform form used by the shuffle path: own' = g1*own + g2*partner with
+// (g1, g2) = (a, b) on the bit-clear side and (d, c) on the bit-set side.
+__device__ __forceinline__ float2 lin2(float2 g1, float2 own, float2 g2, float2 partner) {
+    return cadd(cmul(g1, own), cmul(g2, partner));
+}
+
+// Insert a 0 bit at position p (the paper's nth_cleared, kernel.py:31-37).
+__device__ __forceinline__ uint64_t insert_zero(uint64_t i, int p) {
+    uint64_t lo = i & ((1ull << p) - 1ull);
+    return lo | ((i ^ lo) << 1);
+}
+
+// Up to kMaxFixed fixed bit positions, sorted ascending.
+constexpr int kMaxFixed = 8;
+struct FixedBits {
+    int n;
+    int pos[kMaxFixed];
+};
+
+__device__ __forceinline__ uint64_t deposit(uint64_t i, const FixedBits &fb) {
+#pragma unroll
+    for (int k = 0; k < kMaxFixed; ++k)
+        if (k < fb.n) i = insert_zero(i, fb.pos[k]);
+    return i;
+}
+
+__device__ __forceinline__ float4 ld_stream(const float4 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
+
+}  // namespace qsb

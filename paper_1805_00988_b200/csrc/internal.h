@@ -1,0 +1,65 @@
+// Host-side internals shared by the libqsb200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "qsb200.h"
+
+struct qs_state {
+    int num_qubits;
+    int device;
+    float2 *amps;          // 2^n complex64, 256-B aligned (cudaMalloc)
+    cudaStream_t stream;   // all work on this handle is ordered on it
+    int num_sms;
+    // measurement scratch (lazily grown; freed with the handle)
+    void *scratch;
+    size_t scratch_bytes;
+    void *pinned;          // small pinned host buffer for results
+    size_t pinned_bytes;
+    // fused-pass op buffer (device copy of qs_op arrays)
+    void *ops_dev;
+    size_t ops_bytes;
+};
+
+namespace qsb {
+
+int set_error(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+// RAII guard: switch to the handle's device for the duration of a call.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int ensure_scratch(qs_state *s, size_t bytes);
+int ensure_pinned(qs_state *s, size_t bytes);
+
+// kernels (gates.cu / measure.cu / fused.cu)
+int launch_sweep(qs_state *s, int target, uint64_t ctrl_mask, const float m[8]);
+int launch_phase(qs_state *s, uint64_t mask, float2 d);
+int launch_swap(qs_state *s, int q1, int q2);
+int launch_reset(qs_state *s, uint64_t basis);
+int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
+int run_norm(qs_state *s, double *out);
+int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
+int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops);
+
+}  // namespace qsb
+
+#define QS_CUDA(call)                                          \
+    do {                                                       \
+        cudaError_t _e = (call);                               \
+        if (_e != cudaSuccess) return qsb::cuda_fail(_e, #call); \
+    } while (0)

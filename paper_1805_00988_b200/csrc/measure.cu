@@ -1,0 +1,441 @@
+// Probability / measurement chain (K7-K10) for sm_100a.
+//
+// probabilities (pkg/src/pairsim/measure.py:29-34): p = re*re + im*im in fp64.
+// Both squares of a float32 are exact in fp64, so one __dadd_rn reproduces
+// numpy bit for bit.
+//
+// sample (measure.py:68-85) draws u = (pcg64_next >> 11) * 2^-53 and returns
+// searchsorted(cdf / cdf[-1], u, side="right") clamped to dim-1, where cdf is
+// numpy's *sequential* fp64 cumsum.  A parallel scan rounds differently, so
+// the device reproduces the sequential sum exactly with a shift-equivariance
+// argument:
+//
+//   Inside one binade [2^e, 2^(e+1)) doubles lie on a grid of spacing
+//   u = ulp(2^e), and round-to-nearest onto that grid commutes with shifts by
+//   even multiples of u (odd multiples flip ties-to-even).  So if a chunk's
+//   sequential trajectory is computed from a guessed start g0 (an even grid
+//   point) and from g1 = g0 + u, and both trajectories stay inside the binade,
+//   then the trajectory from the true start s = g0 + m*u (same binade) is the
+//   g0 trajectory shifted by m*u when m is even and the g1 trajectory shifted
+//   by (m-1)*u when m is odd — exactly, including every rounding.
+//
+// Pipeline (C = 4096 amplitudes per chunk):
+//   M1 k_chunk_sums   parallel fp64 chunk sums (any order: guesses only)
+//   M2 k_scan_guess   exclusive scan of the sums -> guessed chunk starts
+//   M3 k_trajectories both guessed trajectories per chunk (warp-transposed
+//                     through shared memory so HBM reads stay coalesced)
+//   M4 k_resolve      one thread walks the chunks: true start s, parity of
+//                     s's mantissa selects the trajectory, end = s + D exactly;
+//                     chunks that cross a binade (or whose guess fell in the
+//                     wrong binade) are re-summed sequentially from s
+//   M5 k_chunk_last   normalised CDF value at each chunk end
+//   M6 k_draws        per draw: PCG64 jump-ahead, binary search over chunk
+//                     ends, then the sequential in-chunk walk from the exact
+//                     chunk start to the first fl(cdf/total) > u.
+// No N-sized CDF is materialised; every value compared against u equals the
+// reference's cdf[j] / total bit for bit.
+
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace qsb {
+
+namespace {
+
+constexpr int kChunkLog = 12;  // 4096 amplitudes per chunk
+
+__device__ __forceinline__ double prob(float2 a) {
+    double re = (double)a.x, im = (double)a.y;
+    return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+}
+
+__global__ void k_probs(const float2 *__restrict__ amps, double *__restrict__ out, uint64_t count) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = prob(amps[i]);
+}
+
+// ---- norm: fixed-shape two-pass tree reduction (deterministic) -------------
+constexpr int kNormBlocks = 1024;
+constexpr int kNormThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (int)(blockDim.x >> 5) ? sh[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
+__global__ void k_norm_partial(const float2 *__restrict__ amps, uint64_t n, double *partial) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        acc += prob(amps[i]);
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+__global__ void k_norm_final(const double *partial, int n, double *out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) *out = acc;
+}
+
+// ---- M1: chunk sums ---------------------------------------------------------
+__global__ void k_chunk_sums(const float2 *__restrict__ amps, int clog, double *__restrict__ csum) {
+    __shared__ double sh[32];
+    const uint64_t c = blockIdx.x;
+    const uint64_t C = 1ull << clog;
+    const float2 *p = amps + (c << clog);
+    double acc = 0.0;
+    for (uint64_t j = threadIdx.x; j < C; j += blockDim.x) acc += prob(p[j]);
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) csum[c] = acc;
+}
+
+// ---- M2: exclusive scan of chunk sums (single block) -------------------------
+__global__ void k_scan_guess(const double *__restrict__ csum, uint64_t nch, double *__restrict__ g) {
+    __shared__ double part[1024];
+    const uint64_t per = (nch + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * per;
+    const uint64_t hi = lo + per < nch ? lo + per : nch;
+    double acc = 0.0;
+    for (uint64_t i = lo; i < hi; ++i) acc += csum[i];
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (unsigned i = 0; i < blockDim.x; ++i) {
+            double t = part[i];
+            part[i] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    double run = part[threadIdx.x];
+    for (uint64_t i = lo; i < hi; ++i) {
+        g[i] = run;
+        run += csum[i];
+    }
+}
+
+// binade helpers on the bit pattern of a non-negative double
+__device__ __forceinline__ double binade_hi(double g) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(g);
+    const uint64_t E = bits >> 52;
+    if (E <= 1) return __longlong_as_double((long long)(2ull << 52));  // 2^-1021
+    return __longlong_as_double((long long)((E + 1) << 52));
+}
+__device__ __forceinline__ double binade_lo(double g) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(g);
+    const uint64_t E = bits >> 52;
+    if (E <= 1) return 0.0;
+    return __longlong_as_double((long long)(E << 52));
+}
+
+enum : int { kFlagOk = 1, kFlagExact0 = 2 };
+
+// ---- M3: guessed trajectories -------------------------------------------------
+// One warp owns 32 consecutive chunks; every 32-element step the warp loads a
+// 32x32 tile (each row = 32 consecutive amplitudes of one chunk, a coalesced
+// 256-B read), converts to probabilities in shared memory, and lane L walks
+// row L sequentially with both chains.
+constexpr int kTrajWarps = 4;
+__global__ void __launch_bounds__(kTrajWarps * 32)
+    k_trajectories(const float2 *__restrict__ amps, uint64_t nch, int clog,
+                   const double *__restrict__ g, double *__restrict__ g0out,
+                   double *__restrict__ d0, double *__restrict__ d1, double *__restrict__ hiout,
+                   int *__restrict__ flags) {
+    __shared__ double tile[kTrajWarps][32][33];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t first = ((uint64_t)blockIdx.x * kTrajWarps + w) * 32;
+    if (first >= nch) return;
+    const uint64_t my = first + lane;
+    const uint64_t C = 1ull << clog;
+    const bool active = my < nch;
+
+    double gg = active ? g[my] : 0.0;
+    const bool exact0 = (my == 0) || gg == 0.0;
+    double g0 = gg, g1 = gg, hi = 0.0;
+    if (!exact0) {
+        g0 = __longlong_as_double(__double_as_longlong(gg) & ~1ll);
+        g1 = __longlong_as_double(__double_as_longlong(g0) + 1ll);
+        hi = binade_hi(g0);
+    } else {
+        g0 = 0.0;
+        g1 = 0.0;
+    }
+    double t0 = g0, t1 = g1;
+    const int rows = (int)((nch - first) < 32 ? (nch - first) : 32);
+    for (uint64_t j0 = 0; j0 < C; j0 += 32) {
+        const int width = (int)((C - j0) < 32 ? (C - j0) : 32);
+        for (int r = 0; r < rows; ++r) {
+            double v = 0.0;
+            if (lane < width) v = prob(amps[((first + r) << clog) + j0 + lane]);
+            tile[w][r][lane] = v;
+        }
+        __syncwarp();
+        if (active) {
+            for (int j = 0; j < width; ++j) {
+                const double p = tile[w][lane][j];
+                t0 = __dadd_rn(t0, p);
+                t1 = __dadd_rn(t1, p);
+            }
+        }
+        __syncwarp();
+    }
+    if (!active) return;
+    g0out[my] = g0;
+    if (exact0) {
+        d0[my] = t0;  // exact end when the true start is 0
+        d1[my] = t0;
+        hiout[my] = 0.0;
+        flags[my] = kFlagExact0;
+    } else {
+        d0[my] = __dsub_rn(t0, g0);  // exact: same grid, same binade
+        d1[my] = __dsub_rn(t1, g1);
+        hiout[my] = hi;
+        flags[my] = (t0 < hi && t1 < hi) ? kFlagOk : 0;
+    }
+}
+
+// sequential re-sum of one chunk from an exact start (the reference's loop)
+__device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, int clog, double s) {
+    const uint64_t C = 1ull << clog;
+    const float2 *p = amps + (chunk << clog);
+    uint64_t j = 0;
+    if (C >= 8) {
+        const float4 *q = (const float4 *)p;
+        for (; j + 8 <= C; j += 8) {
+            float4 v0 = q[(j >> 1) + 0], v1 = q[(j >> 1) + 1], v2 = q[(j >> 1) + 2],
+                   v3 = q[(j >> 1) + 3];
+            s = __dadd_rn(s, prob(make_float2(v0.x, v0.y)));
+            s = __dadd_rn(s, prob(make_float2(v0.z, v0.w)));
+            s = __dadd_rn(s, prob(make_float2(v1.x, v1.y)));
+            s = __dadd_rn(s, prob(make_float2(v1.z, v1.w)));
+            s = __dadd_rn(s, prob(make_float2(v2.x, v2.y)));
+            s = __dadd_rn(s, prob(make_float2(v2.z, v2.w)));
+            s = __dadd_rn(s, prob(make_float2(v3.x, v3.y)));
+            s = __dadd_rn(s, prob(make_float2(v3.z, v3.w)));
+        }
+    }
+    for (; j < C; ++j) s = __dadd_rn(s, prob(p[j]));
+    return s;
+}
+
+// ---- M4: resolve true chunk starts (single thread) ---------------------------
+__global__ void k_resolve(const float2 *__restrict__ amps, uint64_t nch, int clog,
+                          const double *__restrict__ g0, const double *__restrict__ d0,
+                          const double *__restrict__ d1, const double *__restrict__ hi,
+                          const int *__restrict__ flags, double *__restrict__ start,
+                          double *__restrict__ total, unsigned long long *__restrict__ nslow) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s = 0.0;
+    unsigned long long slow = 0;
+    for (uint64_t k = 0; k < nch; ++k) {
+        start[k] = s;
+        const int f = flags[k];
+        double e;
+        bool valid;
+        if (f & kFlagExact0) {
+            valid = (s == 0.0);
+            e = d0[k];
+        } else {
+            const double h = hi[k];
+            const double lo = binade_lo(g0[k]);
+            const bool odd = (__double_as_longlong(s) & 1ll) != 0;
+            e = __dadd_rn(s, odd ? d1[k] : d0[k]);
+            valid = (f & kFlagOk) && s >= lo && s < h && e < h;
+        }
+        if (!valid) {
+            e = walk_chunk(amps, k, clog, s);
+            ++slow;
+        }
+        s = e;
+    }
+    *total = s;
+    *nslow = slow;
+}
+
+// ---- M5: normalised CDF value at each chunk end --------------------------------
+__global__ void k_chunk_last(const double *__restrict__ start, uint64_t nch,
+                             const double *__restrict__ total, double *__restrict__ last) {
+    const double t = *total;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nch;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const double end = (k + 1 < nch) ? start[k + 1] : t;
+        last[k] = __ddiv_rn(end, t);
+    }
+}
+
+// ---- PCG64 (numpy's default bit generator, XSL-RR 128/64) -------------------
+typedef unsigned __int128 u128;
+__device__ __forceinline__ u128 mk128(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
+__device__ __forceinline__ uint64_t pcg_output(u128 st) {
+    const uint64_t x = (uint64_t)(st >> 64) ^ (uint64_t)st;
+    const unsigned rot = (unsigned)(st >> 122);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+// state after `delta` LCG steps (Brown's jump-ahead)
+__device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
+    const u128 mult = mk128(2549297995355413924ull, 4865540595714422341ull);
+    u128 acc_mult = 1, acc_plus = 0, cur_mult = mult, cur_plus = inc;
+    while (delta) {
+        if (delta & 1ull) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return acc_mult * state + acc_plus;
+}
+
+// ---- M6: draws ---------------------------------------------------------------------
+__global__ void k_draws(const float2 *__restrict__ amps, uint64_t nch, int clog, uint64_t dim,
+                        const double *__restrict__ start, const double *__restrict__ last,
+                        const double *__restrict__ total, qs_pcg64 rng, int64_t k,
+                        int64_t *__restrict__ out) {
+    const double t = *total;
+    const u128 st0 = mk128(rng.state_hi, rng.state_lo);
+    const u128 inc = mk128(rng.inc_hi, rng.inc_lo);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const u128 st = pcg_advance(st0, inc, (uint64_t)i + 1ull);  // step, then output
+        const double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+        // first chunk whose last normalised value exceeds u
+        uint64_t lo = 0, hi = nch;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (last[mid] > u)
+                hi = mid;
+            else
+                lo = mid + 1;
+        }
+        uint64_t idx = dim;  // searchsorted returns dim when every value <= u
+        if (lo < nch) {
+            const uint64_t C = 1ull << clog;
+            const float2 *p = amps + (lo << clog);
+            double s = start[lo];
+            // s below `thr` cannot satisfy fl(s / t) > u; skip the division there
+            const double thr = __dmul_rn(__dmul_rn(u, t), 1.0 - 0x1p-50);
+            uint64_t j = 0;
+            for (; j < C; ++j) {
+                s = __dadd_rn(s, prob(p[j]));
+                if (s >= thr && __ddiv_rn(s, t) > u) break;
+            }
+            idx = (lo << clog) + j;
+        }
+        out[i] = (int64_t)(idx < dim - 1 ? idx : dim - 1);
+    }
+}
+
+}  // namespace
+
+int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host) {
+    const uint64_t piece = 1ull << 25;  // 256 MiB of fp64 per staging round
+    const uint64_t step = count < piece ? count : piece;
+    int rc = ensure_scratch(s, step * sizeof(double));
+    if (rc) return rc;
+    double *dev = (double *)s->scratch;
+    for (uint64_t done = 0; done < count; done += step) {
+        const uint64_t m = (count - done) < step ? (count - done) : step;
+        unsigned grid = (unsigned)((m + 255) / 256);
+        if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
+        k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, dev, m);
+        QS_CUDA(cudaGetLastError());
+        QS_CUDA(cudaMemcpyAsync(host + done, dev, m * sizeof(double), cudaMemcpyDeviceToHost,
+                                s->stream));
+        QS_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    return QS_OK;
+}
+
+int run_norm(qs_state *s, double *out) {
+    int rc = ensure_scratch(s, (kNormBlocks + 1) * sizeof(double));
+    if (rc) return rc;
+    double *partial = (double *)s->scratch;
+    const uint64_t n = 1ull << s->num_qubits;
+    k_norm_partial<<<kNormBlocks, kNormThreads, 0, s->stream>>>(s->amps, n, partial);
+    k_norm_final<<<1, kNormThreads, 0, s->stream>>>(partial, kNormBlocks, partial + kNormBlocks);
+    QS_CUDA(cudaGetLastError());
+    rc = ensure_pinned(s, sizeof(double));
+    if (rc) return rc;
+    QS_CUDA(cudaMemcpyAsync(s->pinned, partial + kNormBlocks, sizeof(double),
+                            cudaMemcpyDeviceToHost, s->stream));
+    QS_CUDA(cudaStreamSynchronize(s->stream));
+    *out = *(double *)s->pinned;
+    return QS_OK;
+}
+
+int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
+    const int n = s->num_qubits;
+    const uint64_t dim = 1ull << n;
+    const int clog = n < kChunkLog ? n : kChunkLog;
+    const uint64_t nch = dim >> clog;
+    // scratch: csum/g, g0, d0, d1, hi, start, last (doubles) + flags + total + nslow + outcomes
+    const size_t nd = 7 * nch + 2;
+    const size_t bytes = nd * sizeof(double) + nch * sizeof(int) + 64 + (size_t)k * sizeof(int64_t);
+    int rc = ensure_scratch(s, bytes);
+    if (rc) return rc;
+    double *base = (double *)s->scratch;
+    double *csum = base, *g0 = base + nch, *d0 = base + 2 * nch, *d1 = base + 3 * nch,
+           *hi = base + 4 * nch, *start = base + 5 * nch, *last = base + 6 * nch;
+    double *total = base + 7 * nch;
+    unsigned long long *nslow = (unsigned long long *)(base + 7 * nch + 1);
+    int *flags = (int *)(base + nd);
+    int64_t *dout = (int64_t *)((char *)flags + ((nch * sizeof(int) + 63) & ~(size_t)63));
+    // (bytes above reserves the 64-B alignment slack)
+
+    double *g = csum;  // M2 writes the guesses over a second array below
+    k_chunk_sums<<<(unsigned)nch, 256, 0, s->stream>>>(s->amps, clog, csum);
+    // guesses go to `start` temporarily (overwritten by M4)
+    k_scan_guess<<<1, 1024, 0, s->stream>>>(csum, nch, start);
+    g = start;
+    {
+        const uint64_t warps = (nch + 31) / 32;
+        const unsigned blocks = (unsigned)((warps + kTrajWarps - 1) / kTrajWarps);
+        k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(s->amps, nch, clog, g, g0, d0,
+                                                                  d1, hi, flags);
+    }
+    k_resolve<<<1, 1, 0, s->stream>>>(s->amps, nch, clog, g0, d0, d1, hi, flags, start, total,
+                                      nslow);
+    {
+        unsigned grid = (unsigned)((nch + 255) / 256);
+        if (grid > 4096) grid = 4096;
+        k_chunk_last<<<grid, 256, 0, s->stream>>>(start, nch, total, last);
+    }
+    {
+        unsigned grid = (unsigned)((k + 127) / 128);
+        if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
+        k_draws<<<grid, 128, 0, s->stream>>>(s->amps, nch, clog, dim, start, last, total, *rng, k,
+                                             dout);
+    }
+    QS_CUDA(cudaGetLastError());
+    rc = ensure_pinned(s, sizeof(double));
+    if (rc) return rc;
+    QS_CUDA(cudaMemcpyAsync(s->pinned, total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    QS_CUDA(cudaMemcpyAsync(out, dout, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            s->stream));
+    QS_CUDA(cudaStreamSynchronize(s->stream));
+    const double tot = *(double *)s->pinned;
+    if (!(tot > 0.0))  // measure.py:71-72
+        return set_error(QS_ERR_DEGENERATE, "all outcome probabilities are zero");
+    return QS_OK;
+}
+
+}  // namespace qsb

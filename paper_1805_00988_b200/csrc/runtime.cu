@@ -1,0 +1,358 @@
+// libqsb200 runtime: handle lifecycle, validation, error reporting and the
+// extern "C" entry points declared in include/qsb200.h.
+//
+// Validation order and messages follow the reference functions each entry
+// point replaces (cited per function) so the Python layer can re-raise the
+// same exception types.
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace qsb {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    std::string m = std::string("CUDA error in ") + what + ": " + cudaGetErrorName(e) + " (" +
+                    cudaGetErrorString(e) + ")";
+    return set_error(QS_ERR_CUDA, m);
+}
+
+int ensure_scratch(qs_state *s, size_t bytes) {
+    if (s->scratch_bytes >= bytes) return QS_OK;
+    if (s->scratch) {
+        QS_CUDA(cudaStreamSynchronize(s->stream));
+        QS_CUDA(cudaFree(s->scratch));
+        s->scratch = nullptr;
+        s->scratch_bytes = 0;
+    }
+    QS_CUDA(cudaMalloc(&s->scratch, bytes));
+    s->scratch_bytes = bytes;
+    return QS_OK;
+}
+
+int ensure_pinned(qs_state *s, size_t bytes) {
+    if (s->pinned_bytes >= bytes) return QS_OK;
+    if (s->pinned) {
+        QS_CUDA(cudaStreamSynchronize(s->stream));
+        QS_CUDA(cudaFreeHost(s->pinned));
+        s->pinned = nullptr;
+        s->pinned_bytes = 0;
+    }
+    QS_CUDA(cudaMallocHost(&s->pinned, bytes));
+    s->pinned_bytes = bytes;
+    return QS_OK;
+}
+
+static std::string format_bytes(unsigned long long b) {
+    // decimal units, 4 significant digits (pkg/src/pairsim/state.py:86-97)
+    if (b < 1000ull) return std::to_string(b) + " B";
+    const char *units[] = {"kB", "MB", "GB", "TB", "PB", "EB"};
+    double v = (double)b;
+    int u = 0;
+    for (u = 0; u < 6; ++u) {
+        v /= 1000.0;
+        if (v < 1000.0 || u == 5) break;
+    }
+    char buf[64];
+    int digits = v < 10 ? 3 : (v < 100 ? 2 : 1);
+    snprintf(buf, sizeof buf, "%.*f", digits, v);
+    std::string t(buf);
+    while (!t.empty() && t.back() == '0') t.pop_back();
+    if (!t.empty() && t.back() == '.') t.pop_back();
+    return t + " " + units[u];
+}
+
+}  // namespace qsb
+
+using namespace qsb;
+
+#define CHECK_HANDLE(s) \
+    if (!(s)) return set_error(QS_ERR_NULL, "null qs_state handle")
+
+static int check_qubit(const qs_state *s, int q, const char *what) {
+    if (q < 0 || q >= s->num_qubits)
+        return set_error(QS_ERR_INDEX, std::string(what) + " " + std::to_string(q) +
+                                           " out of range for " + std::to_string(s->num_qubits) +
+                                           " qubits");
+    return QS_OK;
+}
+
+extern "C" {
+
+int qs_abi_version(void) { return QSB200_ABI_VERSION; }
+
+const char *qs_last_error(void) { return g_last_error.c_str(); }
+
+int qs_device_count(int *out) {
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *out = 0;
+        cudaGetLastError();
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    *out = n;
+    return QS_OK;
+}
+
+// new_state: pkg/src/pairsim/state.py:122-143
+int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out) {
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = nullptr;
+    if (num_qubits < 1) return set_error(QS_ERR_VALUE, "num_qubits must be >= 1");
+    if (num_qubits > 300)
+        return set_error(QS_ERR_CAPACITY, std::to_string(num_qubits) +
+                                              " qubits is past the supported limit of 300");
+    int ndev = 0;
+    QS_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_error(QS_ERR_VALUE, "device " + std::to_string(device) + " not present (" +
+                                           std::to_string(ndev) + " devices)");
+    DeviceGuard guard(device);
+    size_t free_b = 0, total_b = 0;
+    QS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    unsigned long long budget = memory_budget ? memory_budget : (unsigned long long)free_b * 3 / 4;
+    // need_bytes = memory_required // 8 = 8 * 2^n (state.py:71-83, 134)
+    if (num_qubits > 60 || (8ull << num_qubits) > budget) {
+        std::string need = num_qubits > 60 ? std::string("more than 2^63 bytes")
+                                           : format_bytes(8ull << num_qubits) + " (" +
+                                                 std::to_string(8ull << num_qubits) + " bytes)";
+        return set_error(QS_ERR_CAPACITY, std::to_string(num_qubits) + " qubits need " + need +
+                                              "; memory budget is " + format_bytes(budget));
+    }
+    qs_state *s = new qs_state();
+    std::memset(s, 0, sizeof *s);
+    s->num_qubits = num_qubits;
+    s->device = device;
+    cudaError_t e = cudaMalloc(&s->amps, 8ull << num_qubits);
+    if (e != cudaSuccess) {
+        delete s;
+        cudaGetLastError();
+        return set_error(QS_ERR_CAPACITY, std::string("cudaMalloc of ") +
+                                              std::to_string(8ull << num_qubits) +
+                                              " bytes failed: " + cudaGetErrorString(e));
+    }
+    e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        cudaFree(s->amps);
+        delete s;
+        return cuda_fail(e, "cudaStreamCreateWithFlags");
+    }
+    cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
+    int rc = launch_reset(s, 0);
+    if (rc != QS_OK) {
+        cudaStreamDestroy(s->stream);
+        cudaFree(s->amps);
+        delete s;
+        return rc;
+    }
+    *out = s;
+    return QS_OK;
+}
+
+int qs_destroy(qs_state *s) {
+    if (!s) return QS_OK;
+    DeviceGuard guard(s->device);
+    cudaStreamSynchronize(s->stream);
+    if (s->amps) cudaFree(s->amps);
+    if (s->scratch) cudaFree(s->scratch);
+    if (s->ops_dev) cudaFree(s->ops_dev);
+    if (s->pinned) cudaFreeHost(s->pinned);
+    cudaStreamDestroy(s->stream);
+    delete s;
+    return QS_OK;
+}
+
+int qs_num_qubits(const qs_state *s, int *out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = s->num_qubits;
+    return QS_OK;
+}
+
+int qs_device(const qs_state *s, int *out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = s->device;
+    return QS_OK;
+}
+
+int qs_device_pointer(qs_state *s, void **out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = s->amps;
+    return QS_OK;
+}
+
+int qs_stream(qs_state *s, void **out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = (void *)s->stream;
+    return QS_OK;
+}
+
+int qs_reset(qs_state *s, uint64_t basis) {
+    CHECK_HANDLE(s);
+    if (basis >> s->num_qubits)
+        return set_error(QS_ERR_INDEX, "basis index " + std::to_string(basis) +
+                                           " out of range [0, " +
+                                           std::to_string(1ull << s->num_qubits) + ")");
+    DeviceGuard guard(s->device);
+    return launch_reset(s, basis);
+}
+
+int qs_synchronize(qs_state *s) {
+    CHECK_HANDLE(s);
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaStreamSynchronize(s->stream));
+    QS_CUDA(cudaGetLastError());
+    return QS_OK;
+}
+
+// apply_gate: pkg/src/pairsim/kernel.py:108-132
+int qs_apply_gate(qs_state *s, int target, const float m[8]) {
+    CHECK_HANDLE(s);
+    if (!m) return set_error(QS_ERR_NULL, "null gate matrix");
+    int rc = check_qubit(s, target, "target");
+    if (rc) return rc;
+    DeviceGuard guard(s->device);
+    return launch_sweep(s, target, 0ull, m);
+}
+
+// apply_controlled_gate: pkg/src/pairsim/kernel.py:135-165 (same check order)
+int qs_apply_controlled_gate(qs_state *s, int control, int target, const float m[8]) {
+    CHECK_HANDLE(s);
+    if (!m) return set_error(QS_ERR_NULL, "null gate matrix");
+    int rc = check_qubit(s, target, "target");
+    if (rc) return rc;
+    rc = check_qubit(s, control, "control");
+    if (rc) return rc;
+    if (control == target) return set_error(QS_ERR_VALUE, "control and target must differ");
+    DeviceGuard guard(s->device);
+    return launch_sweep(s, target, 1ull << control, m);
+}
+
+int qs_apply_controlled_controlled_gate(qs_state *s, int c1, int c2, int target,
+                                        const float m[8]) {
+    CHECK_HANDLE(s);
+    if (!m) return set_error(QS_ERR_NULL, "null gate matrix");
+    int rc = check_qubit(s, target, "target");
+    if (rc) return rc;
+    rc = check_qubit(s, c1, "control");
+    if (rc) return rc;
+    rc = check_qubit(s, c2, "control");
+    if (rc) return rc;
+    if (c1 == target || c2 == target)
+        return set_error(QS_ERR_VALUE, "control and target must differ");
+    if (c1 == c2) return set_error(QS_ERR_VALUE, "the two controls must differ");
+    DeviceGuard guard(s->device);
+    return launch_sweep(s, target, (1ull << c1) | (1ull << c2), m);
+}
+
+int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops,
+                   int nops) {
+    CHECK_HANDLE(s);
+    if (nops == 0) return QS_OK;
+    if (!ops || !tile_qubits) return set_error(QS_ERR_NULL, "null op list or tile qubit list");
+    DeviceGuard guard(s->device);
+    return run_fused(s, tile_qubits, ntile, ops, nops);
+}
+
+int qs_swap_qubits(qs_state *s, int q1, int q2) {
+    CHECK_HANDLE(s);
+    int rc = check_qubit(s, q1, "qubit");
+    if (rc) return rc;
+    rc = check_qubit(s, q2, "qubit");
+    if (rc) return rc;
+    if (q1 == q2) return QS_OK;
+    DeviceGuard guard(s->device);
+    return launch_swap(s, q1 < q2 ? q1 : q2, q1 < q2 ? q2 : q1);
+}
+
+static int check_range(const qs_state *s, uint64_t offset, uint64_t count) {
+    uint64_t dim = 1ull << s->num_qubits;
+    if (offset > dim || count > dim - offset)
+        return set_error(QS_ERR_INDEX, "amplitude range [" + std::to_string(offset) + ", " +
+                                           std::to_string(offset + count) + ") out of range [0, " +
+                                           std::to_string(dim) + ")");
+    return QS_OK;
+}
+
+int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, float *host) {
+    CHECK_HANDLE(s);
+    int rc = check_range(s, offset, count);
+    if (rc) return rc;
+    if (count == 0) return QS_OK;
+    if (!host) return set_error(QS_ERR_NULL, "null host buffer");
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaMemcpyAsync(host, s->amps + offset, count * 8ull, cudaMemcpyDeviceToHost,
+                            s->stream));
+    QS_CUDA(cudaStreamSynchronize(s->stream));
+    return QS_OK;
+}
+
+int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const float *host) {
+    CHECK_HANDLE(s);
+    int rc = check_range(s, offset, count);
+    if (rc) return rc;
+    if (count == 0) return QS_OK;
+    if (!host) return set_error(QS_ERR_NULL, "null host buffer");
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaMemcpyAsync(s->amps + offset, host, count * 8ull, cudaMemcpyHostToDevice,
+                            s->stream));
+    // the caller may reuse `host` as soon as we return
+    QS_CUDA(cudaStreamSynchronize(s->stream));
+    return QS_OK;
+}
+
+int qs_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host) {
+    CHECK_HANDLE(s);
+    int rc = check_range(s, offset, count);
+    if (rc) return rc;
+    if (count == 0) return QS_OK;
+    if (!host) return set_error(QS_ERR_NULL, "null host buffer");
+    DeviceGuard guard(s->device);
+    return run_probabilities(s, offset, count, host);
+}
+
+int qs_norm_squared(qs_state *s, double *out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    DeviceGuard guard(s->device);
+    return run_norm(s, out);
+}
+
+// sample: pkg/src/pairsim/measure.py:76-85
+int qs_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
+    CHECK_HANDLE(s);
+    if (k < 1) return set_error(QS_ERR_VALUE, "n_samples must be >= 1");
+    if (!rng || !out) return set_error(QS_ERR_NULL, "null rng or output buffer");
+    DeviceGuard guard(s->device);
+    return run_sample(s, rng, k, out);
+}
+
+// measure_collapse: pkg/src/pairsim/measure.py:88-99
+int qs_measure_collapse(qs_state *s, const qs_pcg64 *rng, int64_t *outcome) {
+    CHECK_HANDLE(s);
+    if (!rng || !outcome) return set_error(QS_ERR_NULL, "null rng or output pointer");
+    DeviceGuard guard(s->device);
+    int64_t m = 0;
+    int rc = run_sample(s, rng, 1, &m);
+    if (rc) return rc;
+    rc = launch_reset(s, (uint64_t)m);
+    if (rc) return rc;
+    *outcome = m;
+    return QS_OK;
+}
+
+}  // extern "C"
