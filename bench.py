@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the gate-sweep hot path (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1): BASELINE config 2 — a 30-qubit register in HBM, one step =
+a Hadamard layer applied as 30 unfused single-qubit sweeps (targets 0..29),
+i.e. the per-gate HBM roofline configuration.  metric = single-qubit
+gates/s; each sweep moves 16 * 2^30 algorithmic bytes.  The register
+(8 GiB) is larger than L2 (126 MB), so no flush is needed between steps.
+
+N>1 (torchrun, one process per GPU): weak scaling — every rank holds an
+independent 30-qubit register and runs the same layer ("replicas"; the
+sharded 30+log2(N)-qubit register lives in paper_1805_00988_b200.sharded).
+
+--impl reference times the reference CPU path (oracle/port.py, the numpy
+restatement of pairsim's ThreadExecutor sweep; /root/reference is absent on
+the GPU box) on the host cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_QUBITS = 30
+METRIC = "single-qubit gates/sec (H-layer sweep, 30 qubits)"
+UNIT = "gates/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--qubits", type=int, default=N_QUBITS)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time fused layer / QFT")
+    return ap.parse_args()
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per sweep launch from the committed ncu --set full capture."""
+    for p in sorted((ROOT / "profiles").glob("ncu_sweep_*.json"), reverse=True):
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            continue
+    return None
+
+
+# ------------------------------------------------------------- CPU legs ----
+def cpu_sample(n: int, budget_s: float, threads: int):
+    """Time the numpy port of pairsim's sweep (oracle/port.py) on host cores.
+    Returns (gates, seconds, sample description)."""
+    from oracle import port
+    from paper_1805_00988_b200.gates import H
+
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 0
+    # the reference sweep peaks near 4.5x the state bytes
+    while n > 20 and 4.6 * (8 << n) > 0.8 * avail:
+        n -= 1
+    amps = np.zeros(1 << n, dtype=np.complex64)
+    amps[0] = 1
+    ex = port.Executor(workers=threads)
+    targets = [0, n - 1, n // 2, 3, n - 4, 7, n // 3, 11, 2 * n // 3, 1, 15, n - 2, 5, 19, 23, 27, 13, 9]
+    port.apply_gate(amps, n // 2, H, ex)  # warm-up
+    t0 = time.perf_counter()
+    gates = 0
+    while gates < 3 or (time.perf_counter() - t0 < budget_s and gates < len(targets)):
+        port.apply_gate(amps, targets[gates % len(targets)] % n, H, ex)
+        gates += 1
+    dt = time.perf_counter() - t0
+    ex.close()
+    return gates, dt, n
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    from oracle import port
+    from paper_1805_00988_b200.gates import H
+
+    n = args.qubits
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 0
+    while n > 20 and 4.6 * (8 << n) > 0.8 * avail:
+        n -= 1
+    amps = np.zeros(1 << n, dtype=np.complex64)
+    amps[0] = 1
+    ex = port.Executor(workers=threads)
+    per_step = 1  # one H sweep per step: a bounded sample of the 30-gate layer
+    for w in range(args.warmup):
+        port.apply_gate(amps, w % n, H, ex)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        for g in range(per_step):
+            port.apply_gate(amps, (s * per_step + g) % n, H, ex)
+    dt = time.perf_counter() - t0
+    ex.close()
+    gates = args.steps * per_step
+    value = gates / dt
+    sample = (f"{gates} H sweeps on a {n}-qubit complex64 register (targets 0..{gates - 1} mod {n}), "
+              f"numpy port of pairsim ThreadExecutor with {threads} workers")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64",
+        "data": "synthetic", "config": {"workload": "hlayer_sweep", "n_qubits": n, "gates_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------- GPU arm ----
+def run_ours(args):
+    import torch
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+        dist = None
+
+    from paper_1805_00988_b200 import State
+    from paper_1805_00988_b200.gates import H, m8
+    from paper_1805_00988_b200 import _native as N
+
+    n = args.qubits
+    st = State(n, device=local)
+    stream = torch.cuda.ExternalStream(st.stream(), device=torch.device("cuda", local))
+    L = N.lib()
+    h = st.handle
+    hm = m8(H)
+    hp = N.f32ptr(hm)
+
+    def layer():
+        for t in range(n):
+            N.check(L.qs_apply_gate(h, t, hp))
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        layer()
+    st.flush()
+    barrier()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps * n)]
+    step_start = torch.cuda.Event(enable_timing=True)
+    step_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        step_start.record(stream)
+        k = 0
+        for _ in range(args.steps):
+            for t in range(n):
+                evs[k][0].record(stream)
+                N.check(L.qs_apply_gate(h, t, hp))
+                evs[k][1].record(stream)
+                k += 1
+        step_end.record(stream)
+        st.flush()
+        barrier()
+    total_ms = step_start.elapsed_time(step_end)
+    launch_ms = [a.elapsed_time(b) for a, b in evs]
+    per_target = [statistics.mean(launch_ms[t::n]) for t in range(n)]
+    if dist is not None:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+
+    gates = args.steps * n * world
+    value = gates / (total_ms / 1e3)
+    bytes_per_launch = 16 * (1 << n)
+    avg_launch_s = statistics.mean(launch_ms) / 1e3
+    peak, peak_src = measured_peak_gbs()
+    achieved = bytes_per_launch / avg_launch_s / 1e9
+
+    extras = {}
+    if args.extras and rank == 0:
+        extras = run_extras(st, stream, n)
+
+    # ---- e2e through the C ABI with pinned host buffers -------------------
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(2 << n, dtype=torch.float32, pin_memory=True)
+        host[0] = 1.0
+        hptr = host.data_ptr()
+        k2 = max(1, min(args.steps, 3))
+        def e2e_step():
+            N.check(L.qs_set_amplitudes(h, 0, 1 << n, hptr))
+            layer()
+            N.check(L.qs_get_amplitudes(h, 0, 1 << n, hptr))
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            e2e_step()
+        barrier()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": k2 * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": 8 << n,
+               "d2h_bytes_per_step": 8 << n, "steps": k2,
+               "timing": "host wall clock around qs_set_amplitudes + 30 x qs_apply_gate + "
+                         "qs_get_amplitudes (pinned host buffers), max over ranks"}
+        del host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        g, dt, ncpu = cpu_sample(n, 20.0, threads)
+        cpu = {"value": g / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{g} H sweeps on a {ncpu}-qubit register, oracle/port.py (numpy restatement of "
+                         f"pairsim's ThreadExecutor sweep, kernel.py:108-132) with {threads} workers, "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": "hlayer_sweep_unfused", "n_qubits": n, "gates_per_step": n,
+                       "state_bytes": 8 << n, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "register (8 GiB) larger than L2; no flush needed"},
+            "gpu_launches": args.steps * n,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "k_sweep_high/k_sweep_low (unfused 1-qubit sweep)",
+                         "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
+                         "per_target_ms": [round(x, 4) for x in per_target]},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        if extras:
+            out["extras"] = extras
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_extras(st, stream, n):
+    """Fused H layer and a fused QFT on the same register (effective gates/s)."""
+    import torch
+
+    from paper_1805_00988_b200 import build_hadamard_layer, build_qft, fusion
+    from paper_1805_00988_b200.circuits import lower_ops
+
+    res = {}
+    for name, circ in (("hlayer_fused", build_hadamard_layer(n)), ("qft_fused", build_qft(n))):
+        passes = fusion.plan(n, lower_ops(circ))
+        fusion.run(st, passes)
+        st.flush()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a.record(stream)
+        for _ in range(reps):
+            fusion.run(st, passes)
+        b.record(stream)
+        st.flush()
+        ms = a.elapsed_time(b) / reps
+        res[name] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
+                     "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
+                     "pass_bytes": len(passes) * 16 * (1 << n),
+                     "achieved_GBps": len(passes) * 16 * (1 << n) / (ms / 1e3) / 1e9}
+    return res
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

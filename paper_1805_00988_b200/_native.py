@@ -1,0 +1,131 @@
+"""ctypes binding of libqsb200.so (include/qsb200.h).
+
+There is no CPU fallback: if the library is missing, or no CUDA device is
+visible, every operation raises.  The library is built in-tree by
+``python -m paper_1805_00988_b200.build`` (or __graft_entry__.build()).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+from .errors import CapacityError, DegenerateStateError, DeviceError
+
+LIB_PATH = Path(__file__).resolve().parent / "libqsb200.so"
+
+QS_OK, QS_ERR_INDEX, QS_ERR_VALUE, QS_ERR_CAPACITY, QS_ERR_DEGENERATE, QS_ERR_CUDA, QS_ERR_NULL = range(7)
+QS_OP_PAIR, QS_OP_PHASE = 0, 1
+
+# Every symbol include/qsb200.h declares (checked by tests/test_native_abi.py).
+EXPORTS = (
+    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_create", "qs_destroy",
+    "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
+    "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
+    "qs_apply_controlled_controlled_gate", "qs_apply_fused", "qs_swap_qubits",
+    "qs_get_amplitudes", "qs_set_amplitudes", "qs_probabilities", "qs_norm_squared",
+    "qs_sample", "qs_measure_collapse",
+)
+
+
+class qs_pcg64(ctypes.Structure):
+    _fields_ = [("state_hi", ctypes.c_uint64), ("state_lo", ctypes.c_uint64),
+                ("inc_hi", ctypes.c_uint64), ("inc_lo", ctypes.c_uint64)]
+
+
+class qs_op(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("target", ctypes.c_int32),
+                ("ctrl_mask", ctypes.c_uint64), ("m", ctypes.c_float * 8)]
+
+
+OP_DTYPE = np.dtype([("kind", np.int32), ("target", np.int32), ("ctrl_mask", np.uint64),
+                     ("m", np.float32, 8)])
+assert OP_DTYPE.itemsize == ctypes.sizeof(qs_op)
+
+_lib = None
+
+
+def _declare(L):
+    vp = ctypes.c_void_p
+    i32, u64, i64 = ctypes.c_int, ctypes.c_uint64, ctypes.c_int64
+    f32p = ctypes.POINTER(ctypes.c_float)
+    sig = {
+        "qs_abi_version": ([], i32),
+        "qs_last_error": ([], ctypes.c_char_p),
+        "qs_device_count": ([ctypes.POINTER(i32)], i32),
+        "qs_create": ([i32, i32, u64, ctypes.POINTER(vp)], i32),
+        "qs_destroy": ([vp], i32),
+        "qs_num_qubits": ([vp, ctypes.POINTER(i32)], i32),
+        "qs_device": ([vp, ctypes.POINTER(i32)], i32),
+        "qs_device_pointer": ([vp, ctypes.POINTER(vp)], i32),
+        "qs_stream": ([vp, ctypes.POINTER(vp)], i32),
+        "qs_reset": ([vp, u64], i32),
+        "qs_synchronize": ([vp], i32),
+        "qs_apply_gate": ([vp, i32, f32p], i32),
+        "qs_apply_controlled_gate": ([vp, i32, i32, f32p], i32),
+        "qs_apply_controlled_controlled_gate": ([vp, i32, i32, i32, f32p], i32),
+        "qs_apply_fused": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
+        "qs_swap_qubits": ([vp, i32, i32], i32),
+        "qs_get_amplitudes": ([vp, u64, u64, vp], i32),
+        "qs_set_amplitudes": ([vp, u64, u64, vp], i32),
+        "qs_probabilities": ([vp, u64, u64, vp], i32),
+        "qs_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
+        "qs_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),
+        "qs_measure_collapse": ([vp, ctypes.POINTER(qs_pcg64), ctypes.POINTER(i64)], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib():
+    """Load libqsb200.so (building it first if it is absent and nvcc exists)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            from . import build as _build
+
+            _build.build()
+        _lib = ctypes.CDLL(str(LIB_PATH))
+        _declare(_lib)
+    return _lib
+
+
+def last_error() -> str:
+    return lib().qs_last_error().decode(errors="replace")
+
+
+def check(rc: int) -> None:
+    if rc == QS_OK:
+        return
+    msg = last_error()
+    if rc == QS_ERR_INDEX:
+        raise IndexError(msg)
+    if rc in (QS_ERR_VALUE, QS_ERR_NULL):
+        raise ValueError(msg)
+    if rc == QS_ERR_CAPACITY:
+        raise CapacityError(msg)
+    if rc == QS_ERR_DEGENERATE:
+        raise DegenerateStateError(msg)
+    raise DeviceError(msg)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = lib().qs_device_count(ctypes.byref(n))
+    return n.value if rc == QS_OK else 0
+
+
+def pcg_from_seed(seed) -> qs_pcg64:
+    """numpy default_rng(seed)'s PCG64 state (the reference's draw source, measure.py:81)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m = (1 << 64) - 1
+    return qs_pcg64((s >> 64) & m, s & m, (inc >> 64) & m, inc & m)
+
+
+def f32ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))

@@ -1,0 +1,108 @@
+"""Pass planner: groups a gate sequence into fused HBM passes (qs_apply_fused).
+
+Each pass names a tile qubit set Q (|Q| = K, always containing qubits 0..5
+so every tile is made of 512-byte contiguous segments) and takes ops in
+circuit order while:
+
+* a PAIR op's target is in Q, or Q still has room to add it, and
+* a PHASE op (diagonal, a == 1, b == c == 0: u1/z/s/t and their controlled
+  forms) is always absorbable — it is an element-wise multiply with its
+  target/control bits as a predicate, wherever those bits live.
+
+Ops are never reordered, so the fused result is the same as the sequential
+one (kernel.py:244-245 barrier semantics preserved by construction).  A pass
+holding a single op is dispatched to the plain sweep kernels instead (the
+phase kernel touches fewer bytes than a full tile pass).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .gates import is_phase, m8
+
+LOW = 6
+
+
+@dataclass
+class Pass:
+    tile: list[int]
+    ops: list[tuple[int, int, int, np.ndarray]] = field(default_factory=list)  # (kind, target, ctrl_mask, m8)
+
+    def op_array(self) -> np.ndarray:
+        arr = np.zeros(len(self.ops), dtype=N.OP_DTYPE)
+        for i, (kind, t, cm, m) in enumerate(self.ops):
+            arr[i]["kind"] = kind
+            arr[i]["target"] = t
+            arr[i]["ctrl_mask"] = cm
+            arr[i]["m"] = m
+        return arr
+
+
+def lower(gate, target: int, controls=()) -> tuple[int, int, int, np.ndarray]:
+    m = m8(gate)
+    cm = 0
+    for c in controls:
+        cm |= 1 << int(c)
+    kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
+    return kind, int(target), cm, m
+
+
+def default_tile_qubits(num_qubits: int) -> int:
+    return min(13, num_qubits)
+
+
+def plan(num_qubits: int, ops, tile_qubits: int | None = None) -> list[Pass]:
+    """Greedy in-order grouping into passes of at most K tile qubits."""
+    n = num_qubits
+    K = tile_qubits or default_tile_qubits(n)
+    if n < 10 or K < 10:
+        return [Pass(list(range(n)), list(ops))] if ops else []
+    base = list(range(min(LOW, n)))
+    passes: list[Pass] = []
+    cur = Pass(list(base))
+    for op in ops:
+        kind, t = op[0], op[1]
+        if kind == N.QS_OP_PAIR and t not in cur.tile:
+            if len(cur.tile) >= K:
+                passes.append(cur)
+                cur = Pass(list(base))
+            cur.tile.append(t)
+        cur.ops.append(op)
+    if cur.ops:
+        passes.append(cur)
+    for p in passes:  # pad the tile to K qubits (extra qubits are free)
+        extra = [q for q in range(n - 1, -1, -1) if q not in p.tile]
+        p.tile.extend(extra[: max(0, K - len(p.tile))])
+        p.tile.sort()
+    return passes
+
+
+def run(state, passes: list[Pass]) -> None:
+    """Launch the planned passes on a State (asynchronous on its stream)."""
+    for p in passes:
+        if len(p.ops) == 1:
+            kind, t, cm, m = p.ops[0]
+            _single(state, kind, t, cm, m)
+        else:
+            state.apply_fused(p.tile, p.op_array())
+
+
+def _single(state, kind, t, cm, m) -> None:
+    """One op: the dedicated sweep kernels (the phase kernel for diagonal ops)."""
+    L = N.lib()
+    ctrls = [q for q in range(64) if (cm >> q) & 1]
+    mp = N.f32ptr(np.ascontiguousarray(m, dtype=np.float32))
+    if not ctrls:
+        N.check(L.qs_apply_gate(state.handle, t, mp))
+    elif len(ctrls) == 1:
+        N.check(L.qs_apply_controlled_gate(state.handle, ctrls[0], t, mp))
+    elif len(ctrls) == 2:
+        N.check(L.qs_apply_controlled_controlled_gate(state.handle, ctrls[0], ctrls[1], t, mp))
+    else:  # >2 controls: a one-op pass (the library dispatches it to the sweep kernel)
+        op = np.zeros(1, dtype=N.OP_DTYPE)
+        op[0]["kind"], op[0]["target"], op[0]["ctrl_mask"], op[0]["m"] = kind, t, cm, m
+        state.apply_fused([t], op)

@@ -1,0 +1,218 @@
+"""QCGPU-style register object: ``State(n)`` living in B200 HBM.
+
+API (north_star):
+    s = State(n)                        # |0...0>, complex64 in HBM
+    s.apply_gate(gate, target)
+    s.apply_controlled_gate(gate, control, target)
+    s.apply_controlled_controlled_gate(gate, c1, c2, target)
+    s.h(t) s.x(t) s.y(t) s.z(t) s.s(t) s.t(t) s.u1(t, theta)
+    s.cx(c, t) s.cu1(c, t, theta) s.ccx(c1, c2, t)  # control(s) first
+    s.amplitudes() -> complex64 ndarray
+    s.probabilities() -> float64 ndarray
+    s.measure(samples=1000, seed=None) -> {basis_index: count}
+    s.flush(); s.backend.queue.finish()  # device barrier
+
+Gate semantics are the reference's pair sweep (pkg/src/pairsim/kernel.py:108-165);
+every call is one asynchronous launch on the state's CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native as N
+from .gates import FIXED_GATES, Gate, m8, u1 as _u1
+
+
+class _Queue:
+    def __init__(self, state: "State"):
+        self._state = state
+
+    def finish(self) -> None:
+        self._state.flush()
+
+
+class _Backend:
+    """``state.backend.queue.finish()`` compatibility."""
+
+    def __init__(self, state: "State"):
+        self.queue = _Queue(state)
+
+
+class State:
+    def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None):
+        if not isinstance(num_qubits, (int, np.integer)):
+            raise TypeError("num_qubits must be an integer")
+        if num_qubits < 1:
+            raise ValueError("num_qubits must be >= 1")
+        self._h = ctypes.c_void_p()
+        N.check(N.lib().qs_create(int(num_qubits), int(device), int(memory_budget or 0),
+                                  ctypes.byref(self._h)))
+        self.num_qubits = int(num_qubits)
+        self.device = int(device)
+        self.backend = _Backend(self)
+
+    # -- lifecycle ------------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            N.lib().qs_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if not self._h.value:
+            raise ValueError("state has been closed")
+        return self._h
+
+    @property
+    def dim(self) -> int:
+        return 1 << self.num_qubits
+
+    def device_pointer(self) -> int:
+        p = ctypes.c_void_p()
+        N.check(N.lib().qs_device_pointer(self.handle, ctypes.byref(p)))
+        return p.value
+
+    def stream(self) -> int:
+        p = ctypes.c_void_p()
+        N.check(N.lib().qs_stream(self.handle, ctypes.byref(p)))
+        return p.value or 0
+
+    def flush(self) -> None:
+        N.check(N.lib().qs_synchronize(self.handle))
+
+    def reset(self, basis: int = 0) -> "State":
+        N.check(N.lib().qs_reset(self.handle, int(basis)))
+        return self
+
+    # -- gates ----------------------------------------------------------------
+    def apply_gate(self, gate, target: int) -> "State":
+        m = m8(gate)
+        N.check(N.lib().qs_apply_gate(self.handle, int(target), N.f32ptr(m)))
+        return self
+
+    def apply_controlled_gate(self, gate, control: int, target: int) -> "State":
+        m = m8(gate)
+        N.check(N.lib().qs_apply_controlled_gate(self.handle, int(control), int(target), N.f32ptr(m)))
+        return self
+
+    def apply_controlled_controlled_gate(self, gate, control1: int, control2: int, target: int) -> "State":
+        m = m8(gate)
+        N.check(N.lib().qs_apply_controlled_controlled_gate(
+            self.handle, int(control1), int(control2), int(target), N.f32ptr(m)))
+        return self
+
+    def apply_fused(self, tile_qubits, ops: np.ndarray) -> "State":
+        """One fused HBM pass (see fusion.py for the planner)."""
+        tq = np.ascontiguousarray(np.asarray(tile_qubits, dtype=np.int32))
+        ops = np.ascontiguousarray(ops, dtype=N.OP_DTYPE)
+        N.check(N.lib().qs_apply_fused(self.handle, tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       int(tq.size), ops.ctypes.data, int(ops.size)))
+        return self
+
+    def swap_qubits(self, q1: int, q2: int) -> "State":
+        N.check(N.lib().qs_swap_qubits(self.handle, int(q1), int(q2)))
+        return self
+
+    def h(self, t):
+        return self.apply_gate(FIXED_GATES["h"], t)
+
+    def x(self, t):
+        return self.apply_gate(FIXED_GATES["x"], t)
+
+    def y(self, t):
+        return self.apply_gate(FIXED_GATES["y"], t)
+
+    def z(self, t):
+        return self.apply_gate(FIXED_GATES["z"], t)
+
+    def s(self, t):
+        return self.apply_gate(FIXED_GATES["s"], t)
+
+    def t(self, t):
+        return self.apply_gate(FIXED_GATES["t"], t)
+
+    def u1(self, t, theta: float):
+        return self.apply_gate(_u1(theta), t)
+
+    def cx(self, control, target):
+        return self.apply_controlled_gate(FIXED_GATES["x"], control, target)
+
+    def cz(self, control, target):
+        return self.apply_controlled_gate(FIXED_GATES["z"], control, target)
+
+    def cu1(self, control, target, theta: float):
+        return self.apply_controlled_gate(_u1(theta), control, target)
+
+    def ccx(self, control1, control2, target):
+        return self.apply_controlled_controlled_gate(FIXED_GATES["x"], control1, control2, target)
+
+    # -- readout ----------------------------------------------------------------
+    def amplitudes(self, offset: int = 0, count: int | None = None) -> np.ndarray:
+        count = self.dim - offset if count is None else count
+        out = np.empty(count, dtype=np.complex64)
+        N.check(N.lib().qs_get_amplitudes(self.handle, int(offset), int(count), out.ctypes.data))
+        return out
+
+    def set_amplitudes(self, values, offset: int = 0) -> "State":
+        v = np.ascontiguousarray(np.asarray(values), dtype=np.complex64)
+        N.check(N.lib().qs_set_amplitudes(self.handle, int(offset), int(v.size), v.ctypes.data))
+        return self
+
+    def amplitude(self, index: int) -> complex:
+        if not 0 <= index < self.dim:
+            raise IndexError(f"basis index {index} out of range [0, {self.dim})")
+        return complex(self.amplitudes(index, 1)[0])
+
+    def probabilities(self, offset: int = 0, count: int | None = None) -> np.ndarray:
+        count = self.dim - offset if count is None else count
+        out = np.empty(count, dtype=np.float64)
+        N.check(N.lib().qs_probabilities(self.handle, int(offset), int(count), out.ctypes.data))
+        return out
+
+    def norm_squared(self) -> float:
+        v = ctypes.c_double()
+        N.check(N.lib().qs_norm_squared(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def sample_outcomes(self, samples: int, seed=None) -> np.ndarray:
+        """Per-draw outcomes, bit-exact with pairsim.measure.sample for the same seed."""
+        if samples < 1:
+            raise ValueError("n_samples must be >= 1")
+        out = np.empty(int(samples), dtype=np.int64)
+        rng = N.pcg_from_seed(seed)
+        N.check(N.lib().qs_sample(self.handle, ctypes.byref(rng), int(samples), out.ctypes.data))
+        return out
+
+    def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
+        """Non-destructive sampling: {basis index: count}."""
+        keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
+        return {int(k): int(c) for k, c in zip(keys, counts)}
+
+    def measure_bitstrings(self, samples: int = 1000, seed=None) -> dict[str, int]:
+        """Same draws keyed by the n-bit string (qubit n-1 first)."""
+        return {format(k, f"0{self.num_qubits}b"): c for k, c in self.measure(samples, seed).items()}
+
+    def measure_collapse(self, seed=None) -> int:
+        out = ctypes.c_int64()
+        rng = N.pcg_from_seed(seed)
+        N.check(N.lib().qs_measure_collapse(self.handle, ctypes.byref(rng), ctypes.byref(out)))
+        return int(out.value)
+
+    def __repr__(self) -> str:
+        return f"State(num_qubits={self.num_qubits}, device={self.device})"

@@ -1,0 +1,34 @@
+"""Launch exactly the kernels we want ncu to capture (run under ncu on the GPU box).
+
+    python scripts/profile_kernels.py [--n 30]
+
+Order of launches after warm-up (reset + one warm-up sweep per kind):
+  1. k_sweep_high  : H on target n-10 (two-stream path)
+  2. k_sweep_low   : H on target 3    (shuffle path)
+  3. k_phase       : cu1 on (n-1, 7)
+  4. k_fused       : first pass of the fused H layer (13 tile qubits)
+"""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_1805_00988_b200 import State, build_hadamard_layer, fusion, u1  # noqa: E402
+from paper_1805_00988_b200.circuits import lower_ops  # noqa: E402
+from paper_1805_00988_b200.gates import H  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=30)
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+n = a.n
+st = State(n)
+passes = fusion.plan(n, lower_ops(build_hadamard_layer(n)))
+for _ in range(a.reps):
+    st.apply_gate(H, n - 10)
+    st.apply_gate(H, 3)
+    st.apply_controlled_gate(u1(0.5), n - 1, 7)
+    st.apply_fused(passes[0].tile, passes[0].op_array())
+st.flush()
+print("profiled kernels launched", len(passes), "passes in the fused layer")
