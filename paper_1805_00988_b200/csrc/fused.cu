@@ -2,35 +2,49 @@
 //
 // A pass applies a run of gates with ONE read and ONE write of the register:
 // the 2^n amplitudes are cut into 2^(n-K) tiles of 2^K amplitudes, where the
-// K tile qubits Q = {0..5} + (K-6 chosen high qubits) are the qubits every
-// PAIR op of the pass targets.  Controls and phase bits may be anywhere
-// (outside Q they are a per-tile predicate), so diagonal gates such as the
-// QFT's controlled phases fuse into any pass.
+// K tile qubits Q = {0..5} + (K-6 chosen high qubits) hold every PAIR target
+// of the pass.  Controls and phase bits may be anywhere (outside Q they are a
+// per-tile predicate), so diagonal gates such as the QFT's controlled phases
+// fuse into any pass.
 //
 // Data movement per tile (a persistent CTA loops over tiles):
-//   HBM -> smem : cp.async.bulk (TMA engine, UBLKCP) of 2^(K-6) contiguous
-//                 512-B segments, completion on an mbarrier (expect_tx)
-//   smem <-> registers, one "stage" per 4-bit register window: each thread
-//                 holds 16 float4 (32 amplitudes).  Local qubit 0 is the
-//                 float4 half, local qubits 1..5 are the lane id (gates there
-//                 use __shfl_xor_sync), 4 high tile qubits are the register
-//                 index and the remaining K-10 are the warp id.  Lanes always
-//                 cover 512 contiguous bytes, so every shared-memory access is
-//                 bank-conflict free with a dense layout.
-//   smem -> HBM : cp.async.bulk store (bulk_group), drained before the next
-//                 tile's load reuses the buffer.
-// Two CTAs per SM overlap one tile's TMA traffic with the other's math.
+//   HBM -> smem : TMA tensor copies (cp.async.bulk.tensor.5d, UTMALDG) over a
+//                 per-pass 5-D tensor map: dim0 = the 64 contiguous amplitudes
+//                 of local qubits 0..5 (box 66: the 2 out-of-bounds elements
+//                 are zero-filled, giving one float4 of padding per 512-B
+//                 segment so both register layouts below are bank-conflict
+//                 free), dims 1-3 = three high tile qubits (size 2, stride
+//                 2^q * 8 B), dim4 = the 512-B row index.  2^(K-9) copies of
+//                 4.2 KB per tile, completion on an mbarrier (expect_tx).
+//   smem <-> registers, one "stage" per register layout; every thread holds
+//                 16 float4 = 32 amplitudes and every gate is applied inside a
+//                 thread (no shuffles):
+//                   LOW  stage: local qubit 0 = float4 half, 1..4 = register
+//                                index -> gates on qubits 0..4
+//                   HIGH stage: local qubit 0 = float4 half, 4 chosen qubits
+//                                >= 5 = register index -> gates on those
+//                 Lane / warp ids cover the remaining local qubits.
+//   smem -> HBM : the same tensor map, cp.async.bulk.tensor store (UTMASTG;
+//                 the padding elements are out of bounds and never written).
+// One CTA per SM, warp-specialised: a producer warp drives the TMA for a
+// double-buffered tile ring (load of tile i+1 and store of tile i-1 overlap
+// the math on tile i; full/done mbarriers hand buffers back and forth) and
+// 2^(K-5) compute threads run the register stages.
 //
 // Ops are applied in circuit order with the same per-pair arithmetic as the
-// unfused sweep (common.cuh), so a fused pass is bit-identical to the
-// sequence of single-gate sweeps up to the sign of zero results (real-valued
-// gates skip the products with a zero imaginary part; every nonzero value is
-// identical).
+// unfused sweep (common.cuh).  Gate-class specialisations (real entries,
+// H-like a==c & d==-b, X) drop only products that are exactly ±0 or exact
+// negations, so a fused pass equals the sequence of single-gate sweeps in
+// every value (the sign of a zero amplitude is the only freedom).
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -39,43 +53,58 @@ namespace qsb {
 
 namespace {
 
-constexpr int kLow = 6;     // local qubits 0..5 : float4 half + lane id
-constexpr int kRegBits = 4; // 16 float4 per thread
+constexpr int kLow = 6;      // local qubits 0..5 form one 512-B segment
+constexpr int kRegBits = 4;  // 16 float4 per thread
 constexpr int kMaxK = 14;
-constexpr int kMaxWarpBits = kMaxK - kLow - kRegBits;  // 4
+constexpr int kMaxWarpBits = kMaxK - 10;
 
-enum : int { kPair = 0, kPhase = 1 };
-enum : int { kTHalf = 0, kTLane = 1, kTReg = 2 };
+enum : int { kCplx = 0, kReal = 1, kHlike = 2, kSwap = 3 };
 
-// One op, lowered to the layout of the stage it runs in.
-struct FOp {
-    int kind;         // kPair / kPhase
-    int tclass;       // target class (pair): half / lane / reg
-    int tidx;         // lane bit index (0..4) or register bit index (0..3)
-    int real;         // all four entries real -> cheaper exact product
-    uint32_t half_need, lane_need, reg_need, warp_need;  // controls (+ phase bits)
-    uint64_t ext_need;                                   // global bits outside the tile
+// One op, lowered to the layout of the stage it runs in (48 bytes, staged
+// into shared memory once per CTA).
+struct __align__(16) FOp {
+    int variant;         // see kPhaseVariant
+    uint32_t reg_need;   // register-index bits that must be set (warp-uniform)
+    uint32_t tid_need;   // thread-id bits (lane | warp << 5) that must be set
+    uint32_t half_need;  // odd half only (control / phase bit on local qubit 0)
+    uint64_t ext_need;   // global qubits outside the tile that must be 1
+    uint64_t pad;
     float m[8];
 };
+// pair variants: ((slot + 1) * 4 + class) * 2 + has_need, slot -1 = half;
+// phase variants: kPhaseVariant + reg_need * 2 + half_need
+constexpr int kPhaseVariant = 40;
 
 struct FStage {
-    int rbit[kRegBits];       // local bit of register bit r (>= 6)
-    int wbit[kMaxWarpBits];   // local bit of warp bit w (>= 6)
+    int rf[kRegBits];      // f-bit (f = local >> 1) of register bit r
+    int lf[5];             // f-bit of lane bit i
+    int wf[kMaxWarpBits];  // f-bit of warp bit w
     int op_begin, op_end;
 };
 
-// The whole op table travels as the kernel parameter block (<= 32 KB since
-// CUDA 12.1), so consecutive passes need no host synchronisation.
-constexpr int kMaxOps = 352;
-constexpr int kMaxStages = 32;
-struct FParams {
-    int n, K, nwbits, nstages;
-    uint64_t ntiles;
-    uint64_t tile_mask;        // OR of 1 << qpos[i]
-    int qpos[kMaxK];           // global qubit of local bit i
-    FStage stages[kMaxStages];
-    FOp ops[kMaxOps];
+// Tile index -> global base: contiguous runs of non-tile qubits.
+constexpr int kMaxRuns = 16;
+struct Run {
+    int src, dst, len;
 };
+
+constexpr int kMaxOps = 320;
+constexpr int kNB = 3;  // tile buffers in the TMA ring
+constexpr int kMaxStages = 48;
+struct FParams {
+    CUtensorMap tmap;  // 64-B aligned, first member
+    int ncopies;       // TMA copies per tile (2^(K-9))
+    int crow[4];       // row-index bit of copy-index bit i
+    int n, K, nwbits, nstages, nruns, nops;
+    int dry;  // QSB_FUSED_DRY=1: move the tiles, skip the math (ring probe)
+    uint64_t ntiles;
+    int qpos[kMaxK];  // global qubit of local bit i
+    Run runs[kMaxRuns];
+    FStage stages[kMaxStages];
+    FOp ops[kMaxOps];  // copied to shared memory once per CTA
+};
+// The whole table travels as the kernel parameter block (<= 32764 bytes since
+// CUDA 12.1), so consecutive passes need no host synchronisation.
 static_assert(sizeof(FParams) < 32000, "kernel parameter block too large");
 
 // ---- PTX wrappers -----------------------------------------------------------
@@ -90,17 +119,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+// try_wait suspends in hardware between polls; after ~2^22 failed polls (far
+// beyond any legitimate TMA latency) the kernel traps instead of hanging.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t addr = smem_u32(bar);
-    asm volatile(
-        "{\n"
-        ".reg .pred P;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        "@!P bra WAIT_%=;\n"
-        "}\n" ::"r"(addr),
-        "r"(parity)
-        : "memory");
+    const uint32_t addr = smem_u32(bar);
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (spins > (1u << 22)) __trap();
+    }
 }
 __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes,
                                           uint64_t *bar) {
@@ -120,6 +156,20 @@ __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_5d(void *smem_dst, const CUtensorMap *map, int row,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %2, %2, %2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(0), "r"(row), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, int row, const void *smem_src) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %1, %1, %1, %2}], [%3];" ::"l"(map),
+        "r"(0), "r"(row), "r"(smem_u32(smem_src))
+        : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -127,229 +177,334 @@ __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// ---- exact products ---------------------------------------------------------
-// For a real entry g (g.im == 0): fma(g.re, v.re, -rn(0*v.im)) == rn(g.re*v.re)
-// and fma(g.re, v.im, rn(0*v.re)) == rn(g.re*v.im) for every nonzero result.
+// ---- exact pair updates per gate class ----------------------------------------
+// real entry g (g.im == 0): fma(g, v.re, -rn(0*v.im)) == rn(g*v.re) and
+// fma(g, v.im, rn(0*v.re)) == rn(g*v.im) for every nonzero result.
 __device__ __forceinline__ float2 rmul(float g, float2 v) {
     return make_float2(__fmul_rn(g, v.x), __fmul_rn(g, v.y));
 }
-__device__ __forceinline__ void pair_real(const float *m, float2 &va, float2 &vb) {
-    float2 na = cadd(rmul(m[0], va), rmul(m[2], vb));
-    float2 nb = cadd(rmul(m[6], vb), rmul(m[4], va));
-    va = na;
-    vb = nb;
+__device__ __forceinline__ float2 csub(float2 x, float2 y) {
+    return make_float2(__fsub_rn(x.x, y.x), __fsub_rn(x.y, y.y));
 }
-__device__ __forceinline__ void pair_any(const FOp &op, float2 &va, float2 &vb) {
-    if (op.real) {
-        pair_real(op.m, va, vb);
-    } else {
-        Gate2 g = gate_from(op.m);
-        pair_update(g, va, vb);
+
+template <int CLS>
+__device__ __forceinline__ void pair_cls(const float *m, float2 &va, float2 &vb) {
+    if (CLS == kCplx) {
+        float2 na = cadd(cmul(make_float2(m[0], m[1]), va), cmul(make_float2(m[2], m[3]), vb));
+        float2 nb = cadd(cmul(make_float2(m[6], m[7]), vb), cmul(make_float2(m[4], m[5]), va));
+        va = na;
+        vb = nb;
+    } else if (CLS == kReal) {
+        float2 na = cadd(rmul(m[0], va), rmul(m[2], vb));
+        float2 nb = cadd(rmul(m[6], vb), rmul(m[4], va));
+        va = na;
+        vb = nb;
+    } else if (CLS == kHlike) {
+        // c == a, d == -b: c*va == a*va and d*vb == -(b*vb) exactly
+        float2 p = rmul(m[0], va), q = rmul(m[2], vb);
+        va = cadd(p, q);
+        vb = csub(p, q);
+    } else {  // X: a == d == 0, b == c == 1 -> values swap
+        float2 t = va;
+        va = vb;
+        vb = t;
     }
-}
-__device__ __forceinline__ float2 lin_any(const FOp &op, bool hi, float2 own, float2 partner) {
-    // bit-clear side: a*own + b*partner ; bit-set side: d*own + c*partner
-    const float *g1 = hi ? op.m + 6 : op.m + 0;
-    const float *g2 = hi ? op.m + 4 : op.m + 2;
-    if (op.real) return cadd(rmul(g1[0], own), rmul(g2[0], partner));
-    return cadd(cmul(make_float2(g1[0], g1[1]), own), cmul(make_float2(g2[0], g2[1]), partner));
 }
 
 __device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
 __device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
 __device__ __forceinline__ float4 mk4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
 
-template <int R>
-__device__ __forceinline__ void op_reg(const FOp &op, float4 (&v)[16], bool thread_ok) {
+// T = register bit of the target (-1: the float4 half, local qubit 0);
+// NEED: the op has a control / phase bit on the register index or the half
+// (per-j warp-uniform tests); !NEED is the straight-line common case.
+template <int T, int CLS, bool NEED>
+__device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[16]) {
+    const uint32_t need = NEED ? op.reg_need : 0u;
+    const bool odd_only = NEED && op.half_need != 0;
+    float m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = (CLS == kSwap) ? 0.f : op.m[i];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        if (j & (1 << R)) continue;
-        const int k = j | (1 << R);
-        if (!thread_ok || (j & op.reg_need) != op.reg_need) continue;
-        float2 a0 = lo2(v[j]), a1 = hi2(v[j]), b0 = lo2(v[k]), b1 = hi2(v[k]);
-        if (!op.half_need) pair_any(op, a0, b0);
-        pair_any(op, a1, b1);
-        v[j] = mk4(a0, a1);
-        v[k] = mk4(b0, b1);
+        if (T >= 0 && (j & (1 << T))) continue;
+        if (NEED && (j & need) != need) continue;  // warp-uniform
+        if (T < 0) {
+            float2 a = lo2(v[j]), b = hi2(v[j]);
+            pair_cls<CLS>(m, a, b);
+            v[j] = mk4(a, b);
+        } else {
+            const int k = j | (1 << (T < 0 ? 0 : T));
+            float2 a0 = lo2(v[j]), a1 = hi2(v[j]), b0 = lo2(v[k]), b1 = hi2(v[k]);
+            if (!odd_only) pair_cls<CLS>(m, a0, b0);
+            pair_cls<CLS>(m, a1, b1);
+            v[j] = mk4(a0, a1);
+            v[k] = mk4(b0, b1);
+        }
     }
 }
 
-template <int B>
-__device__ __forceinline__ void op_lane(const FOp &op, float4 (&v)[16], bool thread_ok, int lane) {
-    const bool hi = (lane >> B) & 1;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        float4 y;
-        y.x = __shfl_xor_sync(0xffffffffu, v[j].x, 1 << B);
-        y.y = __shfl_xor_sync(0xffffffffu, v[j].y, 1 << B);
-        y.z = __shfl_xor_sync(0xffffffffu, v[j].z, 1 << B);
-        y.w = __shfl_xor_sync(0xffffffffu, v[j].w, 1 << B);
-        if (!thread_ok || (j & op.reg_need) != op.reg_need) continue;
-        float2 o0 = lo2(v[j]), o1 = hi2(v[j]);
-        if (!op.half_need) o0 = lin_any(op, hi, o0, lo2(y));
-        o1 = lin_any(op, hi, o1, hi2(y));
-        v[j] = mk4(o0, o1);
-    }
-}
-
-__device__ __forceinline__ void op_half(const FOp &op, float4 (&v)[16], bool thread_ok) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (!thread_ok || (j & op.reg_need) != op.reg_need) continue;
-        float2 a = lo2(v[j]), b = hi2(v[j]);
-        pair_any(op, a, b);
-        v[j] = mk4(a, b);
-    }
-}
-
-__device__ __forceinline__ void op_phase(const FOp &op, float4 (&v)[16], bool thread_ok) {
+// Diagonal op: multiply the registers whose index has every bit of RNEED set
+// (compile-time pattern) by d; ODD: only the odd half (phase bit on local 0).
+template <int RNEED, bool ODD>
+__device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[16]) {
     const float2 d = make_float2(op.m[6], op.m[7]);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        if (!thread_ok || (j & op.reg_need) != op.reg_need) continue;
+        if ((j & RNEED) != RNEED) continue;
         float2 a = lo2(v[j]), b = hi2(v[j]);
-        if (!op.half_need) a = cmul(d, a);
+        if (!ODD) a = cmul(d, a);
         b = cmul(d, b);
         v[j] = mk4(a, b);
     }
 }
 
-__device__ __forceinline__ uint64_t scatter_bits(uint64_t x, const int *pos, int npos) {
+// Classes with a straight-line (no per-j test) body; the complex and swap
+// bodies keep the per-j branch, which bounds ptxas' register demand there.
+__device__ constexpr bool kStraight[4] = {false, true, true, false};
+
+__device__ __forceinline__ void apply_op(const FOp &op, float4 (&v)[16]) {
+    switch (op.variant) {
+#define QSB_CASE(T, C)                                                              \
+    case (((T) + 1) * 4 + (C)) * 2 + 0: apply_pair<(T), (C), !kStraight[C]>(op, v); break; \
+    case (((T) + 1) * 4 + (C)) * 2 + 1: apply_pair<(T), (C), true>(op, v); break;
+#define QSB_CASES(T) QSB_CASE(T, 0) QSB_CASE(T, 1) QSB_CASE(T, 2) QSB_CASE(T, 3)
+        QSB_CASES(-1)
+        QSB_CASES(0)
+        QSB_CASES(1)
+        QSB_CASES(2)
+        QSB_CASES(3)
+#undef QSB_CASES
+#undef QSB_CASE
+#define QSB_PH(R)                                                   \
+    case kPhaseVariant + (R) * 2 + 0: apply_phase<(R), false>(op, v); break; \
+    case kPhaseVariant + (R) * 2 + 1: apply_phase<(R), true>(op, v); break;
+        QSB_PH(0) QSB_PH(1) QSB_PH(2) QSB_PH(3) QSB_PH(4) QSB_PH(5) QSB_PH(6) QSB_PH(7)
+        QSB_PH(8) QSB_PH(9) QSB_PH(10) QSB_PH(11) QSB_PH(12) QSB_PH(13) QSB_PH(14) QSB_PH(15)
+#undef QSB_PH
+        default: break;
+    }
+}
+
+__device__ __forceinline__ uint64_t tile_base(uint64_t t, const FParams &p) {
     uint64_t r = 0;
-    for (int i = 0; i < npos; ++i) r |= ((x >> i) & 1ull) << pos[i];
+    for (int i = 0; i < p.nruns; ++i)
+        r |= ((t >> p.runs[i].src) & ((1ull << p.runs[i].len) - 1ull)) << p.runs[i].dst;
     return r;
 }
 
-// global index of tile t: its bits go to the non-tile qubits, in order
-__device__ __forceinline__ uint64_t tile_base(uint64_t t, int n, uint64_t tile_mask) {
-    uint64_t r = 0;
-    int k = 0;
-    for (int q = 0; q < n; ++q)
-        if (!((tile_mask >> q) & 1ull)) r |= ((t >> k++) & 1ull) << q;
-    return r;
+__device__ __forceinline__ uint32_t padded(uint32_t f) { return f + (f >> 5); }
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 template <int K>
-__global__ void __launch_bounds__(1 << (K - 5), (K >= 14 ? 1 : 2))
+__global__ void __maxnreg__(128)
     k_fused(float4 *__restrict__ amps, const __grid_constant__ FParams p) {
-    constexpr int kThreads = 1 << (K - 5);
-    constexpr int kF4 = 1 << (K - 1);               // float4 per tile
-    constexpr int kSegs = 1 << (K - kLow);          // 512-B segments per tile
-    constexpr uint32_t kTileBytes = kF4 * 16u;
-    extern __shared__ __align__(128) float4 tile[];
-    __shared__ uint64_t bar;
+    constexpr int kCompute = 1 << (K - 5);        // compute threads
+    constexpr int kSegs = 1 << (K - kLow);        // 512-B segments per tile
+    constexpr int kBufF4 = kSegs * 33;            // padded float4 per buffer
+    extern __shared__ __align__(128) float4 smem[];
+    float4 *buf0 = smem;
+    FOp *sops = (FOp *)(smem + kNB * kBufF4);
+    __shared__ uint64_t full[kNB], done[kNB];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        for (int b = 0; b < kNB; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&done[b], 1);
+        }
         fence_mbar_init();
+    }
+    {  // stage the op table in shared memory
+        const int4 *src = (const int4 *)p.ops;
+        int4 *dst = (int4 *)sops;
+        const int words = p.nops * (int)(sizeof(FOp) / 16);
+        for (int i = tid; i < words; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
 
-    // segment h of tile t starts at global amplitude base | scatter(h, qpos[6..])
-    const bool issuer = warp == 0;
-    uint32_t parity = 0;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t base = tile_base(t, p.n, p.tile_mask);
-        if (issuer) {
-            bulk_wait_read0();  // previous tile's stores have drained this buffer
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&bar, kTileBytes);
-            __syncwarp();
-            for (int h = lane; h < kSegs; h += 32) {
-                const uint64_t g = base | scatter_bits((uint64_t)h, p.qpos + kLow, K - kLow);
-                bulk_load(tile + ((size_t)h << (kLow - 1)), amps + (g >> 1), 512u, &bar);
-            }
-        }
-        mbar_wait(&bar, parity);
-        parity ^= 1u;
-
-        for (int s = 0; s < p.nstages; ++s) {
-            const FStage st = p.stages[s];
-            // float4 index of register slot j: lane | warp bits | register bits
-            uint32_t fbase = (uint32_t)lane;
-            for (int i = 0; i < p.nwbits; ++i)
-                fbase |= (uint32_t)((warp >> i) & 1) << (st.wbit[i] - 1);
-            uint32_t rs[kRegBits];
-#pragma unroll
-            for (int r = 0; r < kRegBits; ++r) rs[r] = 1u << (st.rbit[r] - 1);
-            float4 v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                uint32_t f = fbase;
-#pragma unroll
-                for (int r = 0; r < kRegBits; ++r)
-                    if (j & (1 << r)) f |= rs[r];
-                v[j] = tile[f];
-            }
-            for (int o = st.op_begin; o < st.op_end; ++o) {
-                const FOp op = p.ops[o];
-                const bool ok = ((uint32_t)lane & op.lane_need) == op.lane_need &&
-                                ((uint32_t)warp & op.warp_need) == op.warp_need &&
-                                (base & op.ext_need) == op.ext_need;
-                if (op.kind == kPhase) {
-                    op_phase(op, v, ok);
-                } else if (op.tclass == kTHalf) {
-                    op_half(op, v, ok);
-                } else if (op.tclass == kTLane) {
-                    switch (op.tidx) {
-                        case 0: op_lane<0>(op, v, ok, lane); break;
-                        case 1: op_lane<1>(op, v, ok, lane); break;
-                        case 2: op_lane<2>(op, v, ok, lane); break;
-                        case 3: op_lane<3>(op, v, ok, lane); break;
-                        default: op_lane<4>(op, v, ok, lane); break;
-                    }
-                } else {
-                    switch (op.tidx) {
-                        case 0: op_reg<0>(op, v, ok); break;
-                        case 1: op_reg<1>(op, v, ok); break;
-                        case 2: op_reg<2>(op, v, ok); break;
-                        default: op_reg<3>(op, v, ok); break;
-                    }
+    if (warp == kCompute / 32) {
+        // ---------------- producer warp: TMA loads and stores ----------------
+        const CUtensorMap *map = &p.tmap;
+        constexpr int kCopyF4 = 8 * 33;  // one 5-D box: 8 padded segments
+        constexpr uint32_t kBoxBytes = 8u * 66u * 8u;
+        uint64_t pending[kNB];
+        int i = 0;
+        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+            const int b = i % kNB;
+            float4 *buf = buf0 + b * kBufF4;
+            if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
+                mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
+                const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
+                for (int c = lane; c < p.ncopies; c += 32) {
+                    uint32_t row = row0;
+                    for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
+                    tma_store_5d(map, (int)row, buf + c * kCopyF4);
                 }
+                bulk_commit();
+                bulk_wait_read0();  // buffer b may be overwritten
+                __syncwarp();
             }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                uint32_t f = fbase;
-#pragma unroll
-                for (int r = 0; r < kRegBits; ++r)
-                    if (j & (1 << r)) f |= rs[r];
-                tile[f] = v[j];
+            const uint64_t base = tile_base(t, p);
+            pending[b] = base;
+            if (lane == 0) mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
+            __syncwarp();
+            const uint32_t row0 = (uint32_t)(base >> kLow);
+            for (int c = lane; c < p.ncopies; c += 32) {
+                uint32_t row = row0;
+                for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
+                tma_load_5d(buf + c * kCopyF4, map, (int)row, &full[b]);
             }
-            __syncthreads();
         }
-
-        fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
-        __syncthreads();
-        if (issuer) {
-            for (int h = lane; h < kSegs; h += 32) {
-                const uint64_t g = base | scatter_bits((uint64_t)h, p.qpos + kLow, K - kLow);
-                bulk_store(amps + (g >> 1), tile + ((size_t)h << (kLow - 1)), 512u);
+        // drain the last (up to) kNB tiles
+        for (int k = (i >= kNB ? i - kNB : 0); k < i; ++k) {
+            const int b = k % kNB;
+            mbar_wait(&done[b], (k / kNB) & 1);
+            const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
+            for (int c = lane; c < p.ncopies; c += 32) {
+                uint32_t row = row0;
+                for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
+                tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4);
             }
             bulk_commit();
         }
+        bulk_wait0();
+        return;
     }
-    if (issuer) bulk_wait0();
-    (void)kThreads;
+
+    // -------------------- compute warps: register stages --------------------
+    int i = 0;
+    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+        const int b = i % kNB;
+        float4 *tile = buf0 + b * kBufF4;
+        const uint64_t base = tile_base(t, p);
+        mbar_wait(&full[b], (i / kNB) & 1);
+        for (int s = 0; s < p.nstages; ++s) {
+            const FStage &st = p.stages[s];
+            uint32_t fb = 0;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) fb |= (uint32_t)((lane >> q) & 1) << st.lf[q];
+            for (int q = 0; q < p.nwbits; ++q) fb |= (uint32_t)((warp >> q) & 1) << st.wf[q];
+            const uint32_t pb = padded(fb);
+            uint32_t rs[kRegBits];
+#pragma unroll
+            for (int r = 0; r < kRegBits; ++r) rs[r] = padded(1u << st.rf[r]);
+            float4 v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                uint32_t a = pb;
+#pragma unroll
+                for (int r = 0; r < kRegBits; ++r)
+                    if (j & (1 << r)) a += rs[r];
+                v[j] = tile[a];
+            }
+            for (int o = st.op_begin; o < st.op_end; ++o) {
+                const FOp &op = sops[o];
+                const int4 hdr = *reinterpret_cast<const int4 *>(&op);  // one LDS.128
+                const uint64_t ext = op.ext_need;
+                const bool ok = ((uint32_t)tid & (uint32_t)hdr.z) == (uint32_t)hdr.z &&
+                                (base & ext) == ext;
+                if (ok && !p.dry) apply_op(op, v);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                uint32_t a = pb;
+#pragma unroll
+                for (int r = 0; r < kRegBits; ++r)
+                    if (j & (1 << r)) a += rs[r];
+                tile[a] = v[j];
+            }
+            if (s + 1 < p.nstages) named_sync(1, kCompute);
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+        named_sync(1, kCompute);
+        if (tid == 0) mbar_arrive(&done[b]);
+    }
 }
 
 template <int K>
 int launch_fused_k(qs_state *s, const FParams &p) {
-    const size_t smem = (size_t)(1u << (K - 1)) * 16u;
-    static bool configured = false;
-    if (!configured) {
+    const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
+    const size_t smem = bufs + (size_t)p.nops * sizeof(FOp);
+    static int configured = -1;
+    if (configured < (int)smem) {
         QS_CUDA(cudaFuncSetAttribute(k_fused<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        configured = true;
+                                     (int)(bufs + kMaxOps * sizeof(FOp))));
+        configured = (int)(bufs + kMaxOps * sizeof(FOp));
     }
-    uint64_t grid = (uint64_t)s->num_sms * 2;
+    uint64_t grid = (uint64_t)s->num_sms;
     if (grid > p.ntiles) grid = p.ntiles;
-    k_fused<K><<<(unsigned)grid, 1 << (K - 5), smem, s->stream>>>((float4 *)s->amps, p);
+    k_fused<K><<<(unsigned)grid, (1 << (K - 5)) + 32, smem, s->stream>>>((float4 *)s->amps, p);
     QS_CUDA(cudaGetLastError());
     return QS_OK;
 }
 
-bool is_real(const float m[8]) { return m[1] == 0.f && m[3] == 0.f && m[5] == 0.f && m[7] == 0.f; }
+int gate_class(const float m[8]) {
+    const bool real = m[1] == 0.f && m[3] == 0.f && m[5] == 0.f && m[7] == 0.f;
+    if (!real) return kCplx;
+    if (m[0] == 0.f && m[6] == 0.f && m[2] == 1.f && m[4] == 1.f) return kSwap;
+    if (m[4] == m[0] && m[6] == -m[2]) return kHlike;
+    return kReal;
+}
+
+// register layouts (f = local bit - 1; f has K-1 bits)
+//   LOW : regs f0..f3, lanes (f5, f6, f7, f4, f8), warps f9..
+//   HIGH: regs = 4 chosen f-bits >= 4, lanes (f0, f1, f2, f3, x), warps = rest
+FStage make_low_stage(int K) {
+    FStage st;
+    std::memset(&st, 0, sizeof st);
+    for (int r = 0; r < kRegBits; ++r) st.rf[r] = r;
+    const int lanes[5] = {5, 6, 7, 4, 8};
+    for (int i = 0; i < 5; ++i) st.lf[i] = lanes[i];
+    for (int w = 0; w < K - 10; ++w) st.wf[w] = 9 + w;
+    return st;
+}
+
+FStage make_high_stage(int K, const std::vector<int> &rbits_f) {
+    FStage st;
+    std::memset(&st, 0, sizeof st);
+    for (int r = 0; r < kRegBits; ++r) st.rf[r] = rbits_f[r];
+    std::vector<int> rest;
+    for (int f = 4; f < K - 1; ++f)
+        if (std::find(rbits_f.begin(), rbits_f.end(), f) == rbits_f.end()) rest.push_back(f);
+    for (int i = 0; i < 4; ++i) st.lf[i] = i;
+    st.lf[4] = rest[0];
+    for (int w = 0; w < K - 10; ++w) st.wf[w] = rest[1 + w];
+    return st;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link dependency, so the library still loads on a GPU-less build host).
+int encode_tile_map(qs_state *s, FParams &p) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        QS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn)
+            return set_error(QS_ERR_CUDA, "cuTensorMapEncodeTiled entry point not available");
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[5] = {64, 2, 2, 2, 1ull << (p.n - kLow)};
+    const cuuint64_t strides[4] = {8ull << p.qpos[kLow], 8ull << p.qpos[kLow + 1],
+                                   8ull << p.qpos[kLow + 2], 512ull};
+    const cuuint32_t box[5] = {66, 2, 2, 2, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)s->amps, dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return set_error(QS_ERR_CUDA, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
+    p.ncopies = 1 << (p.K - kLow - 3);
+    for (int k = 0; k < 4; ++k) p.crow[k] = (kLow + 3 + k < p.K) ? p.qpos[kLow + 3 + k] - kLow : 0;
+    return QS_OK;
+}
 
 }  // namespace
 
@@ -380,10 +535,10 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     }
     const int K = __builtin_popcountll(tile_mask);
     const uint64_t low_mask = (1ull << kLow) - 1ull;
-    const bool kernel_ok = n >= 10 && K >= 10 && K <= kMaxK && (tile_mask & low_mask) == low_mask;
+    const bool kernel_ok = n >= 10 && K >= 10 && K <= 13 && (tile_mask & low_mask) == low_mask;
     if (!kernel_ok) {
-        // Registers below 10 qubits (or an unsupported tile shape): apply the
-        // ops one sweep at a time — the same arithmetic, one pass per op.
+        // Registers below 10 qubits (or an unsupported tile shape): one sweep
+        // per op — the same arithmetic, one HBM pass per op.
         for (int i = 0; i < nops; ++i) {
             const qs_op &op = ops[i];
             int rc = op.kind == QS_OP_PHASE
@@ -399,9 +554,12 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     std::memset(&p, 0, sizeof p);
     p.n = n;
     p.K = K;
-    p.nwbits = K - kLow - kRegBits;
+    p.nwbits = K - 10;
     p.ntiles = 1ull << (n - K);
-    p.tile_mask = tile_mask;
+    {
+        const char *d = std::getenv("QSB_FUSED_DRY");
+        p.dry = d && *d == '1';
+    }
     int local_of[64];
     for (int q = 0, i = 0; q < n; ++q) {
         local_of[q] = -1;
@@ -410,97 +568,127 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
             local_of[q] = i++;
         }
     }
+    {
+        int rc = encode_tile_map(s, p);
+        if (rc) return rc;
+    }
+    // tile index bits fill the non-tile qubits in order, as contiguous runs
+    for (int q = 0, src = 0; q < n;) {
+        if ((tile_mask >> q) & 1ull) {
+            ++q;
+            continue;
+        }
+        int len = 0;
+        while (q + len < n && !((tile_mask >> (q + len)) & 1ull)) ++len;
+        if (p.nruns == kMaxRuns) return set_error(QS_ERR_VALUE, "tile qubit set too fragmented");
+        p.runs[p.nruns++] = Run{src, q, len};
+        src += len;
+        q += len;
+    }
 
-    // ---- stage planning: each stage holds 4 high local bits in registers ----
+    // ---- stage planning -----------------------------------------------------
+    // need: 0 = any stage (phase op / target on local qubit 0), 1 = LOW
+    // (target on local 1..4), 2 = HIGH holding the target's f-bit
+    auto need_of = [&](const qs_op &op, int *fbit) -> int {
+        if (op.kind != QS_OP_PAIR) return 0;
+        const int lb = local_of[op.target];
+        if (lb == 0) return 0;
+        if (lb <= 4) return 1;
+        *fbit = lb - 1;
+        return 2;
+    };
     std::vector<FStage> stages;
     std::vector<FOp> fops;
-    const int nhigh = K - kLow;
-    auto high_target = [&](const qs_op &op) -> int {
-        if (op.kind != QS_OP_PAIR) return -1;
-        int lb = local_of[op.target];
-        return lb >= kLow ? lb : -1;
-    };
     int i = 0;
     while (i < nops) {
-        // choose the register window: the next distinct high targets, in order
-        std::vector<int> rbits;
-        for (int j = i; j < nops && (int)rbits.size() < kRegBits; ++j) {
-            int hb = high_target(ops[j]);
-            if (hb >= 0 && std::find(rbits.begin(), rbits.end(), hb) == rbits.end())
-                rbits.push_back(hb);
-        }
-        for (int b = kLow; b < K && (int)rbits.size() < kRegBits; ++b)
-            if (std::find(rbits.begin(), rbits.end(), b) == rbits.end()) rbits.push_back(b);
-        std::sort(rbits.begin(), rbits.end());
-        FStage st;
-        std::memset(&st, 0, sizeof st);
-        int rpos_of[kMaxK], wpos_of[kMaxK];
-        for (int b = 0; b < kMaxK; ++b) rpos_of[b] = wpos_of[b] = -1;
-        for (int r = 0; r < kRegBits; ++r) {
-            st.rbit[r] = rbits[r];
-            rpos_of[rbits[r]] = r;
-        }
-        for (int b = kLow, w = 0; b < K; ++b)
-            if (rpos_of[b] < 0) {
-                st.wbit[w] = b;
-                wpos_of[b] = w++;
+        // the layout follows the first op that constrains it
+        int kind = 1;
+        for (int j = i; j < nops; ++j) {
+            int f = -1, nd = need_of(ops[j], &f);
+            if (nd) {
+                kind = nd;
+                break;
             }
+        }
+        FStage st;
+        if (kind == 1) {
+            st = make_low_stage(K);
+        } else {
+            std::vector<int> rb;
+            for (int j = i; j < nops && (int)rb.size() < kRegBits; ++j) {
+                int f = -1, nd = need_of(ops[j], &f);
+                if (nd == 1) break;
+                if (nd == 2 && std::find(rb.begin(), rb.end(), f) == rb.end()) rb.push_back(f);
+            }
+            for (int f = 4; f < K - 1 && (int)rb.size() < kRegBits; ++f)
+                if (std::find(rb.begin(), rb.end(), f) == rb.end()) rb.push_back(f);
+            std::sort(rb.begin(), rb.end());
+            st = make_high_stage(K, rb);
+        }
+        int reg_of[kMaxK], lane_of[kMaxK], warp_of[kMaxK];
+        for (int f = 0; f < kMaxK; ++f) reg_of[f] = lane_of[f] = warp_of[f] = -1;
+        for (int r = 0; r < kRegBits; ++r) reg_of[st.rf[r]] = r;
+        for (int l = 0; l < 5; ++l) lane_of[st.lf[l]] = l;
+        for (int w = 0; w < K - 10; ++w) warp_of[st.wf[w]] = w;
         st.op_begin = (int)fops.size();
-        // take ops while their pair target is representable in this stage
-        for (; i < nops && (int)fops.size() - st.op_begin < kMaxOps; ++i) {
+        for (; i < nops; ++i) {
             const qs_op &op = ops[i];
-            int hb = high_target(op);
-            if (hb >= 0 && rpos_of[hb] < 0) break;
-            FOp f;
-            std::memset(&f, 0, sizeof f);
-            f.kind = op.kind == QS_OP_PHASE ? kPhase : kPair;
-            std::memcpy(f.m, op.m, sizeof f.m);
-            f.real = is_real(op.m);
+            int f = -1, nd = need_of(op, &f);
+            if (nd == 1 && kind != 1) break;
+            if (nd == 2 && (kind != 2 || reg_of[f] < 0)) break;
+            FOp o;
+            std::memset(&o, 0, sizeof o);
+            std::memcpy(o.m, op.m, sizeof o.m);
             uint64_t need = op.ctrl_mask;
             if (op.kind == QS_OP_PHASE) need |= 1ull << op.target;
             for (int q = 0; q < n; ++q) {
                 if (!((need >> q) & 1ull)) continue;
-                int lb = local_of[q];
+                const int lb = local_of[q];
                 if (lb < 0)
-                    f.ext_need |= 1ull << q;
+                    o.ext_need |= 1ull << q;
                 else if (lb == 0)
-                    f.half_need = 1;
-                else if (lb < kLow)
-                    f.lane_need |= 1u << (lb - 1);
-                else if (rpos_of[lb] >= 0)
-                    f.reg_need |= 1u << rpos_of[lb];
+                    o.half_need = 1;
+                else if (reg_of[lb - 1] >= 0)
+                    o.reg_need |= 1u << reg_of[lb - 1];
+                else if (lane_of[lb - 1] >= 0)
+                    o.tid_need |= 1u << lane_of[lb - 1];
                 else
-                    f.warp_need |= 1u << wpos_of[lb];
+                    o.tid_need |= 1u << (5 + warp_of[lb - 1]);
             }
-            if (op.kind == QS_OP_PAIR) {
-                int lb = local_of[op.target];
-                if (lb == 0) {
-                    f.tclass = kTHalf;
-                } else if (lb < kLow) {
-                    f.tclass = kTLane;
-                    f.tidx = lb - 1;
-                } else {
-                    f.tclass = kTReg;
-                    f.tidx = rpos_of[lb];
-                }
+            const int has_need = o.reg_need != 0 || o.half_need != 0;
+            if (op.kind == QS_OP_PHASE) {
+                o.variant = kPhaseVariant + (int)o.reg_need * 2 + (o.half_need ? 1 : 0);
+            } else {
+                const int lb = local_of[op.target];
+                const int slot = lb == 0 ? -1 : reg_of[lb - 1];
+                o.variant = ((slot + 1) * 4 + gate_class(op.m)) * 2 + has_need;
             }
-            fops.push_back(f);
+            fops.push_back(o);
         }
         st.op_end = (int)fops.size();
         stages.push_back(st);
-        (void)nhigh;
     }
-    // ---- launch: consecutive stage groups that fit one parameter block ----
+
+    // ---- launch: consecutive stage groups within the op / stage limits ------
     size_t si = 0;
     while (si < stages.size()) {
         size_t sj = si;
         int nop = 0;
         while (sj < stages.size() && (int)(sj - si) < kMaxStages &&
-               nop + (stages[sj].op_end - stages[sj].op_begin) <= kMaxOps) {
+               (nop + (stages[sj].op_end - stages[sj].op_begin) <= kMaxOps || sj == si)) {
             nop += stages[sj].op_end - stages[sj].op_begin;
             ++sj;
         }
+        if (nop > kMaxOps) {  // one huge stage: split its op range
+            FStage a = stages[si], b = stages[si];
+            a.op_end = a.op_begin + kMaxOps;
+            b.op_begin = a.op_end;
+            stages[si] = a;
+            stages.insert(stages.begin() + si + 1, b);
+            continue;
+        }
         p.nstages = (int)(sj - si);
+        p.nops = nop;
         const int off = stages[si].op_begin;
         for (size_t k = si; k < sj; ++k) {
             p.stages[k - si] = stages[k];
@@ -513,8 +701,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
             case 10: rc = launch_fused_k<10>(s, p); break;
             case 11: rc = launch_fused_k<11>(s, p); break;
             case 12: rc = launch_fused_k<12>(s, p); break;
-            case 13: rc = launch_fused_k<13>(s, p); break;
-            default: rc = launch_fused_k<14>(s, p); break;
+            default: rc = launch_fused_k<13>(s, p); break;
         }
         if (rc) return rc;
         si = sj;

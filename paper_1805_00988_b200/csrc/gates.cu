@@ -33,7 +33,6 @@ namespace qsb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarpsPerBlock = kThreads / 32;
 
 int env_int(const char *name, int dflt) {
     const char *v = std::getenv(name);

@@ -44,11 +44,11 @@ def test_sm100a_cubin_embedded():
     assert "sm_100a" in out
 
 
-def test_fused_kernel_uses_bulk_async_copies():
-    """The fused pass stages tiles with the TMA bulk-copy engine (UBLKCP in SASS)."""
+def test_fused_kernel_uses_tma_tensor_copies():
+    """The fused pass stages tiles through the TMA engine (tensor copies in SASS)."""
     sass = subprocess.run(["cuobjdump", "-sass", str(N.LIB_PATH)], capture_output=True, text=True).stdout
-    assert "UBLKCP.S.G" in sass  # global -> shared bulk load
-    assert "UBLKCP.G.S" in sass  # shared -> global bulk store
+    assert "UTMALDG.5D" in sass  # global -> shared tensor load
+    assert "UTMASTG.5D" in sass  # shared -> global tensor store
     assert "SYNCS.ARRIVE.TRANS64" in sass  # mbarrier expect_tx
 
 
