@@ -9,9 +9,13 @@ i.e. the per-gate HBM roofline configuration.  metric = single-qubit
 gates/s; each sweep moves 16 * 2^30 algorithmic bytes.  The register
 (8 GiB) is larger than L2 (126 MB), so no flush is needed between steps.
 
-N>1 (torchrun, one process per GPU): weak scaling — every rank holds an
-independent 30-qubit register and runs the same layer ("replicas"; the
-sharded 30+log2(N)-qubit register lives in paper_1805_00988_b200.sharded).
+N>1 (torchrun, one process per GPU): weak scaling — ONE register of
+30 + log2(N) qubits sharded over the N GPUs on its top log2(N) qubits
+(paper_1805_00988_b200.sharded, NCCL over NVLink).  A step applies H to every
+logical qubit; the log2(N) gates on global qubits each trigger a qubit swap
+(half-shard NCCL exchange with the partner rank).  value counts shard sweeps
+(each 2^30 amplitudes) per second summed over GPUs, so N=1 and N>1 values
+are directly comparable.
 
 --impl reference times the reference CPU path (oracle/port.py, the numpy
 restatement of pairsim's ThreadExecutor sweep; /root/reference is absent on
@@ -213,13 +217,9 @@ def run_ours(args):
 
     rank, world, local = _dist_env()
     if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-        dist = None
+        return run_sharded(args)
+    torch.cuda.set_device(local)
+    dist = None
 
     from paper_1805_00988_b200 import State
     from paper_1805_00988_b200.gates import H, m8
@@ -343,6 +343,99 @@ def run_ours(args):
         print(json.dumps(out))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def run_sharded(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_00988_b200 import _native as N
+    from paper_1805_00988_b200.gates import H
+    from paper_1805_00988_b200.sharded import ShardedState
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    g = int(round(math.log2(world)))
+    if 1 << g != world:
+        raise SystemExit("--gpus must be a power of two")
+    L = args.qubits
+    n = L + g
+    st = ShardedState.distributed(n, device=local)
+    eng = st.engines[0]
+    stream = torch.cuda.ExternalStream(eng.state.stream(), device=torch.device("cuda", local))
+
+    def layer():
+        for q in range(n):
+            st.apply_gate(H, q)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        dist.barrier()
+
+    for _ in range(args.warmup):
+        layer()
+    barrier()
+    swaps0 = st.swaps
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        a.record(stream)
+        for _ in range(args.steps):
+            layer()
+        b.record(stream)
+        barrier()
+    ms = a.elapsed_time(b)
+    tt = torch.tensor([ms], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    swaps = (st.swaps - swaps0) // args.steps
+    sweeps = args.steps * n * world
+    value = sweeps / (ms / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(2 << L, dtype=torch.float32, pin_memory=True)
+        hptr = host.data_ptr()
+        h = eng.state.handle
+        L_ = N.lib()
+        k2 = max(1, min(args.steps, 2))
+
+        def e2e_step():
+            N.check(L_.qs_set_amplitudes(h, 0, 1 << L, hptr))
+            layer()
+            N.check(L_.qs_get_amplitudes(h, 0, 1 << L, hptr))
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            e2e_step()
+        barrier()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": k2 * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": (8 << L) * world,
+               "d2h_bytes_per_step": (8 << L) * world, "steps": k2,
+               "timing": "host wall clock, every rank uploads/downloads its shard around the layer, max over ranks"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": "hlayer_sweep_unfused_sharded", "n_qubits": n, "shard_qubits": L,
+                       "gates_per_step": n, "global_qubit_swaps_per_step": swaps,
+                       "parallelism": f"shard{world} (top {g} qubits)",
+                       "value_unit": "shard sweeps (2^%d amplitudes) per second, summed over GPUs" % L,
+                       "l2": "shards (8 GiB) larger than L2; no flush needed"},
+            "gpu_launches": args.steps * n,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": None,
+        }))
+    dist.destroy_process_group()
 
 
 def run_extras(st, stream, n):

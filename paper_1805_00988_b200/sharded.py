@@ -1,0 +1,491 @@
+"""Registers sharded over P = 2^g GPUs on their top g qubits.
+
+Layout: physical qubit positions 0..L-1 (L = n - g) are local index bits of
+every shard; positions L..n-1 are the shard (rank) bits, so shard r owns the
+contiguous slice [r * 2^L, (r+1) * 2^L) of the physical index space.  A
+logical -> physical qubit map (QubitLayout) is kept on the host and updated
+lazily:
+
+* a gate whose target and controls are local runs on every shard with no
+  communication; a control on a global qubit is a shard predicate (shards
+  whose bit is 0 skip the gate);
+* a gate targeting a global qubit first swaps that physical position with
+  local position L-1 ("qubit swap"): partner shards r and r ^ (1 << b)
+  exchange the half of their slice whose bit L-1 differs from their own
+  rank bit b.  With s = L-1 that half is contiguous, so the exchange is two
+  plain buffers (NCCL send/recv over NVLink, or an in-process copy for
+  virtual shards) and needs no pack/unpack kernel.  No swap-back: the map
+  records the permutation and readout un-permutes it (canonicalize()).
+
+Transports:
+* DistTransport  — one process per GPU, torch.distributed (NCCL on GPUs,
+  gloo for the CPU tests), chunked through a staging buffer;
+* LocalTransport — P virtual shards in one process (one GPU or CPU engines),
+  the same swap logic with in-process copies.
+
+The per-shard compute engine is pluggable: CudaEngine wraps a device State
+(libqsb200); tests plug in an oracle engine on the CPU.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .gates import FIXED_GATES, m8, u1 as _u1
+
+
+# ----------------------------------------------------------------------------
+class QubitLayout:
+    """Logical -> physical qubit positions for n qubits over 2^g shards."""
+
+    def __init__(self, n: int, g: int):
+        if g < 0 or g >= n:
+            raise ValueError("need 0 <= g < n")
+        self.n, self.g, self.L = n, g, n - g
+        self.pos = list(range(n))  # pos[logical] = physical
+        self.at = list(range(n))   # at[physical] = logical
+
+    def is_local(self, q: int) -> bool:
+        return self.pos[q] < self.L
+
+    def swap_physical(self, p1: int, p2: int) -> None:
+        a, b = self.at[p1], self.at[p2]
+        self.at[p1], self.at[p2] = b, a
+        self.pos[a], self.pos[b] = p2, p1
+
+    def is_identity(self) -> bool:
+        return self.pos == list(range(self.n))
+
+    def logical_of_physical_index(self, phys: np.ndarray) -> np.ndarray:
+        """Map physical basis indices to logical ones (bit at[p] <- bit p)."""
+        phys = np.asarray(phys, dtype=np.int64)
+        out = np.zeros_like(phys)
+        for p in range(self.n):
+            out |= ((phys >> p) & 1) << self.at[p]
+        return out
+
+
+def exchange_plan(rank: int, rank_bit: int, L: int) -> tuple[int, int, int]:
+    """(partner, offset, count) for swapping physical position L + rank_bit
+    with local position L-1: send/receive the contiguous half of the local
+    slice whose bit L-1 differs from this rank's bit `rank_bit`."""
+    partner = rank ^ (1 << rank_bit)
+    rb = (rank >> rank_bit) & 1
+    half = 1 << (L - 1)
+    offset = half if rb == 0 else 0
+    return partner, offset, half
+
+
+# ----------------------------------------------------------------------------
+class CudaEngine:
+    """One shard on a GPU: a libqsb200 State of L qubits."""
+
+    def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None):
+        from .state import State
+
+        self.state = State(num_qubits, device=device, memory_budget=memory_budget)
+        self.num_qubits = num_qubits
+        self.device = device
+        self._view = None
+
+    def reset(self, basis: int | None) -> None:
+        """e_basis, or the zero vector for basis=None (a shard not holding |basis>)."""
+        self.state.reset(0 if basis is None else basis)
+        if basis is None:
+            self.state.set_amplitudes(np.zeros(1, np.complex64), offset=0)
+
+    def apply(self, kind: int, target: int, ctrl_mask: int, m: np.ndarray) -> None:
+        from . import fusion
+
+        fusion._single(self.state, kind, target, ctrl_mask, m)
+
+    def apply_ops(self, ops) -> None:
+        from . import fusion
+
+        fusion.run(self.state, fusion.plan(self.num_qubits, ops))
+
+    def swap_qubits(self, a: int, b: int) -> None:
+        self.state.swap_qubits(a, b)
+
+    def view(self):
+        """torch float32 view (2 * 2^L,) of the device amplitudes (zero-copy)."""
+        import torch
+
+        if self._view is None:
+            ptr = self.state.device_pointer()
+            nfloat = 2 << self.num_qubits
+
+            class _CAI:
+                __cuda_array_interface__ = {"shape": (nfloat,), "typestr": "<f4", "data": (ptr, False),
+                                            "version": 3, "strides": None}
+
+            self._view = torch.as_tensor(_CAI(), device=torch.device("cuda", self.device))
+        return self._view
+
+    def comm_begin(self) -> None:
+        """Order torch's stream after this shard's kernels."""
+        import torch
+
+        ext = torch.cuda.ExternalStream(self.state.stream(), device=torch.device("cuda", self.device))
+        torch.cuda.current_stream(self.device).wait_stream(ext)
+
+    def comm_end(self) -> None:
+        """Order this shard's stream after torch's (copies / NCCL) work."""
+        import torch
+
+        ext = torch.cuda.ExternalStream(self.state.stream(), device=torch.device("cuda", self.device))
+        ext.wait_stream(torch.cuda.current_stream(self.device))
+
+    def amplitudes(self) -> np.ndarray:
+        return self.state.amplitudes()
+
+    def probabilities(self) -> np.ndarray:
+        return self.state.probabilities()
+
+    def norm_squared(self) -> float:
+        return self.state.norm_squared()
+
+    def synchronize(self) -> None:
+        self.state.flush()
+
+
+# ----------------------------------------------------------------------------
+class LocalTransport:
+    """All shards live in this process (virtual shards)."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def exchange(self, engines, rank_bit: int, L: int, chunk: int) -> None:
+        for r in range(len(engines)):
+            partner, off, cnt = exchange_plan(r, rank_bit, L)
+            if partner < r:
+                continue
+            _, poff, _ = exchange_plan(partner, rank_bit, L)
+            a, b = engines[r], engines[partner]
+            a.comm_begin()
+            b.comm_begin()
+            va, vb = a.view(), b.view()
+            sa = va[2 * off: 2 * (off + cnt)]
+            sb = vb[2 * poff: 2 * (poff + cnt)]
+            tmp = sa.clone()
+            sa.copy_(sb)
+            sb.copy_(tmp)
+            a.comm_end()
+            b.comm_end()
+
+    def allreduce_sum(self, values):
+        return [sum(values)] * len(values)
+
+
+class DistTransport:
+    """One shard per process; torch.distributed point-to-point exchange."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._staging = None
+
+    def exchange(self, engines, rank_bit: int, L: int, chunk: int) -> None:
+        dist = self.dist
+        (eng,) = engines
+        partner, off, cnt = exchange_plan(self.rank, rank_bit, L)
+        eng.comm_begin()
+        v = eng.view()
+        step = min(cnt, chunk)
+        if self._staging is None or self._staging.numel() < 2 * step or self._staging.device != v.device:
+            self._staging = v.new_empty(2 * step)
+        stg = self._staging[: 2 * step]
+        peer = dist.get_global_rank(self.group, partner) if self.group is not None else partner
+        for c in range(off, off + cnt, step):
+            mine = v[2 * c: 2 * (c + step)]
+            ops = [dist.P2POp(dist.isend, mine, peer, self.group), dist.P2POp(dist.irecv, stg, peer, self.group)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            mine.copy_(stg)
+        eng.comm_end()
+
+    def allreduce_sum(self, values):
+        import torch
+
+        (x,) = values
+        t = torch.tensor([x], dtype=torch.float64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, group=self.group)
+        return [float(t.item())]
+
+
+# ----------------------------------------------------------------------------
+class ShardedState:
+    """A 2^n register over 2^g shards (QCGPU-style gate API)."""
+
+    def __init__(self, num_qubits: int, engines, transport, ranks, world: int,
+                 chunk_amps: int = 1 << 26):
+        g = int(round(math.log2(world)))
+        if 1 << g != world:
+            raise ValueError("the shard count must be a power of two")
+        self.num_qubits = num_qubits
+        self.layout = QubitLayout(num_qubits, g)
+        self.engines = list(engines)
+        self.ranks = list(ranks)  # rank id of each local engine
+        self.transport = transport
+        self.world = world
+        self.chunk = chunk_amps
+        self.swaps = 0
+
+    # ---- constructors ------------------------------------------------------
+    @classmethod
+    def distributed(cls, num_qubits: int, group=None, device: int | None = None, engine_factory=None):
+        import torch.distributed as dist
+
+        tr = DistTransport(group)
+        g = int(round(math.log2(tr.world)))
+        L = num_qubits - g
+        if engine_factory is None:
+            import torch
+
+            dev = torch.cuda.current_device() if device is None else device
+            eng = CudaEngine(L, dev)
+        else:
+            eng = engine_factory(L)
+        st = cls(num_qubits, [eng], tr, [tr.rank], tr.world)
+        st.reset(0)
+        return st
+
+    @classmethod
+    def virtual(cls, num_qubits: int, shards: int, device: int = 0, engine_factory=None):
+        g = int(round(math.log2(shards)))
+        L = num_qubits - g
+        make = engine_factory or (lambda L_: CudaEngine(L_, device))
+        engines = [make(L) for _ in range(shards)]
+        st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards)
+        st.reset(0)
+        return st
+
+    # ---- state ----------------------------------------------------------------
+    @property
+    def L(self) -> int:
+        return self.layout.L
+
+    def reset(self, basis: int = 0) -> "ShardedState":
+        """|basis> with the identity qubit map."""
+        self.layout = QubitLayout(self.num_qubits, self.layout.g)
+        owner, local = basis >> self.L, basis & ((1 << self.L) - 1)
+        for eng, r in zip(self.engines, self.ranks):
+            eng.reset(local if r == owner else None)
+        return self
+
+    # ---- gates ------------------------------------------------------------------
+    def _ensure_local(self, target: int) -> None:
+        lay = self.layout
+        if lay.is_local(target):
+            return
+        p = lay.pos[target]
+        self.transport.exchange(self.engines, p - lay.L, lay.L, self.chunk)
+        lay.swap_physical(p, lay.L - 1)
+        self.swaps += 1
+
+    def apply_op(self, gate, target: int, controls=()) -> "ShardedState":
+        n = self.num_qubits
+        qs = [int(target), *map(int, controls)]
+        for q in qs:
+            if not 0 <= q < n:
+                raise IndexError(f"qubit {q} out of range for {n} qubits")
+        if len(set(qs)) != len(qs):
+            raise ValueError("control and target must differ")
+        m = m8(gate)
+        from .gates import is_phase
+
+        kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
+        lay = self.layout
+        if kind == N.QS_OP_PHASE and not lay.is_local(target):
+            # a diagonal gate is symmetric in its target/control bits: keep the
+            # data in place and pick a local bit as the "target" if one exists
+            local = [q for q in qs if lay.is_local(q)]
+            if local:
+                target = local[0]
+                controls = [q for q in qs if q != target]
+        if kind == N.QS_OP_PAIR or not any(lay.is_local(q) for q in [target, *controls]):
+            self._ensure_local(target)
+        t_phys = lay.pos[target]
+        cmask, need_rank = 0, 0
+        for c in controls:
+            pc = lay.pos[c]
+            if pc < lay.L:
+                cmask |= 1 << pc
+            else:
+                need_rank |= 1 << (pc - lay.L)
+        for eng, r in zip(self.engines, self.ranks):
+            if (r & need_rank) == need_rank:
+                eng.apply(kind, t_phys, cmask, m)
+        return self
+
+    def apply_gate(self, gate, target):
+        return self.apply_op(gate, target)
+
+    def apply_controlled_gate(self, gate, control, target):
+        return self.apply_op(gate, target, (control,))
+
+    def apply_controlled_controlled_gate(self, gate, c1, c2, target):
+        return self.apply_op(gate, target, (c1, c2))
+
+    def h(self, t):
+        return self.apply_op(FIXED_GATES["h"], t)
+
+    def x(self, t):
+        return self.apply_op(FIXED_GATES["x"], t)
+
+    def t(self, t):
+        return self.apply_op(FIXED_GATES["t"], t)
+
+    def cx(self, c, t):
+        return self.apply_op(FIXED_GATES["x"], t, (c,))
+
+    def cu1(self, c, t, theta):
+        return self.apply_op(_u1(theta), t, (c,))
+
+    def ccx(self, c1, c2, t):
+        return self.apply_op(FIXED_GATES["x"], t, (c1, c2))
+
+    def run(self, circuit) -> "ShardedState":
+        """Apply a circuit: maximal runs of local ops go to each shard's fused
+        planner in one call; global targets trigger a swap in between."""
+        from .circuits import Apply, ControlledApply, ControlledControlledApply
+
+        pending: list = []
+
+        def flush():
+            if pending:
+                for eng, r in zip(self.engines, self.ranks):
+                    ops = [(k, t, cm, m) for (k, t, cm, m, need) in pending if (r & need) == need]
+                    if ops:
+                        eng.apply_ops(ops)
+                pending.clear()
+
+        for ins in circuit.instructions:
+            if isinstance(ins, Apply):
+                gate, target, controls = ins.gate, ins.target, ()
+            elif isinstance(ins, ControlledApply):
+                gate, target, controls = ins.gate, ins.target, (ins.control,)
+            elif isinstance(ins, ControlledControlledApply):
+                gate, target, controls = ins.gate, ins.target, (ins.control1, ins.control2)
+            else:
+                continue
+            m = m8(gate)
+            from .gates import is_phase
+
+            kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
+            lay = self.layout
+            qs = [target, *controls]
+            if kind == N.QS_OP_PHASE and not lay.is_local(target):
+                local = [q for q in qs if lay.is_local(q)]
+                if local:
+                    target = local[0]
+                    controls = tuple(q for q in qs if q != target)
+            if not lay.is_local(target):
+                flush()
+                self._ensure_local(target)
+            cmask, need = 0, 0
+            for c in controls:
+                pc = lay.pos[c]
+                if pc < lay.L:
+                    cmask |= 1 << pc
+                else:
+                    need |= 1 << (pc - lay.L)
+            pending.append((kind, lay.pos[target], cmask, m, need))
+        flush()
+        return self
+
+    # ---- readout ---------------------------------------------------------------
+    def canonicalize(self) -> "ShardedState":
+        """Restore the identity qubit map (local swap kernels + exchanges)."""
+        lay = self.layout
+        for p in range(self.num_qubits):
+            q = lay.at[p]
+            if q == p:
+                continue
+            # bring logical qubit p (now at physical pp) to physical p
+            pp = lay.pos[p]
+            if p < lay.L and pp < lay.L:
+                for eng in self.engines:
+                    eng.swap_qubits(p, pp)
+                lay.swap_physical(p, pp)
+            elif p >= lay.L and pp >= lay.L:
+                # swap two global positions through local L-1
+                self._swap_global_via_local(p, pp)
+            elif p < lay.L:  # target local, source global
+                self._swap_local_global(p, pp)
+            else:  # target global, source local
+                self._swap_local_global(pp, p)
+        return self
+
+    def _swap_local_global(self, loc: int, glob: int) -> None:
+        lay = self.layout
+        s = lay.L - 1
+        if loc != s:
+            for eng in self.engines:
+                eng.swap_qubits(loc, s)
+            lay.swap_physical(loc, s)
+        self.transport.exchange(self.engines, glob - lay.L, lay.L, self.chunk)
+        lay.swap_physical(glob, s)
+        self.swaps += 1
+        if loc != s:
+            for eng in self.engines:
+                eng.swap_qubits(loc, s)
+            lay.swap_physical(loc, s)
+
+    def _swap_global_via_local(self, g1: int, g2: int) -> None:
+        self._swap_local_global(self.layout.L - 1, g1)
+        self._swap_local_global(self.layout.L - 1, g2)
+        self._swap_local_global(self.layout.L - 1, g1)
+
+    def local_amplitudes(self):
+        """{rank: amplitudes of its canonical slice} for the local engines."""
+        self.canonicalize()
+        return {r: eng.amplitudes() for eng, r in zip(self.engines, self.ranks)}
+
+    def amplitudes(self) -> np.ndarray:
+        """Full logical amplitude vector (virtual mode, or gathered over ranks)."""
+        parts = self.local_amplitudes()
+        if len(parts) == self.world:
+            return np.concatenate([parts[r] for r in range(self.world)])
+        return self._gather(parts, np.complex64)
+
+    def probabilities(self) -> np.ndarray:
+        self.canonicalize()
+        parts = {r: eng.probabilities() for eng, r in zip(self.engines, self.ranks)}
+        if len(parts) == self.world:
+            return np.concatenate([parts[r] for r in range(self.world)])
+        return self._gather(parts, np.float64)
+
+    def _gather(self, parts, dtype):
+        import torch
+
+        dist = self.transport.dist
+        (r, arr), = parts.items()
+        raw = np.ascontiguousarray(arr).view(np.uint8)
+        t = torch.from_numpy(raw.copy())
+        if dist.get_backend(self.transport.group) == "nccl":
+            t = t.cuda()
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.transport.group)
+        return np.concatenate([o.cpu().numpy().view(dtype) for o in out])
+
+    def norm_squared(self) -> float:
+        vals = [eng.norm_squared() for eng in self.engines]
+        if len(vals) == self.world:
+            return float(sum(vals))
+        return self.transport.allreduce_sum(vals)[0]
+
+    def synchronize(self) -> None:
+        for eng in self.engines:
+            eng.synchronize()

@@ -1,0 +1,65 @@
+"""CPU shard engine for the sharded-layer tests: the oracle (TEST INFRASTRUCTURE)
+applied to a numpy complex64 shard.  Implements the engine interface of
+paper_1805_00988_b200.sharded.CudaEngine."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from golden_util import M8Gate
+from oracle import c as oc
+
+
+class OracleEngine:
+    def __init__(self, num_qubits: int):
+        self.num_qubits = num_qubits
+        self.amps = np.zeros(1 << num_qubits, np.complex64)
+
+    def reset(self, basis):
+        self.amps[:] = 0
+        if basis is not None:
+            self.amps[basis] = 1
+
+    def apply(self, kind, target, ctrl_mask, m):
+        g = M8Gate(m)
+        ctrls = [q for q in range(64) if (ctrl_mask >> q) & 1]
+        if not ctrls:
+            oc.apply_gate(self.amps, target, g)
+        elif len(ctrls) == 1:
+            oc.apply_controlled_gate(self.amps, ctrls[0], target, g)
+        elif len(ctrls) == 2:
+            oc.apply_cc_gate(self.amps, ctrls[0], ctrls[1], target, g)
+        else:
+            raise NotImplementedError
+
+    def apply_ops(self, ops):
+        for kind, t, cm, m in ops:
+            self.apply(kind, t, cm, m)
+
+    def swap_qubits(self, a, b):
+        idx = np.arange(self.amps.size)
+        ba, bb = (idx >> a) & 1, (idx >> b) & 1
+        src = idx ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
+        self.amps[:] = self.amps[src]
+
+    def view(self):
+        return torch.from_numpy(self.amps.view(np.float32))
+
+    def comm_begin(self):
+        pass
+
+    def comm_end(self):
+        pass
+
+    def amplitudes(self):
+        return self.amps.copy()
+
+    def probabilities(self):
+        return oc.probabilities(self.amps)
+
+    def norm_squared(self):
+        return float(oc.probabilities(self.amps).sum())
+
+    def synchronize(self):
+        pass

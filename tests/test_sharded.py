@@ -1,0 +1,173 @@
+"""Sharded-register host logic on the CPU (gloo, world size 2 and 4; virtual
+shards), with the oracle as the per-shard engine.  The same ShardedState code
+drives libqsb200 shards over NCCL on GPUs (tests/test_gpu_sharded.py)."""
+
+from __future__ import annotations
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from golden_util import M8Gate, same_values
+from oracle import c as oc
+from paper_1805_00988_b200 import FIXED_GATES, Circuit, build_hadamard_layer, build_qft, random_circuit, u1
+from paper_1805_00988_b200.circuits import Apply, ControlledApply, ControlledControlledApply
+from paper_1805_00988_b200.sharded import QubitLayout, ShardedState, exchange_plan
+from shard_engines import OracleEngine
+
+
+def oracle_run(circuit, basis=0):
+    amps = np.zeros(1 << circuit.num_qubits, np.complex64)
+    amps[basis] = 1
+    for ins in circuit.instructions:
+        if isinstance(ins, Apply):
+            oc.apply_gate(amps, ins.target, ins.gate)
+        elif isinstance(ins, ControlledApply):
+            oc.apply_controlled_gate(amps, ins.control, ins.target, ins.gate)
+        elif isinstance(ins, ControlledControlledApply):
+            oc.apply_cc_gate(amps, ins.control1, ins.control2, ins.target, ins.gate)
+    return amps
+
+
+def mixed_circuit(n, depth, seed):
+    rng = np.random.default_rng(seed)
+    circ = random_circuit(n, depth, rng)
+    extra = []
+    for _ in range(depth // 8):
+        c1, c2, t = (int(x) for x in rng.choice(n, 3, replace=False))
+        extra.append(ControlledControlledApply(FIXED_GATES["x"], c1, c2, t))
+    ins = list(circ.instructions)
+    for k, e in enumerate(extra):
+        ins.insert((k * 7) % (len(ins) + 1), e)
+    return Circuit(n, tuple(ins))
+
+
+class TestLayout:
+    def test_swap_bookkeeping(self):
+        lay = QubitLayout(6, 2)
+        lay.swap_physical(5, 3)
+        assert lay.pos[5] == 3 and lay.pos[3] == 5 and lay.at[3] == 5 and lay.at[5] == 3
+        assert not lay.is_local(3) and lay.is_local(5)
+        phys = np.arange(64)
+        log = lay.logical_of_physical_index(phys)
+        assert sorted(log.tolist()) == list(range(64))
+        assert log[1 << 3] == 1 << 5
+
+    def test_exchange_plan_halves(self):
+        L = 5
+        for rb in range(3):
+            for r in range(8):
+                partner, off, cnt = exchange_plan(r, rb, L)
+                assert partner == r ^ (1 << rb) and cnt == 16
+                assert off == (16 if not (r >> rb) & 1 else 0)
+                # partners exchange complementary halves
+                assert exchange_plan(partner, rb, L)[1] == 16 - off
+
+    def test_exchange_is_the_bit_swap(self):
+        """Swapping halves by exchange_plan == permuting index bits L-1 <-> L+b."""
+        n, g = 6, 2
+        L = n - g
+        full = np.arange(1 << n).astype(np.complex64)
+        shards = [full[r << L:(r + 1) << L].copy() for r in range(1 << g)]
+        b = 1
+        for r in range(1 << g):
+            p, off, cnt = exchange_plan(r, b, L)
+            if p < r:
+                continue
+            _, poff, _ = exchange_plan(p, b, L)
+            tmp = shards[r][off:off + cnt].copy()
+            shards[r][off:off + cnt] = shards[p][poff:poff + cnt]
+            shards[p][poff:poff + cnt] = tmp
+        got = np.concatenate(shards)
+        idx = np.arange(1 << n)
+        s, t = L - 1, L + b
+        bs, bt = (idx >> s) & 1, (idx >> t) & 1
+        src = idx ^ ((bs ^ bt) << s) ^ ((bs ^ bt) << t)
+        assert np.array_equal(got, full[src])
+
+
+class TestVirtualShards:
+    @pytest.mark.parametrize("n,shards", [(6, 2), (7, 4), (8, 8), (9, 4)])
+    def test_random_circuits_bitwise(self, n, shards):
+        for seed in range(3):
+            circ = mixed_circuit(n, 60, seed + 10 * n)
+            ref = oracle_run(circ)
+            st = ShardedState.virtual(n, shards, engine_factory=OracleEngine)
+            st.run(circ)
+            assert same_values(st.amplitudes(), ref)
+            assert abs(st.norm_squared() - float(oc.probabilities(ref).sum())) < 1e-12
+            assert st.probabilities().tobytes() == oc.probabilities(ref).tobytes()
+
+    def test_gate_api_matches_run(self):
+        n, shards = 7, 4
+        circ = mixed_circuit(n, 40, 99)
+        a = ShardedState.virtual(n, shards, engine_factory=OracleEngine)
+        for ins in circ.instructions:
+            if isinstance(ins, Apply):
+                a.apply_gate(ins.gate, ins.target)
+            elif isinstance(ins, ControlledApply):
+                a.apply_controlled_gate(ins.gate, ins.control, ins.target)
+            else:
+                a.apply_controlled_controlled_gate(ins.gate, ins.control1, ins.control2, ins.target)
+        assert same_values(a.amplitudes(), oracle_run(circ))
+
+    def test_hlayer_and_qft_global_qubits(self):
+        n, shards = 8, 4
+        circ = Circuit(n, build_hadamard_layer(n).instructions + build_qft(n).instructions)
+        st = ShardedState.virtual(n, shards, engine_factory=OracleEngine)
+        st.run(circ)
+        assert st.swaps >= 2  # both global qubits were swapped in
+        assert same_values(st.amplitudes(), oracle_run(circ))
+
+    def test_reset_basis_on_other_shard(self):
+        n = 6
+        st = ShardedState.virtual(n, 4, engine_factory=OracleEngine)
+        st.reset(0b110101)
+        a = st.amplitudes()
+        assert a[0b110101] == 1 and np.count_nonzero(a) == 1
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        circ = mixed_circuit(n, 50, seed)
+        st = ShardedState.distributed(n, engine_factory=OracleEngine)
+        st.run(circ)
+        amps = st.amplitudes()
+        probs = st.probabilities()
+        norm = st.norm_squared()
+        if rank == 0:
+            ref = oracle_run(circ)
+            q.put((bool(same_values(amps, ref)), probs.tobytes() == oc.probabilities(ref).tobytes(),
+                   abs(norm - float(oc.probabilities(ref).sum())) < 1e-12, st.swaps))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 7), (4, 8)])
+def test_gloo_distributed_matches_oracle(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, 1234 + n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    amps_ok, probs_ok, norm_ok, swaps = q.get(timeout=5)
+    assert amps_ok and probs_ok and norm_ok and swaps > 0
