@@ -54,7 +54,8 @@ def _args():
     ap.add_argument("--qubits", type=int, default=N_QUBITS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extras", action="store_true", help="also time fused layer / QFT")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the fused-pass / config 1, 3, 4 measurements")
     return ap.parse_args()
 
 
@@ -280,36 +281,50 @@ def run_ours(args):
     achieved = bytes_per_launch / avg_launch_s / 1e9
 
     extras = {}
-    if args.extras and rank == 0:
-        extras = run_extras(st, stream, n)
+    if not args.no_extras and rank == 0:
+        extras = run_extras(st, stream, n, cpu=not args.no_cpu)
 
     # ---- e2e through the C ABI with pinned host buffers -------------------
     e2e = None
     if not args.no_e2e:
-        host = torch.empty(2 << n, dtype=torch.float32, pin_memory=True)
-        host[0] = 1.0
-        hptr = host.data_ptr()
-        k2 = max(1, min(args.steps, 3))
-        def e2e_step():
-            N.check(L.qs_set_amplitudes(h, 0, 1 << n, hptr))
-            layer()
-            N.check(L.qs_get_amplitudes(h, 0, 1 << n, hptr))
-        e2e_step()
+        # Every step uploads a register from pinned host memory, applies the
+        # layer and downloads the result.  Two registers are kept in flight so
+        # step k+1's H2D overlaps step k's D2H on the other copy engine.
+        inp = torch.zeros(2 << n, dtype=torch.float32, pin_memory=True)
+        inp[0] = 1.0
+        outs = [torch.empty(2 << n, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        st2 = State(n, device=local)
+        regs = [st, st2]
+        k2 = max(2, min(args.steps, 6))
+
+        def e2e_step(k):
+            s = regs[k % 2]
+            if k >= 2:
+                s.flush()  # its previous step (incl. the download) has finished
+            s.upload_async(inp.data_ptr())
+            for t in range(n):
+                N.check(L.qs_apply_gate(s.handle, t, hp))
+            s.download_async(outs[k % 2].data_ptr())
+
+        for k in range(2):
+            e2e_step(k)
+        for s in regs:
+            s.flush()
         barrier()
         t0 = time.perf_counter()
-        for _ in range(k2):
-            e2e_step()
+        for k in range(k2):
+            e2e_step(k)
+        for s in regs:
+            s.flush()
         barrier()
         dt = time.perf_counter() - t0
-        if dist is not None:
-            tt = torch.tensor([dt], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+        ok = bool(torch.equal(outs[0], outs[1]))
         e2e = {"value": k2 * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": 8 << n,
-               "d2h_bytes_per_step": 8 << n, "steps": k2,
-               "timing": "host wall clock around qs_set_amplitudes + 30 x qs_apply_gate + "
-                         "qs_get_amplitudes (pinned host buffers), max over ranks"}
-        del host
+               "d2h_bytes_per_step": 8 << n, "steps": k2, "outputs_identical": ok,
+               "timing": "host wall clock: per step qs_set_amplitudes_async (pinned) + 30 x qs_apply_gate "
+                         "+ qs_get_amplitudes_async (pinned), two registers in flight, synchronized at the end"}
+        st2.close()
+        del inp, outs
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -438,31 +453,93 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
-def run_extras(st, stream, n):
-    """Fused H layer and a fused QFT on the same register (effective gates/s)."""
+def run_extras(st, stream, n, cpu=True):
+    """Fused passes on the 30-qubit register, plus BASELINE configs 1, 3, 4."""
     import torch
 
-    from paper_1805_00988_b200 import build_hadamard_layer, build_qft, fusion
+    from paper_1805_00988_b200 import State, build_hadamard_layer, build_qft, fusion, layered_random_circuit
     from paper_1805_00988_b200.circuits import lower_ops
 
-    res = {}
-    for name, circ in (("hlayer_fused", build_hadamard_layer(n)), ("qft_fused", build_qft(n))):
-        passes = fusion.plan(n, lower_ops(circ))
-        fusion.run(st, passes)
-        st.flush()
+    def timed(state, strm, passes, reps=3):
+        fusion.run(state, passes)
+        state.flush()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        reps = 3
-        a.record(stream)
+        a.record(strm)
         for _ in range(reps):
-            fusion.run(st, passes)
-        b.record(stream)
-        st.flush()
-        ms = a.elapsed_time(b) / reps
+            fusion.run(state, passes)
+        b.record(strm)
+        state.flush()
+        return a.elapsed_time(b) / reps
+
+    res = {}
+    for name, circ in (("hlayer30_fused", build_hadamard_layer(n)), ("qft30_fused", build_qft(n))):
+        passes = fusion.plan(n, lower_ops(circ))
+        ms = timed(st, stream, passes)
         res[name] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
                      "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
                      "pass_bytes": len(passes) * 16 * (1 << n),
                      "achieved_GBps": len(passes) * 16 * (1 << n) / (ms / 1e3) / 1e9}
+
+    # config 1: 20-qubit H on every qubit + probabilities (host wall clock, incl. the fp64 D2H)
+    s20 = State(20)
+    s20.h(0)
+    s20.probabilities()
+    best = float("inf")
+    for _ in range(5):
+        t0 = time.perf_counter()
+        s20.reset(0)
+        for q in range(20):
+            s20.h(q)
+        probs = s20.probabilities()
+        best = min(best, time.perf_counter() - t0)
+    res["config1_hlayer20_probs"] = {"ms_wall": best * 1e3, "gates": 20,
+                                     "note": "State(20).reset + 20 x h + probabilities() to host, best of 5"}
+    if cpu:
+        from oracle import port
+        from paper_1805_00988_b200.gates import H
+
+        ex = port.Executor(workers=len(os.sched_getaffinity(0)))
+        amps = np.zeros(1 << 20, np.complex64)
+        cbest = float("inf")
+        for _ in range(3):
+            t0 = time.perf_counter()
+            amps[:] = 0
+            amps[0] = 1
+            for q in range(20):
+                port.apply_gate(amps, q, H, ex)
+            p = port.probabilities(amps)
+            cbest = min(cbest, time.perf_counter() - t0)
+        ex.close()
+        res["config1_hlayer20_probs"]["cpu_port_ms"] = cbest * 1e3
+        res["config1_hlayer20_probs"]["probabilities_bit_identical"] = bool(p.tobytes() == probs.tobytes())
+    s20.close()
+
+    # config 3: 28-qubit QFT (fused), parity vs pairsim is in tests/test_gpu_parity.py
+    s28 = State(28)
+    s28_stream = torch.cuda.ExternalStream(s28.stream())
+    circ = build_qft(28)
+    passes = fusion.plan(28, lower_ops(circ))
+    ms = timed(s28, s28_stream, passes)
+    res["config3_qft28_fused"] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
+                                  "effective_gates_per_s": circ.gate_count() / (ms / 1e3)}
+    s28.close()
+
+    # config 4: 32-qubit layered random H/T/CX circuit, depth 20, fused
+    try:
+        s32 = State(32)
+    except Exception as exc:  # noqa: BLE001
+        res["config4_random32_fused"] = {"skipped": str(exc)}
+        return res
+    s32_stream = torch.cuda.ExternalStream(s32.stream())
+    circ = layered_random_circuit(32, 20, seed=32)
+    passes = fusion.plan(32, lower_ops(circ))
+    ms = timed(s32, s32_stream, passes, reps=1)
+    res["config4_random32_fused"] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
+                                     "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
+                                     "pass_bytes": len(passes) * 16 * (1 << 32),
+                                     "achieved_GBps": len(passes) * 16 * (1 << 32) / (ms / 1e3) / 1e9}
+    s32.close()
     return res
 
 

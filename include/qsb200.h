@@ -113,6 +113,11 @@ int qs_swap_qubits(qs_state *s, int q1, int q2);
 /* ---- readout: state.py:146-161, measure.py:29-99 ------------------------- */
 int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, float *host);
 int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const float *host);
+/* Asynchronous variants: enqueue the copy on the handle's stream and return.
+ * `host` must stay valid (and, for full overlap, be pinned) until the next
+ * qs_synchronize on this handle. */
+int qs_set_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, const float *host);
+int qs_get_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, float *host);
 /* probabilities (measure.py:29-34): p[j] = re^2 + im^2 in fp64, bit-exact. */
 int qs_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
 /* norm_squared (state.py:146-151): fp64 sum of |a|^2 (tree order). */

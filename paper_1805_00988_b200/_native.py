@@ -25,7 +25,8 @@ EXPORTS = (
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
     "qs_apply_controlled_controlled_gate", "qs_apply_fused", "qs_swap_qubits",
-    "qs_get_amplitudes", "qs_set_amplitudes", "qs_probabilities", "qs_norm_squared",
+    "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
+    "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse",
 )
 
@@ -70,6 +71,8 @@ def _declare(L):
         "qs_swap_qubits": ([vp, i32, i32], i32),
         "qs_get_amplitudes": ([vp, u64, u64, vp], i32),
         "qs_set_amplitudes": ([vp, u64, u64, vp], i32),
+        "qs_get_amplitudes_async": ([vp, u64, u64, vp], i32),
+        "qs_set_amplitudes_async": ([vp, u64, u64, vp], i32),
         "qs_probabilities": ([vp, u64, u64, vp], i32),
         "qs_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),

@@ -315,6 +315,30 @@ int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const float 
     return QS_OK;
 }
 
+int qs_set_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, const float *host) {
+    CHECK_HANDLE(s);
+    int rc = check_range(s, offset, count);
+    if (rc) return rc;
+    if (count == 0) return QS_OK;
+    if (!host) return set_error(QS_ERR_NULL, "null host buffer");
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaMemcpyAsync(s->amps + offset, host, count * 8ull, cudaMemcpyHostToDevice,
+                            s->stream));
+    return QS_OK;
+}
+
+int qs_get_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, float *host) {
+    CHECK_HANDLE(s);
+    int rc = check_range(s, offset, count);
+    if (rc) return rc;
+    if (count == 0) return QS_OK;
+    if (!host) return set_error(QS_ERR_NULL, "null host buffer");
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaMemcpyAsync(host, s->amps + offset, count * 8ull, cudaMemcpyDeviceToHost,
+                            s->stream));
+    return QS_OK;
+}
+
 int qs_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host) {
     CHECK_HANDLE(s);
     int rc = check_range(s, offset, count);

@@ -174,6 +174,19 @@ class State:
         N.check(N.lib().qs_set_amplitudes(self.handle, int(offset), int(v.size), v.ctypes.data))
         return self
 
+    def upload_async(self, host_ptr: int, count: int | None = None, offset: int = 0) -> "State":
+        """Enqueue a host->device copy from a (pinned) buffer address; the buffer
+        must stay valid until flush()."""
+        count = self.dim - offset if count is None else count
+        N.check(N.lib().qs_set_amplitudes_async(self.handle, int(offset), int(count), int(host_ptr)))
+        return self
+
+    def download_async(self, host_ptr: int, count: int | None = None, offset: int = 0) -> "State":
+        """Enqueue a device->host copy into a (pinned) buffer address."""
+        count = self.dim - offset if count is None else count
+        N.check(N.lib().qs_get_amplitudes_async(self.handle, int(offset), int(count), int(host_ptr)))
+        return self
+
     def amplitude(self, index: int) -> complex:
         if not 0 <= index < self.dim:
             raise IndexError(f"basis index {index} out of range [0, {self.dim})")
