@@ -369,6 +369,7 @@ def run_sharded(args):
     from paper_1805_00988_b200.sharded import ShardedState
 
     rank, world, local = _dist_env()
+    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only in tests
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     g = int(round(math.log2(world)))

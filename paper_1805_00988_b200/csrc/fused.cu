@@ -54,9 +54,9 @@ namespace qsb {
 namespace {
 
 constexpr int kLow = 6;      // local qubits 0..5 form one 512-B segment
-constexpr int kRegBits = 4;  // 16 float4 per thread
+constexpr int kMaxRegBits = 4;  // RB: 2^RB float4 per thread (RB = 3 or 4)
 constexpr int kMaxK = 14;
-constexpr int kMaxWarpBits = kMaxK - 10;
+constexpr int kMaxWarpBits = 5;
 
 enum : int { kCplx = 0, kReal = 1, kHlike = 2, kSwap = 3 };
 
@@ -76,7 +76,7 @@ struct __align__(16) FOp {
 constexpr int kPhaseVariant = 40;
 
 struct FStage {
-    int rf[kRegBits];      // f-bit (f = local >> 1) of register bit r
+    int rf[kMaxRegBits];   // f-bit (f = local >> 1) of register bit r
     int lf[5];             // f-bit of lane bit i
     int wf[kMaxWarpBits];  // f-bit of warp bit w
     int op_begin, op_end;
@@ -218,15 +218,15 @@ __device__ __forceinline__ float4 mk4(float2 a, float2 b) { return make_float4(a
 // T = register bit of the target (-1: the float4 half, local qubit 0);
 // NEED: the op has a control / phase bit on the register index or the half
 // (per-j warp-uniform tests); !NEED is the straight-line common case.
-template <int T, int CLS, bool NEED>
-__device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[16]) {
+template <int T, int CLS, bool NEED, int RB>
+__device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[1 << RB]) {
     const uint32_t need = NEED ? op.reg_need : 0u;
     const bool odd_only = NEED && op.half_need != 0;
     float m[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) m[i] = (CLS == kSwap) ? 0.f : op.m[i];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < (1 << RB); ++j) {
         if (T >= 0 && (j & (1 << T))) continue;
         if (NEED && (j & need) != need) continue;  // warp-uniform
         if (T < 0) {
@@ -246,11 +246,11 @@ __device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[16]) {
 
 // Diagonal op: multiply the registers whose index has every bit of RNEED set
 // (compile-time pattern) by d; ODD: only the odd half (phase bit on local 0).
-template <int RNEED, bool ODD>
-__device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[16]) {
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[1 << RB]) {
     const float2 d = make_float2(op.m[6], op.m[7]);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < (1 << RB); ++j) {
         if ((j & RNEED) != RNEED) continue;
         float2 a = lo2(v[j]), b = hi2(v[j]);
         if (!ODD) a = cmul(d, a);
@@ -263,11 +263,16 @@ __device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[16]) {
 // bodies keep the per-j branch, which bounds ptxas' register demand there.
 __device__ constexpr bool kStraight[4] = {false, true, true, false};
 
-__device__ __forceinline__ void apply_op(const FOp &op, float4 (&v)[16]) {
+template <int RB>
+__device__ __forceinline__ void apply_op(const FOp &op, float4 (&v)[1 << RB]) {
     switch (op.variant) {
-#define QSB_CASE(T, C)                                                              \
-    case (((T) + 1) * 4 + (C)) * 2 + 0: apply_pair<(T), (C), !kStraight[C]>(op, v); break; \
-    case (((T) + 1) * 4 + (C)) * 2 + 1: apply_pair<(T), (C), true>(op, v); break;
+#define QSB_CASE(T, C)                                                                            \
+    case (((T) + 1) * 4 + (C)) * 2 + 0:                                                           \
+        if constexpr ((T) < RB) apply_pair<(T), (C), !kStraight[C], RB>(op, v);                    \
+        break;                                                                                    \
+    case (((T) + 1) * 4 + (C)) * 2 + 1:                                                           \
+        if constexpr ((T) < RB) apply_pair<(T), (C), true, RB>(op, v);                             \
+        break;
 #define QSB_CASES(T) QSB_CASE(T, 0) QSB_CASE(T, 1) QSB_CASE(T, 2) QSB_CASE(T, 3)
         QSB_CASES(-1)
         QSB_CASES(0)
@@ -276,9 +281,13 @@ __device__ __forceinline__ void apply_op(const FOp &op, float4 (&v)[16]) {
         QSB_CASES(3)
 #undef QSB_CASES
 #undef QSB_CASE
-#define QSB_PH(R)                                                   \
-    case kPhaseVariant + (R) * 2 + 0: apply_phase<(R), false>(op, v); break; \
-    case kPhaseVariant + (R) * 2 + 1: apply_phase<(R), true>(op, v); break;
+#define QSB_PH(R)                                                        \
+    case kPhaseVariant + (R) * 2 + 0:                                     \
+        if constexpr ((R) < (1 << RB)) apply_phase<(R), false, RB>(op, v); \
+        break;                                                            \
+    case kPhaseVariant + (R) * 2 + 1:                                     \
+        if constexpr ((R) < (1 << RB)) apply_phase<(R), true, RB>(op, v);  \
+        break;
         QSB_PH(0) QSB_PH(1) QSB_PH(2) QSB_PH(3) QSB_PH(4) QSB_PH(5) QSB_PH(6) QSB_PH(7)
         QSB_PH(8) QSB_PH(9) QSB_PH(10) QSB_PH(11) QSB_PH(12) QSB_PH(13) QSB_PH(14) QSB_PH(15)
 #undef QSB_PH
@@ -302,10 +311,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int K>
-__global__ void __maxnreg__(128)
+template <int K, int RB>
+__global__ void __maxnreg__(RB == 4 ? 128 : 96)
     k_fused(float4 *__restrict__ amps, const __grid_constant__ FParams p) {
-    constexpr int kCompute = 1 << (K - 5);        // compute threads
+    constexpr int kCompute = 1 << (K - 1 - RB);   // compute threads
     constexpr int kSegs = 1 << (K - kLow);        // 512-B segments per tile
     constexpr int kBufF4 = kSegs * 33;            // padded float4 per buffer
     extern __shared__ __align__(128) float4 smem[];
@@ -392,15 +401,15 @@ __global__ void __maxnreg__(128)
             for (int q = 0; q < 5; ++q) fb |= (uint32_t)((lane >> q) & 1) << st.lf[q];
             for (int q = 0; q < p.nwbits; ++q) fb |= (uint32_t)((warp >> q) & 1) << st.wf[q];
             const uint32_t pb = padded(fb);
-            uint32_t rs[kRegBits];
+            uint32_t rs[RB];
 #pragma unroll
-            for (int r = 0; r < kRegBits; ++r) rs[r] = padded(1u << st.rf[r]);
-            float4 v[16];
+            for (int r = 0; r < RB; ++r) rs[r] = padded(1u << st.rf[r]);
+            float4 v[1 << RB];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
+            for (int j = 0; j < (1 << RB); ++j) {
                 uint32_t a = pb;
 #pragma unroll
-                for (int r = 0; r < kRegBits; ++r)
+                for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
                 v[j] = tile[a];
             }
@@ -410,13 +419,13 @@ __global__ void __maxnreg__(128)
                 const uint64_t ext = op.ext_need;
                 const bool ok = ((uint32_t)tid & (uint32_t)hdr.z) == (uint32_t)hdr.z &&
                                 (base & ext) == ext;
-                if (ok && !p.dry) apply_op(op, v);
+                if (ok && !p.dry) apply_op<RB>(op, v);
             }
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
+            for (int j = 0; j < (1 << RB); ++j) {
                 uint32_t a = pb;
 #pragma unroll
-                for (int r = 0; r < kRegBits; ++r)
+                for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
                 tile[a] = v[j];
             }
@@ -428,19 +437,19 @@ __global__ void __maxnreg__(128)
     }
 }
 
-template <int K>
+template <int K, int RB>
 int launch_fused_k(qs_state *s, const FParams &p) {
     const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
     const size_t smem = bufs + (size_t)p.nops * sizeof(FOp);
     static int configured = -1;
     if (configured < (int)smem) {
-        QS_CUDA(cudaFuncSetAttribute(k_fused<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        QS_CUDA(cudaFuncSetAttribute(k_fused<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(bufs + kMaxOps * sizeof(FOp))));
         configured = (int)(bufs + kMaxOps * sizeof(FOp));
     }
     uint64_t grid = (uint64_t)s->num_sms;
     if (grid > p.ntiles) grid = p.ntiles;
-    k_fused<K><<<(unsigned)grid, (1 << (K - 5)) + 32, smem, s->stream>>>((float4 *)s->amps, p);
+    k_fused<K, RB><<<(unsigned)grid, (1 << (K - 1 - RB)) + 32, smem, s->stream>>>((float4 *)s->amps, p);
     QS_CUDA(cudaGetLastError());
     return QS_OK;
 }
@@ -453,29 +462,46 @@ int gate_class(const float m[8]) {
     return kReal;
 }
 
-// register layouts (f = local bit - 1; f has K-1 bits)
-//   LOW : regs f0..f3, lanes (f5, f6, f7, f4, f8), warps f9..
-//   HIGH: regs = 4 chosen f-bits >= 4, lanes (f0, f1, f2, f3, x), warps = rest
-FStage make_low_stage(int K) {
+// Register layouts (f = local bit - 1; f has K-1 bits; RB register bits).
+// An LDS/STS.128 phase serves 8 lanes; with the padded address f + (f >> 5)
+// those 8 lanes hit 8 distinct bank quads iff lanes 0..2 vary f0..f2 (same
+// padded row) or f5..f7 (distinct padding offsets).
+//   LOW : regs f0..f(RB-1), lanes (f5, f6, f7, then the two lowest free bits),
+//         warps = the remaining bits
+//   HIGH: regs = RB chosen f-bits >= RB, lanes (f0, f1, f2, then the two
+//         lowest free bits), warps = the remaining bits
+void fill_lanes_warps(FStage &st, int K, int RB, const int *first3) {
+    bool used[32] = {false};
+    for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
+    for (int i = 0; i < 3; ++i) {
+        st.lf[i] = first3[i];
+        used[first3[i]] = true;
+    }
+    int nl = 3, nw = 0;
+    for (int f = 0; f < K - 1; ++f) {
+        if (used[f]) continue;
+        if (nl < 5)
+            st.lf[nl++] = f;
+        else
+            st.wf[nw++] = f;
+    }
+}
+
+FStage make_low_stage(int K, int RB) {
     FStage st;
     std::memset(&st, 0, sizeof st);
-    for (int r = 0; r < kRegBits; ++r) st.rf[r] = r;
-    const int lanes[5] = {5, 6, 7, 4, 8};
-    for (int i = 0; i < 5; ++i) st.lf[i] = lanes[i];
-    for (int w = 0; w < K - 10; ++w) st.wf[w] = 9 + w;
+    for (int r = 0; r < RB; ++r) st.rf[r] = r;
+    const int first3[3] = {5, 6, 7};
+    fill_lanes_warps(st, K, RB, first3);
     return st;
 }
 
-FStage make_high_stage(int K, const std::vector<int> &rbits_f) {
+FStage make_high_stage(int K, int RB, const std::vector<int> &rbits_f) {
     FStage st;
     std::memset(&st, 0, sizeof st);
-    for (int r = 0; r < kRegBits; ++r) st.rf[r] = rbits_f[r];
-    std::vector<int> rest;
-    for (int f = 4; f < K - 1; ++f)
-        if (std::find(rbits_f.begin(), rbits_f.end(), f) == rbits_f.end()) rest.push_back(f);
-    for (int i = 0; i < 4; ++i) st.lf[i] = i;
-    st.lf[4] = rest[0];
-    for (int w = 0; w < K - 10; ++w) st.wf[w] = rest[1 + w];
+    for (int r = 0; r < RB; ++r) st.rf[r] = rbits_f[r];
+    const int first3[3] = {0, 1, 2};
+    fill_lanes_warps(st, K, RB, first3);
     return st;
 }
 
@@ -554,7 +580,15 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     std::memset(&p, 0, sizeof p);
     p.n = n;
     p.K = K;
-    p.nwbits = K - 10;
+    // RB = register bits per thread: 4 (16 float4 per thread) by default; 3
+    // (8 float4, twice the compute warps) with QSB_FUSED_RB=3 — measured
+    // slower on B200 because the per-op overhead scales with the thread count.
+    int RB = 4;
+    {
+        const char *r = std::getenv("QSB_FUSED_RB");
+        if (r && *r == '3') RB = 3;
+    }
+    p.nwbits = K - 6 - RB;
     p.ntiles = 1ull << (n - K);
     {
         const char *d = std::getenv("QSB_FUSED_DRY");
@@ -588,12 +622,12 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
 
     // ---- stage planning -----------------------------------------------------
     // need: 0 = any stage (phase op / target on local qubit 0), 1 = LOW
-    // (target on local 1..4), 2 = HIGH holding the target's f-bit
+    // (target on local 1..RB), 2 = HIGH holding the target's f-bit
     auto need_of = [&](const qs_op &op, int *fbit) -> int {
         if (op.kind != QS_OP_PAIR) return 0;
         const int lb = local_of[op.target];
         if (lb == 0) return 0;
-        if (lb <= 4) return 1;
+        if (lb <= RB) return 1;
         *fbit = lb - 1;
         return 2;
     };
@@ -612,24 +646,24 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         }
         FStage st;
         if (kind == 1) {
-            st = make_low_stage(K);
+            st = make_low_stage(K, RB);
         } else {
             std::vector<int> rb;
-            for (int j = i; j < nops && (int)rb.size() < kRegBits; ++j) {
+            for (int j = i; j < nops && (int)rb.size() < RB; ++j) {
                 int f = -1, nd = need_of(ops[j], &f);
                 if (nd == 1) break;
                 if (nd == 2 && std::find(rb.begin(), rb.end(), f) == rb.end()) rb.push_back(f);
             }
-            for (int f = 4; f < K - 1 && (int)rb.size() < kRegBits; ++f)
+            for (int f = RB; f < K - 1 && (int)rb.size() < RB; ++f)
                 if (std::find(rb.begin(), rb.end(), f) == rb.end()) rb.push_back(f);
             std::sort(rb.begin(), rb.end());
-            st = make_high_stage(K, rb);
+            st = make_high_stage(K, RB, rb);
         }
         int reg_of[kMaxK], lane_of[kMaxK], warp_of[kMaxK];
         for (int f = 0; f < kMaxK; ++f) reg_of[f] = lane_of[f] = warp_of[f] = -1;
-        for (int r = 0; r < kRegBits; ++r) reg_of[st.rf[r]] = r;
+        for (int r = 0; r < RB; ++r) reg_of[st.rf[r]] = r;
         for (int l = 0; l < 5; ++l) lane_of[st.lf[l]] = l;
-        for (int w = 0; w < K - 10; ++w) warp_of[st.wf[w]] = w;
+        for (int w = 0; w < p.nwbits; ++w) warp_of[st.wf[w]] = w;
         st.op_begin = (int)fops.size();
         for (; i < nops; ++i) {
             const qs_op &op = ops[i];
@@ -698,10 +732,10 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         std::memcpy(p.ops, fops.data() + off, (size_t)nop * sizeof(FOp));
         int rc;
         switch (K) {
-            case 10: rc = launch_fused_k<10>(s, p); break;
-            case 11: rc = launch_fused_k<11>(s, p); break;
-            case 12: rc = launch_fused_k<12>(s, p); break;
-            default: rc = launch_fused_k<13>(s, p); break;
+            case 10: rc = RB == 4 ? launch_fused_k<10, 4>(s, p) : launch_fused_k<10, 3>(s, p); break;
+            case 11: rc = RB == 4 ? launch_fused_k<11, 4>(s, p) : launch_fused_k<11, 3>(s, p); break;
+            case 12: rc = RB == 4 ? launch_fused_k<12, 4>(s, p) : launch_fused_k<12, 3>(s, p); break;
+            default: rc = RB == 4 ? launch_fused_k<13, 4>(s, p) : launch_fused_k<13, 3>(s, p); break;
         }
         if (rc) return rc;
         si = sj;

@@ -255,8 +255,9 @@ def entangled(n):
 
 
 class TestFusedEqualsUnfused:
+    @pytest.mark.parametrize("rb", ["3", "4"])
     @pytest.mark.parametrize("n,K", [(10, 10), (12, 11), (13, 13), (16, 12), (18, 13), (19, 14)])
-    def test_random_circuits(self, n, K):
+    def test_random_circuits(self, n, K, rb):
         rng = np.random.default_rng(500 + n)
         a0 = rand_amps(n, rng)
         circ = random_circuit(n, 120, rng)
@@ -267,10 +268,11 @@ class TestFusedEqualsUnfused:
             extra.append(ControlledControlledApply(gate_mix(rng), c1, c2, t))
         circ = Circuit(n, circ.instructions + tuple(extra))
         outs = []
-        for fuse in (False, True):
-            st = load(n, a0)
-            execute(circ, st, fuse=fuse, tile_qubits=K)
-            outs.append(st.amplitudes())
+        with env(QSB_FUSED_RB=rb):
+            for fuse in (False, True):
+                st = load(n, a0)
+                execute(circ, st, fuse=fuse, tile_qubits=K)
+                outs.append(st.amplitudes())
         assert same_values(outs[0], outs[1])
 
     def test_layered_config4_shape(self):
