@@ -71,6 +71,11 @@ typedef struct {
 int qs_abi_version(void);
 const char *qs_last_error(void);
 int qs_device_count(int *out);
+/* Return cached register buffers / streams of `device` (all devices when
+ * device < 0) to the driver.  Destroyed handles park their buffers in a
+ * bounded per-device cache (QSB_CACHE_BYTES, default 1/4 of HBM) so that
+ * new_state-style create/destroy cycles skip cudaMalloc/cudaFree. */
+int qs_release_cached(int device);
 
 /* ---- lifecycle: pkg/src/pairsim/state.py:122-143 (new_state) ------------ */
 /* Allocates 8 * 2^n bytes on `device` and initialises |0...0>.

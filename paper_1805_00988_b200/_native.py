@@ -21,7 +21,7 @@ QS_OP_PAIR, QS_OP_PHASE = 0, 1
 
 # Every symbol include/qsb200.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
-    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_create", "qs_destroy",
+    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_release_cached", "qs_create", "qs_destroy",
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
     "qs_apply_controlled_controlled_gate", "qs_apply_fused", "qs_swap_qubits",
@@ -56,6 +56,7 @@ def _declare(L):
         "qs_abi_version": ([], i32),
         "qs_last_error": ([], ctypes.c_char_p),
         "qs_device_count": ([ctypes.POINTER(i32)], i32),
+        "qs_release_cached": ([i32], i32),
         "qs_create": ([i32, i32, u64, ctypes.POINTER(vp)], i32),
         "qs_destroy": ([vp], i32),
         "qs_num_qubits": ([vp, ctypes.POINTER(i32)], i32),

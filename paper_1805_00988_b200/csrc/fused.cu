@@ -454,6 +454,81 @@ int launch_fused_k(qs_state *s, const FParams &p) {
     return QS_OK;
 }
 
+// ---- small registers (n <= 13): the whole state in shared memory ------------
+// One CTA loads the register (<= 64 KB), applies every op in order with the
+// exact pair/phase arithmetic of the sweep kernels, and writes it back: one
+// launch per circuit instead of one per gate, for registers too small to fill
+// the GPU anyway.
+struct SOp {
+    int kind, target;
+    uint64_t ctrl_mask;
+    float m[8];
+};
+constexpr int kSmallMaxOps = 640;
+constexpr int kSmallMaxQubits = 13;
+struct SParams {
+    int n, nops;
+    SOp ops[kSmallMaxOps];
+};
+static_assert(sizeof(SParams) < 32000, "kernel parameter block too large");
+
+__global__ void __launch_bounds__(1024) k_small(float2 *__restrict__ amps,
+                                                const __grid_constant__ SParams p) {
+    extern __shared__ float2 sv[];
+    const int N = 1 << p.n;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sv[i] = amps[i];
+    __syncthreads();
+    for (int o = 0; o < p.nops; ++o) {
+        const SOp &op = p.ops[o];
+        const uint32_t cm = (uint32_t)op.ctrl_mask;
+        if (op.kind == QS_OP_PHASE) {
+            const uint32_t mask = cm | (1u << op.target);
+            const float2 d = make_float2(op.m[6], op.m[7]);
+            for (int i = threadIdx.x; i < N; i += blockDim.x)
+                if ((i & mask) == mask) sv[i] = cmul(d, sv[i]);
+        } else {
+            const Gate2 g = gate_from(op.m);
+            const uint32_t tbit = 1u << op.target;
+            for (int k = threadIdx.x; k < (N >> 1); k += blockDim.x) {
+                const uint32_t a = (uint32_t)insert_zero((uint64_t)k, op.target);
+                if ((a & cm) != cm) continue;
+                float2 va = sv[a], vb = sv[a | tbit];
+                pair_update(g, va, vb);
+                sv[a] = va;
+                sv[a | tbit] = vb;
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) amps[i] = sv[i];
+}
+
+int run_small(qs_state *s, const qs_op *ops, int nops) {
+    static bool configured = false;
+    if (!configured) {
+        QS_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(8u << kSmallMaxQubits)));
+        configured = true;
+    }
+    SParams p;
+    std::memset(&p, 0, sizeof p);
+    p.n = s->num_qubits;
+    const int threads = (1 << p.n) >= 2048 ? 1024 : ((1 << p.n) / 2 < 32 ? 32 : (1 << p.n) / 2);
+    for (int base = 0; base < nops; base += kSmallMaxOps) {
+        p.nops = nops - base < kSmallMaxOps ? nops - base : kSmallMaxOps;
+        for (int i = 0; i < p.nops; ++i) {
+            const qs_op &op = ops[base + i];
+            p.ops[i].kind = op.kind;
+            p.ops[i].target = op.target;
+            p.ops[i].ctrl_mask = op.ctrl_mask;
+            std::memcpy(p.ops[i].m, op.m, sizeof op.m);
+        }
+        k_small<<<1, threads, 8u << p.n, s->stream>>>(s->amps, p);
+        QS_CUDA(cudaGetLastError());
+    }
+    return QS_OK;
+}
+
 int gate_class(const float m[8]) {
     const bool real = m[1] == 0.f && m[3] == 0.f && m[5] == 0.f && m[7] == 0.f;
     if (!real) return kCplx;
@@ -562,9 +637,10 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     const int K = __builtin_popcountll(tile_mask);
     const uint64_t low_mask = (1ull << kLow) - 1ull;
     const bool kernel_ok = n >= 10 && K >= 10 && K <= 13 && (tile_mask & low_mask) == low_mask;
+    if (!kernel_ok && n <= kSmallMaxQubits) return run_small(s, ops, nops);
     if (!kernel_ok) {
-        // Registers below 10 qubits (or an unsupported tile shape): one sweep
-        // per op — the same arithmetic, one HBM pass per op.
+        // Unsupported tile shape on a large register: one sweep per op — the
+        // same arithmetic, one HBM pass per op.
         for (int i = 0; i < nops; ++i) {
             const qs_op &op = ops[i];
             int rc = op.kind == QS_OP_PHASE

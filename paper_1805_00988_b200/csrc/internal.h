@@ -46,6 +46,14 @@ struct DeviceGuard {
 int ensure_scratch(qs_state *s, size_t bytes);
 int ensure_pinned(qs_state *s, size_t bytes);
 
+// device-memory / stream caches (pool.cu)
+cudaError_t pool_alloc(int device, size_t bytes, void **out);
+void pool_free(int device, void *ptr, size_t bytes);
+size_t pool_cached(int device);
+void pool_trim(int device);
+cudaError_t stream_acquire(int device, cudaStream_t *out);
+void stream_release(int device, cudaStream_t s);
+
 // kernels (gates.cu / measure.cu / fused.cu)
 int launch_sweep(qs_state *s, int target, uint64_t ctrl_mask, const float m[8]);
 int launch_phase(qs_state *s, uint64_t mask, float2 d);

@@ -36,6 +36,7 @@
 // reference's cdf[j] / total bit for bit.
 
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -346,22 +347,63 @@ __global__ void k_draws(const float2 *__restrict__ amps, uint64_t nch, int clog,
 
 }  // namespace
 
+// Host-side copy of one staged piece, split over a few threads (a single
+// memcpy thread caps at ~10 GB/s, well below the PCIe D2H rate).
+static void parallel_memcpy(void *dst, const void *src, size_t bytes) {
+    const size_t kThreadsMax = 8, kMinPer = 4u << 20;
+    size_t nt = bytes / kMinPer;
+    if (nt > kThreadsMax) nt = kThreadsMax;
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (bytes + nt - 1) / nt;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t lo = t * per, hi = lo + per < bytes ? lo + per : bytes;
+        if (lo >= hi) break;
+        th.emplace_back([=] { std::memcpy((char *)dst + lo, (const char *)src + lo, hi - lo); });
+    }
+    for (auto &x : th) x.join();
+}
+
+// probabilities into a (pageable) host array: |a|^2 pieces computed on the
+// device, copied D2H into two pinned staging buffers, and drained to `host`
+// by host threads while the next piece is in flight.
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host) {
-    const uint64_t piece = 1ull << 25;  // 256 MiB of fp64 per staging round
+    const uint64_t piece = 1ull << 22;  // 32 MiB of fp64 per staging round
     const uint64_t step = count < piece ? count : piece;
-    int rc = ensure_scratch(s, step * sizeof(double));
+    int rc = ensure_scratch(s, 2 * step * sizeof(double));
     if (rc) return rc;
-    double *dev = (double *)s->scratch;
-    for (uint64_t done = 0; done < count; done += step) {
+    rc = ensure_pinned(s, 2 * step * sizeof(double));
+    if (rc) return rc;
+    double *dev[2] = {(double *)s->scratch, (double *)s->scratch + step};
+    double *pin[2] = {(double *)s->pinned, (double *)s->pinned + step};
+    cudaEvent_t ev[2];
+    QS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    QS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    uint64_t prev_off = 0, prev_len = 0;
+    int b = 0;
+    for (uint64_t done = 0; done < count; done += step, b ^= 1) {
         const uint64_t m = (count - done) < step ? (count - done) : step;
         unsigned grid = (unsigned)((m + 255) / 256);
         if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
-        k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, dev, m);
+        k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, dev[b], m);
         QS_CUDA(cudaGetLastError());
-        QS_CUDA(cudaMemcpyAsync(host + done, dev, m * sizeof(double), cudaMemcpyDeviceToHost,
+        QS_CUDA(cudaMemcpyAsync(pin[b], dev[b], m * sizeof(double), cudaMemcpyDeviceToHost,
                                 s->stream));
-        QS_CUDA(cudaStreamSynchronize(s->stream));
+        QS_CUDA(cudaEventRecord(ev[b], s->stream));
+        if (prev_len) {  // drain the previous piece while this one is in flight
+            QS_CUDA(cudaEventSynchronize(ev[b ^ 1]));
+            parallel_memcpy(host + prev_off, pin[b ^ 1], prev_len * sizeof(double));
+        }
+        prev_off = done;
+        prev_len = m;
     }
+    QS_CUDA(cudaEventSynchronize(ev[b ^ 1]));
+    parallel_memcpy(host + prev_off, pin[b ^ 1], prev_len * sizeof(double));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
     return QS_OK;
 }
 

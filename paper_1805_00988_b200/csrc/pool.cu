@@ -1,0 +1,130 @@
+// Device-memory and stream caches for register handles.
+//
+// pairsim allocates a fresh register per run (state.py:122-143) and the
+// paper's benchmark times that allocation, so repeated
+// State(n) / qs_destroy cycles are on the measured path.  cudaMalloc/cudaFree
+// (the latter synchronises the device) and stream creation cost ~0.1-1 ms;
+// this cache keeps freed register buffers (exact-size reuse) and streams per
+// device, bounded by QSB_CACHE_BYTES (default: 1/4 of the device memory).
+// A failed cudaMalloc trims the cache and retries; the memory budget check
+// counts cached bytes as free.
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace qsb {
+
+namespace {
+
+struct DevCache {
+    std::multimap<size_t, void *> blocks;
+    size_t cached = 0;
+    std::vector<cudaStream_t> streams;
+};
+
+std::mutex g_mu;
+std::map<int, DevCache> g_cache;
+
+size_t cache_limit(int device) {
+    const char *e = std::getenv("QSB_CACHE_BYTES");
+    if (e && *e) return (size_t)std::strtoull(e, nullptr, 10);
+    size_t free_b = 0, total_b = 0;
+    DeviceGuard guard(device);
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
+    return total_b / 4;
+}
+
+}  // namespace
+
+cudaError_t pool_alloc(int device, size_t bytes, void **out) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        DevCache &c = g_cache[device];
+        auto it = c.blocks.find(bytes);
+        if (it != c.blocks.end()) {
+            *out = it->second;
+            c.cached -= bytes;
+            c.blocks.erase(it);
+            return cudaSuccess;
+        }
+    }
+    DeviceGuard guard(device);
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        pool_trim(device);
+        e = cudaMalloc(out, bytes);
+    }
+    return e;
+}
+
+void pool_free(int device, void *ptr, size_t bytes) {
+    if (!ptr) return;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        DevCache &c = g_cache[device];
+        const size_t lim = cache_limit(device);
+        if (c.cached + bytes <= lim) {
+            c.blocks.emplace(bytes, ptr);
+            c.cached += bytes;
+            return;
+        }
+    }
+    DeviceGuard guard(device);
+    cudaFree(ptr);
+}
+
+size_t pool_cached(int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(device);
+    return it == g_cache.end() ? 0 : it->second.cached;
+}
+
+void pool_trim(int device) {
+    std::vector<void *> ptrs;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        DevCache &c = g_cache[device];
+        for (auto &kv : c.blocks) ptrs.push_back(kv.second);
+        c.blocks.clear();
+        c.cached = 0;
+    }
+    DeviceGuard guard(device);
+    for (void *p : ptrs) cudaFree(p);
+}
+
+cudaError_t stream_acquire(int device, cudaStream_t *out) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        DevCache &c = g_cache[device];
+        if (!c.streams.empty()) {
+            *out = c.streams.back();
+            c.streams.pop_back();
+            return cudaSuccess;
+        }
+    }
+    DeviceGuard guard(device);
+    return cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+}
+
+void stream_release(int device, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_cache[device].streams.push_back(s);
+}
+
+}  // namespace qsb
+
+extern "C" int qs_release_cached(int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+        cudaGetLastError();
+        return qsb::set_error(QS_ERR_CUDA, "no CUDA device");
+    }
+    for (int d = 0; d < ndev; ++d)
+        if (device < 0 || d == device) qsb::pool_trim(d);
+    return QS_OK;
+}

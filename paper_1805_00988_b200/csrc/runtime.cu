@@ -30,11 +30,11 @@ int ensure_scratch(qs_state *s, size_t bytes) {
     if (s->scratch_bytes >= bytes) return QS_OK;
     if (s->scratch) {
         QS_CUDA(cudaStreamSynchronize(s->stream));
-        QS_CUDA(cudaFree(s->scratch));
+        pool_free(s->device, s->scratch, s->scratch_bytes);
         s->scratch = nullptr;
         s->scratch_bytes = 0;
     }
-    QS_CUDA(cudaMalloc(&s->scratch, bytes));
+    QS_CUDA(pool_alloc(s->device, bytes, &s->scratch));
     s->scratch_bytes = bytes;
     return QS_OK;
 }
@@ -121,7 +121,9 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
     DeviceGuard guard(device);
     size_t free_b = 0, total_b = 0;
     QS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    unsigned long long budget = memory_budget ? memory_budget : (unsigned long long)free_b * 3 / 4;
+    // cached register buffers (pool.cu) are reusable, so they count as free
+    unsigned long long budget =
+        memory_budget ? memory_budget : (unsigned long long)(free_b + pool_cached(device)) * 3 / 4;
     // need_bytes = memory_required // 8 = 8 * 2^n (state.py:71-83, 134)
     if (num_qubits > 60 || (8ull << num_qubits) > budget) {
         std::string need = num_qubits > 60 ? std::string("more than 2^63 bytes")
@@ -134,7 +136,7 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
     std::memset(s, 0, sizeof *s);
     s->num_qubits = num_qubits;
     s->device = device;
-    cudaError_t e = cudaMalloc(&s->amps, 8ull << num_qubits);
+    cudaError_t e = pool_alloc(device, 8ull << num_qubits, (void **)&s->amps);
     if (e != cudaSuccess) {
         delete s;
         cudaGetLastError();
@@ -142,17 +144,17 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
                                               std::to_string(8ull << num_qubits) +
                                               " bytes failed: " + cudaGetErrorString(e));
     }
-    e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    e = stream_acquire(device, &s->stream);
     if (e != cudaSuccess) {
-        cudaFree(s->amps);
+        pool_free(device, s->amps, 8ull << num_qubits);
         delete s;
         return cuda_fail(e, "cudaStreamCreateWithFlags");
     }
     cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
     int rc = launch_reset(s, 0);
     if (rc != QS_OK) {
-        cudaStreamDestroy(s->stream);
-        cudaFree(s->amps);
+        stream_release(device, s->stream);
+        pool_free(device, s->amps, 8ull << num_qubits);
         delete s;
         return rc;
     }
@@ -163,12 +165,12 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
 int qs_destroy(qs_state *s) {
     if (!s) return QS_OK;
     DeviceGuard guard(s->device);
-    cudaStreamSynchronize(s->stream);
-    if (s->amps) cudaFree(s->amps);
-    if (s->scratch) cudaFree(s->scratch);
+    cudaStreamSynchronize(s->stream);  // the buffers may be recycled right away
+    pool_free(s->device, s->amps, 8ull << s->num_qubits);
+    pool_free(s->device, s->scratch, s->scratch_bytes);
     if (s->ops_dev) cudaFree(s->ops_dev);
     if (s->pinned) cudaFreeHost(s->pinned);
-    cudaStreamDestroy(s->stream);
+    stream_release(s->device, s->stream);
     delete s;
     return QS_OK;
 }

@@ -275,6 +275,40 @@ class TestFusedEqualsUnfused:
                 outs.append(st.amplitudes())
         assert same_values(outs[0], outs[1])
 
+    @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 12, 13])
+    def test_small_register_single_launch(self, n):
+        """n < 10 fused passes run in one shared-memory launch (k_small)."""
+        rng = np.random.default_rng(600 + n)
+        a0 = rand_amps(n, rng)
+        circ = random_circuit(n, 150, rng)
+        if n >= 3:
+            extra = []
+            for _ in range(10):
+                c1, c2, t = (int(x) for x in rng.choice(n, 3, replace=False))
+                extra.append(ControlledControlledApply(gate_mix(rng), c1, c2, t))
+            circ = Circuit(n, circ.instructions + tuple(extra))
+        ref = a0.copy()
+        for ins in circ.instructions:
+            if isinstance(ins, Apply):
+                oc.apply_gate(ref, ins.target, ins.gate)
+            elif isinstance(ins, ControlledApply):
+                oc.apply_controlled_gate(ref, ins.control, ins.target, ins.gate)
+            else:
+                oc.apply_cc_gate(ref, ins.control1, ins.control2, ins.target, ins.gate)
+        st = load(n, a0)
+        execute(circ, st, fuse=True, tile_qubits=n)
+        assert same_values(st.amplitudes(), ref)
+
+    def test_register_cache_reuse(self):
+        """Destroyed registers park their buffers; a new one starts at |0>."""
+        for _ in range(3):
+            st = State(18)
+            st.h(3)
+            st.close()
+        st = State(18)
+        assert st.amplitude(0) == 1 and st.norm_squared() == 1.0
+        assert np.count_nonzero(st.amplitudes()) == 1
+
     def test_layered_config4_shape(self):
         n = 20
         circ = layered_random_circuit(n, 6, seed=32)
