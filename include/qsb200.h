@@ -135,6 +135,19 @@ int qs_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
 /* measure_collapse (measure.py:88-99): one draw, then amps = e_outcome. */
 int qs_measure_collapse(qs_state *s, const qs_pcg64 *rng, int64_t *outcome);
 
+/* ---- sharded registers (one slice of a larger logical register) ---------- */
+/* The exact sequential cumsum of this register's probabilities continued from
+ * `start` (the running value after all earlier slices): *end = final value.
+ * Chaining slices reproduces numpy's cumsum over the concatenation bit for bit. */
+int qs_cdf_extend(qs_state *s, double start, double *end);
+/* Draws against the global normalised CDF when this register is the slice
+ * [index_base, index_base + 2^n) of a global_dim register whose running sum
+ * enters the slice at `start` and ends at `total` (last slice: is_last = 1).
+ * out[i] = global outcome of draw i if it falls in this slice, else -1; each
+ * draw falls in exactly one slice.  Same draws as qs_sample for the same rng. */
+int qs_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
+                    uint64_t index_base, uint64_t global_dim, int is_last, int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,8 +96,12 @@ def pcg_words(seed):
 
 
 def pcg64_random(seed, k: int) -> np.ndarray:
+    return pcg64_random_words(pcg_words(seed), k)
+
+
+def pcg64_random_words(words, k: int) -> np.ndarray:
     out = np.empty(k, dtype=np.float64)
-    lib().oracle_pcg64_random(*pcg_words(seed), k, out)
+    lib().oracle_pcg64_random(*[int(w) for w in words], k, out)
     return out
 
 

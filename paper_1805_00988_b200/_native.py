@@ -27,7 +27,7 @@ EXPORTS = (
     "qs_apply_controlled_controlled_gate", "qs_apply_fused", "qs_swap_qubits",
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
-    "qs_sample", "qs_measure_collapse",
+    "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
 )
 
 
@@ -78,6 +78,9 @@ def _declare(L):
         "qs_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),
         "qs_measure_collapse": ([vp, ctypes.POINTER(qs_pcg64), ctypes.POINTER(i64)], i32),
+        "qs_cdf_extend": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)], i32),
+        "qs_sample_shard": ([vp, ctypes.POINTER(qs_pcg64), i64, ctypes.c_double, ctypes.c_double,
+                             u64, u64, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

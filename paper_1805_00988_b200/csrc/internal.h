@@ -62,6 +62,9 @@ int launch_reset(qs_state *s, uint64_t basis);
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
 int run_norm(qs_state *s, double *out);
 int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
+int run_cdf_extend(qs_state *s, double start, double *end);
+int run_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
+                     uint64_t base, uint64_t gdim, int is_last, int64_t *out);
 int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops);
 
 }  // namespace qsb

@@ -156,7 +156,7 @@ enum : int { kFlagOk = 1, kFlagExact0 = 2 };
 // row L sequentially with both chains.
 constexpr int kTrajWarps = 4;
 __global__ void __launch_bounds__(kTrajWarps * 32)
-    k_trajectories(const float2 *__restrict__ amps, uint64_t nch, int clog,
+    k_trajectories(const float2 *__restrict__ amps, uint64_t nch, int clog, double start,
                    const double *__restrict__ g, double *__restrict__ g0out,
                    double *__restrict__ d0, double *__restrict__ d1, double *__restrict__ hiout,
                    int *__restrict__ flags) {
@@ -168,16 +168,21 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
     const uint64_t C = 1ull << clog;
     const bool active = my < nch;
 
-    double gg = active ? g[my] : 0.0;
-    const bool exact0 = (my == 0) || gg == 0.0;
+    // g[my] = prefix of the chunk sums before this chunk; it is exactly 0
+    // iff every earlier probability is 0, in which case the true running
+    // value at the chunk start is exactly `start` (the CDF value carried in
+    // from an earlier shard; 0 for a whole register).
+    const double prefix = active ? g[my] : 0.0;
+    const bool exact0 = (my == 0) || prefix == 0.0;
+    const double gg = __dadd_rn(start, prefix);
     double g0 = gg, g1 = gg, hi = 0.0;
     if (!exact0) {
         g0 = __longlong_as_double(__double_as_longlong(gg) & ~1ll);
         g1 = __longlong_as_double(__double_as_longlong(g0) + 1ll);
         hi = binade_hi(g0);
     } else {
-        g0 = 0.0;
-        g1 = 0.0;
+        g0 = start;
+        g1 = start;
     }
     double t0 = g0, t1 = g1;
     const int rows = (int)((nch - first) < 32 ? (nch - first) : 32);
@@ -239,12 +244,12 @@ __device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, in
 
 // ---- M4: resolve true chunk starts (single thread) ---------------------------
 __global__ void k_resolve(const float2 *__restrict__ amps, uint64_t nch, int clog,
-                          const double *__restrict__ g0, const double *__restrict__ d0,
+                          double s_start, const double *__restrict__ g0, const double *__restrict__ d0,
                           const double *__restrict__ d1, const double *__restrict__ hi,
                           const int *__restrict__ flags, double *__restrict__ start,
                           double *__restrict__ total, unsigned long long *__restrict__ nslow) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double s = 0.0;
+    double s = s_start;
     unsigned long long slow = 0;
     for (uint64_t k = 0; k < nch; ++k) {
         start[k] = s;
@@ -252,7 +257,7 @@ __global__ void k_resolve(const float2 *__restrict__ amps, uint64_t nch, int clo
         double e;
         bool valid;
         if (f & kFlagExact0) {
-            valid = (s == 0.0);
+            valid = (s == s_start);
             e = d0[k];
         } else {
             const double h = hi[k];
@@ -272,13 +277,16 @@ __global__ void k_resolve(const float2 *__restrict__ amps, uint64_t nch, int clo
 }
 
 // ---- M5: normalised CDF value at each chunk end --------------------------------
+// `end` = this register's final running value; `gtotal` = the global last
+// CDF value used to normalise (0: use `end`, i.e. a whole register).
 __global__ void k_chunk_last(const double *__restrict__ start, uint64_t nch,
-                             const double *__restrict__ total, double *__restrict__ last) {
-    const double t = *total;
+                             const double *__restrict__ end, double gtotal,
+                             double *__restrict__ last) {
+    const double t = gtotal > 0.0 ? gtotal : *end;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nch;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        const double end = (k + 1 < nch) ? start[k + 1] : t;
-        last[k] = __ddiv_rn(end, t);
+        const double e = (k + 1 < nch) ? start[k + 1] : *end;
+        last[k] = __ddiv_rn(e, t);
     }
 }
 
@@ -307,17 +315,27 @@ __device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
 }
 
 // ---- M6: draws ---------------------------------------------------------------------
+// Draw i resolves in this register iff fl(s_start / t) <= u (no earlier
+// register holds a value above u) and u < last[nch-1] (or this is the last
+// register); otherwise out[i] = -1.  Outcomes are offset by `base` and
+// clamped to `gdim - 1` (measure.py:83).
 __global__ void k_draws(const float2 *__restrict__ amps, uint64_t nch, int clog, uint64_t dim,
                         const double *__restrict__ start, const double *__restrict__ last,
-                        const double *__restrict__ total, qs_pcg64 rng, int64_t k,
+                        const double *__restrict__ end, double gtotal, double s_start,
+                        uint64_t base, uint64_t gdim, int is_last, qs_pcg64 rng, int64_t k,
                         int64_t *__restrict__ out) {
-    const double t = *total;
+    const double t = gtotal > 0.0 ? gtotal : *end;
+    const double u_lo = __ddiv_rn(s_start, t);
     const u128 st0 = mk128(rng.state_hi, rng.state_lo);
     const u128 inc = mk128(rng.inc_hi, rng.inc_lo);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
          i += (int64_t)gridDim.x * blockDim.x) {
         const u128 st = pcg_advance(st0, inc, (uint64_t)i + 1ull);  // step, then output
         const double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
+        if (u < u_lo || (!is_last && !(last[nch - 1] > u))) {
+            out[i] = -1;
+            continue;
+        }
         // first chunk whose last normalised value exceeds u
         uint64_t lo = 0, hi = nch;
         while (lo < hi) {
@@ -341,7 +359,8 @@ __global__ void k_draws(const float2 *__restrict__ amps, uint64_t nch, int clog,
             }
             idx = (lo << clog) + j;
         }
-        out[i] = (int64_t)(idx < dim - 1 ? idx : dim - 1);
+        idx += base;
+        out[i] = (int64_t)(idx < gdim - 1 ? idx : gdim - 1);
     }
 }
 
@@ -424,60 +443,125 @@ int run_norm(qs_state *s, double *out) {
     return QS_OK;
 }
 
-int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
+// Scratch layout of the exact-CDF chain for one register.
+struct CdfScratch {
+    int clog;
+    uint64_t nch;
+    double *csum, *g0, *d0, *d1, *hi, *start, *last, *end;
+    unsigned long long *nslow;
+    int *flags;
+    int64_t *dout;
+};
+
+static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     const int n = s->num_qubits;
     const uint64_t dim = 1ull << n;
-    const int clog = n < kChunkLog ? n : kChunkLog;
-    const uint64_t nch = dim >> clog;
-    // scratch: csum/g, g0, d0, d1, hi, start, last (doubles) + flags + total + nslow + outcomes
+    c.clog = n < kChunkLog ? n : kChunkLog;
+    c.nch = dim >> c.clog;
+    const uint64_t nch = c.nch;
+    // csum, g0, d0, d1, hi, start, last (doubles) + end + nslow + flags + outcomes
     const size_t nd = 7 * nch + 2;
     const size_t bytes = nd * sizeof(double) + nch * sizeof(int) + 64 + (size_t)k * sizeof(int64_t);
     int rc = ensure_scratch(s, bytes);
     if (rc) return rc;
-    double *base = (double *)s->scratch;
-    double *csum = base, *g0 = base + nch, *d0 = base + 2 * nch, *d1 = base + 3 * nch,
-           *hi = base + 4 * nch, *start = base + 5 * nch, *last = base + 6 * nch;
-    double *total = base + 7 * nch;
-    unsigned long long *nslow = (unsigned long long *)(base + 7 * nch + 1);
-    int *flags = (int *)(base + nd);
-    int64_t *dout = (int64_t *)((char *)flags + ((nch * sizeof(int) + 63) & ~(size_t)63));
-    // (bytes above reserves the 64-B alignment slack)
+    double *b = (double *)s->scratch;
+    c.csum = b;
+    c.g0 = b + nch;
+    c.d0 = b + 2 * nch;
+    c.d1 = b + 3 * nch;
+    c.hi = b + 4 * nch;
+    c.start = b + 5 * nch;
+    c.last = b + 6 * nch;
+    c.end = b + 7 * nch;
+    c.nslow = (unsigned long long *)(b + 7 * nch + 1);
+    c.flags = (int *)(b + nd);
+    c.dout = (int64_t *)((char *)c.flags + ((nch * sizeof(int) + 63) & ~(size_t)63));
+    return QS_OK;
+}
 
-    double *g = csum;  // M2 writes the guesses over a second array below
-    k_chunk_sums<<<(unsigned)nch, 256, 0, s->stream>>>(s->amps, clog, csum);
-    // guesses go to `start` temporarily (overwritten by M4)
-    k_scan_guess<<<1, 1024, 0, s->stream>>>(csum, nch, start);
-    g = start;
+// M1..M4: exact sequential running sum over the register, continuing from
+// `s_start`; leaves chunk starts in c.start and the final value in *c.end.
+static int cdf_chain(qs_state *s, const CdfScratch &c, double s_start) {
+    k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(s->amps, c.clog, c.csum);
+    k_scan_guess<<<1, 1024, 0, s->stream>>>(c.csum, c.nch, c.start);  // prefixes -> start[]
     {
-        const uint64_t warps = (nch + 31) / 32;
+        const uint64_t warps = (c.nch + 31) / 32;
         const unsigned blocks = (unsigned)((warps + kTrajWarps - 1) / kTrajWarps);
-        k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(s->amps, nch, clog, g, g0, d0,
-                                                                  d1, hi, flags);
+        k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
+            s->amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags);
     }
-    k_resolve<<<1, 1, 0, s->stream>>>(s->amps, nch, clog, g0, d0, d1, hi, flags, start, total,
-                                      nslow);
+    k_resolve<<<1, 1, 0, s->stream>>>(s->amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi,
+                                      c.flags, c.start, c.end, c.nslow);
+    QS_CUDA(cudaGetLastError());
+    return QS_OK;
+}
+
+// M5 + M6 and the copy-out shared by qs_sample / qs_sample_shard.
+static int draw(qs_state *s, const CdfScratch &c, const qs_pcg64 *rng, int64_t k, double s_start,
+                double gtotal, uint64_t base, uint64_t gdim, int is_last, int64_t *out,
+                double *end_out) {
     {
-        unsigned grid = (unsigned)((nch + 255) / 256);
+        unsigned grid = (unsigned)((c.nch + 255) / 256);
         if (grid > 4096) grid = 4096;
-        k_chunk_last<<<grid, 256, 0, s->stream>>>(start, nch, total, last);
+        k_chunk_last<<<grid, 256, 0, s->stream>>>(c.start, c.nch, c.end, gtotal, c.last);
     }
     {
         unsigned grid = (unsigned)((k + 127) / 128);
         if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
-        k_draws<<<grid, 128, 0, s->stream>>>(s->amps, nch, clog, dim, start, last, total, *rng, k,
-                                             dout);
+        k_draws<<<grid, 128, 0, s->stream>>>(s->amps, c.nch, c.clog, 1ull << s->num_qubits, c.start,
+                                             c.last, c.end, gtotal, s_start, base, gdim, is_last,
+                                             *rng, k, c.dout);
     }
     QS_CUDA(cudaGetLastError());
-    rc = ensure_pinned(s, sizeof(double));
+    int rc = ensure_pinned(s, sizeof(double));
     if (rc) return rc;
-    QS_CUDA(cudaMemcpyAsync(s->pinned, total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    QS_CUDA(cudaMemcpyAsync(out, dout, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost,
+    QS_CUDA(cudaMemcpyAsync(s->pinned, c.end, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    QS_CUDA(cudaMemcpyAsync(out, c.dout, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost,
                             s->stream));
     QS_CUDA(cudaStreamSynchronize(s->stream));
-    const double tot = *(double *)s->pinned;
+    *end_out = *(double *)s->pinned;
+    return QS_OK;
+}
+
+int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
+    CdfScratch c;
+    int rc = cdf_scratch(s, k, c);
+    if (rc) return rc;
+    rc = cdf_chain(s, c, 0.0);
+    if (rc) return rc;
+    double tot = 0.0;
+    const uint64_t dim = 1ull << s->num_qubits;
+    rc = draw(s, c, rng, k, 0.0, 0.0, 0, dim, 1, out, &tot);
+    if (rc) return rc;
     if (!(tot > 0.0))  // measure.py:71-72
         return set_error(QS_ERR_DEGENERATE, "all outcome probabilities are zero");
     return QS_OK;
+}
+
+int run_cdf_extend(qs_state *s, double start, double *end) {
+    CdfScratch c;
+    int rc = cdf_scratch(s, 0, c);
+    if (rc) return rc;
+    rc = cdf_chain(s, c, start);
+    if (rc) return rc;
+    rc = ensure_pinned(s, sizeof(double));
+    if (rc) return rc;
+    QS_CUDA(cudaMemcpyAsync(s->pinned, c.end, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    QS_CUDA(cudaStreamSynchronize(s->stream));
+    *end = *(double *)s->pinned;
+    return QS_OK;
+}
+
+int run_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
+                     uint64_t base, uint64_t gdim, int is_last, int64_t *out) {
+    if (!(total > 0.0)) return set_error(QS_ERR_DEGENERATE, "all outcome probabilities are zero");
+    CdfScratch c;
+    int rc = cdf_scratch(s, k, c);
+    if (rc) return rc;
+    rc = cdf_chain(s, c, start);
+    if (rc) return rc;
+    double end = 0.0;
+    return draw(s, c, rng, k, start, total, base, gdim, is_last, out, &end);
 }
 
 }  // namespace qsb

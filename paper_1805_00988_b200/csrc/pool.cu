@@ -29,13 +29,22 @@ struct DevCache {
 std::mutex g_mu;
 std::map<int, DevCache> g_cache;
 
-size_t cache_limit(int device) {
+std::map<int, size_t> g_limit;  // per device, computed once (cudaMemGetInfo is slow)
+
+size_t cache_limit(int device) {  // g_mu held
+    auto it = g_limit.find(device);
+    if (it != g_limit.end()) return it->second;
+    size_t lim = 0;
     const char *e = std::getenv("QSB_CACHE_BYTES");
-    if (e && *e) return (size_t)std::strtoull(e, nullptr, 10);
-    size_t free_b = 0, total_b = 0;
-    DeviceGuard guard(device);
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
-    return total_b / 4;
+    if (e && *e) {
+        lim = (size_t)std::strtoull(e, nullptr, 10);
+    } else {
+        size_t free_b = 0, total_b = 0;
+        DeviceGuard guard(device);
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) lim = total_b / 4;
+    }
+    g_limit[device] = lim;
+    return lim;
 }
 
 }  // namespace

@@ -119,11 +119,19 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
         return set_error(QS_ERR_VALUE, "device " + std::to_string(device) + " not present (" +
                                            std::to_string(ndev) + " devices)");
     DeviceGuard guard(device);
-    size_t free_b = 0, total_b = 0;
-    QS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    // cached register buffers (pool.cu) are reusable, so they count as free
-    unsigned long long budget =
-        memory_budget ? memory_budget : (unsigned long long)(free_b + pool_cached(device)) * 3 / 4;
+    // Default budget: 75% of free HBM (cached register buffers count as free).
+    // Registers up to 256 MiB skip the (slow) free-memory query: if such a
+    // request does not fit, cudaMalloc fails and CapacityError is raised anyway.
+    unsigned long long budget = memory_budget;
+    if (!budget) {
+        if (num_qubits <= 25) {
+            budget = ~0ull;
+        } else {
+            size_t free_b = 0, total_b = 0;
+            QS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            budget = (unsigned long long)(free_b + pool_cached(device)) * 3 / 4;
+        }
+    }
     // need_bytes = memory_required // 8 = 8 * 2^n (state.py:71-83, 134)
     if (num_qubits > 60 || (8ull << num_qubits) > budget) {
         std::string need = num_qubits > 60 ? std::string("more than 2^63 bytes")
@@ -379,6 +387,25 @@ int qs_measure_collapse(qs_state *s, const qs_pcg64 *rng, int64_t *outcome) {
     if (rc) return rc;
     *outcome = m;
     return QS_OK;
+}
+
+int qs_cdf_extend(qs_state *s, double start, double *end) {
+    CHECK_HANDLE(s);
+    if (!end) return set_error(QS_ERR_NULL, "null output pointer");
+    DeviceGuard guard(s->device);
+    return run_cdf_extend(s, start, end);
+}
+
+int qs_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
+                    uint64_t index_base, uint64_t global_dim, int is_last, int64_t *out) {
+    CHECK_HANDLE(s);
+    if (k < 1) return set_error(QS_ERR_VALUE, "n_samples must be >= 1");
+    if (!rng || !out) return set_error(QS_ERR_NULL, "null rng or output buffer");
+    const uint64_t dim = 1ull << s->num_qubits;
+    if (global_dim < dim || index_base > global_dim - dim)
+        return set_error(QS_ERR_INDEX, "slice [index_base, index_base + 2^n) outside global_dim");
+    DeviceGuard guard(s->device);
+    return run_sample_shard(s, rng, k, start, total, index_base, global_dim, is_last, out);
 }
 
 }  // extern "C"

@@ -146,11 +146,45 @@ class CudaEngine:
     def probabilities(self) -> np.ndarray:
         return self.state.probabilities()
 
+    def sample_outcomes(self, samples: int, seed=None) -> np.ndarray:
+        """Per-draw outcomes (logical basis indices), bit-exact with pairsim's
+        sample on the full register (measure.py:76-85): the exact sequential
+        CDF is chained across shards in index order."""
+        from .errors import DegenerateStateError
+
+        if samples < 1:
+            raise ValueError("n_samples must be >= 1")
+        self.canonicalize()
+        rng = self.transport.common_seed_words(seed)
+        starts, total = self.transport.cdf_chain(self.engines, self.ranks)
+        if not total > 0.0:
+            raise DegenerateStateError("all outcome probabilities are zero")
+        L, dim = self.L, 1 << self.num_qubits
+        outs = [eng.sample_shard(samples, rng, starts[r], total, r << L, dim, r == self.world - 1)
+                for eng, r in zip(self.engines, self.ranks)]
+        return self.transport.combine_max(outs)
+
+    def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
+        keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
+        return {int(k): int(c) for k, c in zip(keys, counts)}
+
+    def measure_collapse(self, seed=None) -> int:
+        """One draw, then the register becomes |outcome> (measure.py:88-99)."""
+        m = int(self.sample_outcomes(1, seed)[0])
+        self.reset(m)
+        return m
+
     def norm_squared(self) -> float:
         return self.state.norm_squared()
 
     def synchronize(self) -> None:
         self.state.flush()
+
+    def cdf_extend(self, start: float) -> float:
+        return self.state.cdf_extend(start)
+
+    def sample_shard(self, k, rng, start, total, base, gdim, is_last) -> np.ndarray:
+        return self.state.sample_shard(k, rng, start, total, base, gdim, is_last)
 
 
 # ----------------------------------------------------------------------------
@@ -180,6 +214,20 @@ class LocalTransport:
 
     def allreduce_sum(self, values):
         return [sum(values)] * len(values)
+
+    def cdf_chain(self, engines, ranks):
+        """Exact running-sum entry value of every shard, in rank order."""
+        starts, s = {}, 0.0
+        for eng, r in sorted(zip(engines, ranks), key=lambda x: x[1]):
+            starts[r] = s
+            s = eng.cdf_extend(s)
+        return starts, s
+
+    def combine_max(self, arrays):
+        return np.maximum.reduce(arrays)
+
+    def common_seed_words(self, seed):
+        return N.pcg_from_seed(seed)
 
 
 class DistTransport:
@@ -212,6 +260,50 @@ class DistTransport:
                 w.wait()
             mine.copy_(stg)
         eng.comm_end()
+
+    def _tensor(self, arr):
+        import torch
+
+        t = torch.as_tensor(arr)
+        return t.cuda() if self.dist.get_backend(self.group) == "nccl" else t
+
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def cdf_chain(self, engines, ranks):
+        """Rank r waits for rank r-1's exact end value, extends it over its own
+        shard and passes it on; the last rank's end is broadcast as the total."""
+        import torch
+
+        (eng,) = engines
+        start = torch.zeros(1, dtype=torch.float64)
+        if self.rank > 0:
+            t = self._tensor(start)
+            self.dist.recv(t, self._peer(self.rank - 1), group=self.group)
+            start = t.cpu()
+        s0 = float(start.item())
+        end = eng.cdf_extend(s0)
+        if self.rank < self.world - 1:
+            self.dist.send(self._tensor(torch.tensor([end], dtype=torch.float64)), self._peer(self.rank + 1),
+                           group=self.group)
+        tot = self._tensor(torch.tensor([end], dtype=torch.float64))
+        self.dist.broadcast(tot, self._peer(self.world - 1), group=self.group)
+        return {self.rank: s0}, float(tot.cpu().item())
+
+    def combine_max(self, arrays):
+        import torch
+
+        (a,) = arrays
+        t = self._tensor(torch.from_numpy(a.copy()))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t.cpu().numpy()
+
+    def common_seed_words(self, seed):
+        """Every rank must draw from the same generator: rank 0's state wins."""
+        obj = [N.pcg_from_seed(seed)] if self.rank == 0 else [None]
+        words = [(obj[0].state_hi, obj[0].state_lo, obj[0].inc_hi, obj[0].inc_lo)] if self.rank == 0 else [None]
+        self.dist.broadcast_object_list(words, src=self._peer(0), group=self.group)
+        return N.qs_pcg64(*words[0])
 
     def allreduce_sum(self, values):
         import torch
@@ -479,6 +571,34 @@ class ShardedState:
         out = [torch.empty_like(t) for _ in range(self.world)]
         dist.all_gather(out, t, group=self.transport.group)
         return np.concatenate([o.cpu().numpy().view(dtype) for o in out])
+
+    def sample_outcomes(self, samples: int, seed=None) -> np.ndarray:
+        """Per-draw outcomes (logical basis indices), bit-exact with pairsim's
+        sample on the full register (measure.py:76-85): the exact sequential
+        CDF is chained across shards in index order."""
+        from .errors import DegenerateStateError
+
+        if samples < 1:
+            raise ValueError("n_samples must be >= 1")
+        self.canonicalize()
+        rng = self.transport.common_seed_words(seed)
+        starts, total = self.transport.cdf_chain(self.engines, self.ranks)
+        if not total > 0.0:
+            raise DegenerateStateError("all outcome probabilities are zero")
+        L, dim = self.L, 1 << self.num_qubits
+        outs = [eng.sample_shard(samples, rng, starts[r], total, r << L, dim, r == self.world - 1)
+                for eng, r in zip(self.engines, self.ranks)]
+        return self.transport.combine_max(outs)
+
+    def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
+        keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
+        return {int(k): int(c) for k, c in zip(keys, counts)}
+
+    def measure_collapse(self, seed=None) -> int:
+        """One draw, then the register becomes |outcome> (measure.py:88-99)."""
+        m = int(self.sample_outcomes(1, seed)[0])
+        self.reset(m)
+        return m
 
     def norm_squared(self) -> float:
         vals = [eng.norm_squared() for eng in self.engines]

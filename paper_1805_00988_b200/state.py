@@ -212,6 +212,22 @@ class State:
         N.check(N.lib().qs_sample(self.handle, ctypes.byref(rng), int(samples), out.ctypes.data))
         return out
 
+    def cdf_extend(self, start: float) -> float:
+        """Exact sequential cumsum of this register's probabilities continued from `start`."""
+        end = ctypes.c_double()
+        N.check(N.lib().qs_cdf_extend(self.handle, float(start), ctypes.byref(end)))
+        return end.value
+
+    def sample_shard(self, samples: int, rng: "N.qs_pcg64", start: float, total: float,
+                     base: int, global_dim: int, is_last: bool) -> np.ndarray:
+        """Draws of a global register of which this is the slice [base, base + 2^n):
+        global outcomes for draws landing here, -1 elsewhere (qs_sample_shard)."""
+        out = np.empty(int(samples), dtype=np.int64)
+        N.check(N.lib().qs_sample_shard(self.handle, ctypes.byref(rng), int(samples), float(start),
+                                        float(total), int(base), int(global_dim), int(bool(is_last)),
+                                        out.ctypes.data))
+        return out
+
     def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
         """Non-destructive sampling: {basis index: count}."""
         keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)

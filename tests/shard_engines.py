@@ -63,3 +63,15 @@ class OracleEngine:
 
     def synchronize(self):
         pass
+
+    def cdf_extend(self, start):
+        return float(np.cumsum(np.concatenate([[start], oc.probabilities(self.amps)]))[-1])
+
+    def sample_shard(self, k, rng, start, total, base, gdim, is_last):
+        cdf = np.cumsum(np.concatenate([[start], oc.probabilities(self.amps)]))[1:]
+        ncdf = cdf / total
+        u = oc.pcg64_random_words((rng.state_hi, rng.state_lo, rng.inc_hi, rng.inc_lo), k)
+        idx = np.searchsorted(ncdf, u, side="right")
+        own = (u >= start / total) & (is_last | (ncdf[-1] > u))
+        out = np.minimum(base + idx, gdim - 1)
+        return np.where(own, out, -1).astype(np.int64)

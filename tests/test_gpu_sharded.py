@@ -43,3 +43,15 @@ def test_gate_api_and_canonicalize_roundtrip():
     ref.cu1(n - 1, n - 2, 0.7)
     assert same_values(st.amplitudes(), ref.amplitudes())
     assert st.layout.is_identity()
+
+
+@pytest.mark.parametrize("n,shards", [(12, 2), (16, 4), (20, 8)])
+def test_sharded_sampling_equals_unsharded(n, shards):
+    circ = Circuit(n, mixed_circuit(n, 60, 3 * n).instructions)
+    ref = State(n)
+    execute(circ, ref, fuse=False)
+    st = ShardedState.virtual(n, shards)
+    st.run(circ)
+    for seed in (1, 77):
+        assert np.array_equal(st.sample_outcomes(5000, seed), ref.sample_outcomes(5000, seed))
+    assert st.measure(1000, seed=4) == ref.measure(1000, seed=4)

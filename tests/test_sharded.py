@@ -125,6 +125,27 @@ class TestVirtualShards:
         assert st.swaps >= 2  # both global qubits were swapped in
         assert same_values(st.amplitudes(), oracle_run(circ))
 
+    @pytest.mark.parametrize("n,shards", [(6, 2), (8, 4), (9, 8)])
+    def test_sampling_matches_unsharded(self, n, shards):
+        """The exact CDF is chained across shard boundaries: same draws as pairsim."""
+        circ = mixed_circuit(n, 50, 7 * n)
+        ref = oracle_run(circ)
+        st = ShardedState.virtual(n, shards, engine_factory=OracleEngine)
+        st.run(circ)
+        for seed in (0, 5, 123):
+            got = st.sample_outcomes(4000, seed)
+            assert np.array_equal(got, oc.sample_outcomes(ref, 4000, seed))
+        m = st.measure_collapse(seed=9)
+        assert m == int(oc.sample_outcomes(ref, 1, 9)[0])
+        a = st.amplitudes()
+        assert a[m] == 1 and np.count_nonzero(a) == 1
+
+    def test_sampling_zero_probability_shards(self):
+        n = 7
+        st = ShardedState.virtual(n, 4, engine_factory=OracleEngine)
+        st.reset(0b1011011)  # all probability in shard 2
+        assert np.all(st.sample_outcomes(100, 3) == 0b1011011)
+
     def test_reset_basis_on_other_shard(self):
         n = 6
         st = ShardedState.virtual(n, 4, engine_factory=OracleEngine)
@@ -150,10 +171,12 @@ def _worker(rank, world, port, n, seed, q):
         amps = st.amplitudes()
         probs = st.probabilities()
         norm = st.norm_squared()
+        draws = st.sample_outcomes(3000, seed)
         if rank == 0:
             ref = oracle_run(circ)
             q.put((bool(same_values(amps, ref)), probs.tobytes() == oc.probabilities(ref).tobytes(),
-                   abs(norm - float(oc.probabilities(ref).sum())) < 1e-12, st.swaps))
+                   abs(norm - float(oc.probabilities(ref).sum())) < 1e-12, st.swaps,
+                   bool(np.array_equal(draws, oc.sample_outcomes(ref, 3000, seed)))))
     finally:
         dist.destroy_process_group()
 
@@ -169,5 +192,5 @@ def test_gloo_distributed_matches_oracle(world, n):
     for p in procs:
         p.join(timeout=240)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    amps_ok, probs_ok, norm_ok, swaps = q.get(timeout=5)
-    assert amps_ok and probs_ok and norm_ok and swaps > 0
+    amps_ok, probs_ok, norm_ok, swaps, draws_ok = q.get(timeout=5)
+    assert amps_ok and probs_ok and norm_ok and swaps > 0 and draws_ok
