@@ -8,6 +8,7 @@ visible, every operation raises.  The library is built in-tree by
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
@@ -15,6 +16,8 @@ import numpy as np
 from .errors import CapacityError, DegenerateStateError, DeviceError
 
 LIB_PATH = Path(__file__).resolve().parent / "libqsb200.so"
+if os.environ.get("QSB_LIB"):  # A/B experiments with an alternative in-tree build
+    LIB_PATH = Path(os.environ["QSB_LIB"]).resolve()
 
 QS_OK, QS_ERR_INDEX, QS_ERR_VALUE, QS_ERR_CAPACITY, QS_ERR_DEGENERATE, QS_ERR_CUDA, QS_ERR_NULL = range(7)
 QS_OP_PAIR, QS_OP_PHASE = 0, 1

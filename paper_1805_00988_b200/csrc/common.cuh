@@ -7,7 +7,8 @@
 //     (g * v).im = fma(g.re, v.im,  rn(g.im * v.re))
 // with the gate entry g as the left operand (pkg/src/pairsim/kernel.py:128-129),
 // and the two products of a pair update added component-wise in fp32.
-// Explicit __f*_rn intrinsics keep nvcc from re-contracting the expression.
+// Explicit rounding (packed .rn f32x2 PTX below) keeps nvcc from re-contracting
+// the expression.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,15 +31,48 @@ __host__ __device__ inline Gate2 gate_from(const float m[8]) {
     return g;
 }
 
-__device__ __forceinline__ float2 cmul(float2 g, float2 v) {
-    float re = __fmaf_rn(g.x, v.x, -__fmul_rn(g.y, v.y));
-    float im = __fmaf_rn(g.x, v.y, __fmul_rn(g.y, v.x));
-    return make_float2(re, im);
+// Packed fp32 pairs (sm_100a FMUL2 / FFMA2 / FADD2): each lane is an
+// independent IEEE round-to-nearest operation, so a complex product needs two
+// instructions instead of four with the same bits as the scalar form.  The
+// lane swap (v.im, v.re) and the negated broadcast are free operand modifiers.
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) {
+    return (unsigned long long)__float_as_uint(v.x) | ((unsigned long long)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ float2 f2_from(unsigned long long b) {
+    return make_float2(__uint_as_float((unsigned)b), __uint_as_float((unsigned)(b >> 32)));
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return f2_from(r);
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
 }
 
-__device__ __forceinline__ float2 cadd(float2 x, float2 y) {
-    return make_float2(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y));
+// (re, im) = (fma(g.re, v.re, rn(-g.im * v.im)), fma(g.re, v.im, rn(g.im * v.re)));
+// rn(-x) == -rn(x), so this is numpy's form bit for bit.  The two g.im
+// products are scalar FMULs writing a fresh register pair (a packed FMUL2
+// would need the lane-swapped (v.im, v.re), which ptxas tends to materialise
+// with MOVs), then one FFMA2 with g.re broadcast: 3 instructions, no copies.
+__device__ __forceinline__ float2 cmul(float2 g, float2 v) {
+    const float2 t = make_float2(__fmul_rn(-g.y, v.y), __fmul_rn(g.y, v.x));
+    return f2fma(make_float2(g.x, g.x), v, t);
 }
+
+__device__ __forceinline__ float2 cadd(float2 x, float2 y) { return f2add(x, y); }
 
 // v_a' = a v_a + b v_b ; v_b' = d v_b + c v_a  (kernel.py:128-129)
 __device__ __forceinline__ void pair_update(const Gate2 &g, float2 &va, float2 &vb) {

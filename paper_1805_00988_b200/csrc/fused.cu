@@ -68,7 +68,8 @@ struct __align__(16) FOp {
     uint32_t tid_need;   // thread-id bits (lane | warp << 5) that must be set
     uint32_t half_need;  // odd half only (control / phase bit on local qubit 0)
     uint64_t ext_need;   // global qubits outside the tile that must be 1
-    uint64_t pad;
+    float one;           // == 1.0f, loaded at run time (see rsum / csub)
+    int run;             // at a run head: number of consecutive ops with this variant
     float m[8];
 };
 // pair variants: ((slot + 1) * 4 + class) * 2 + has_need, slot -1 = half;
@@ -180,30 +181,38 @@ __device__ __forceinline__ void fence_mbar_init() {
 // ---- exact pair updates per gate class ----------------------------------------
 // real entry g (g.im == 0): fma(g, v.re, -rn(0*v.im)) == rn(g*v.re) and
 // fma(g, v.im, rn(0*v.re)) == rn(g*v.im) for every nonzero result.
-__device__ __forceinline__ float2 rmul(float g, float2 v) {
-    return make_float2(__fmul_rn(g, v.x), __fmul_rn(g, v.y));
+// ptxas (CUDA 12.9) contracts mul.rn.f32x2 feeding add.rn.f32x2 (and even
+// fma.rn.f32x2(x, 1.0, y), which it first folds to an add) into one FFMA2,
+// which would round a sum of two products once instead of three times.  The
+// sums below are fma(x, one, y) / fma(y, -one, x) with `one` == 1.0f loaded
+// from the op table at run time, so ptxas cannot fold them: exactly
+// rn(x + y) / rn(x - y), and the products stay separately rounded.  The GPU
+// parity tests compare every gate class bit for bit against the oracle.
+__device__ __forceinline__ float2 rmul(float g, float2 v) { return f2mul(make_float2(g, g), v); }
+__device__ __forceinline__ float2 rsum(float2 x, float2 y, float one) {
+    return f2fma(x, make_float2(one, one), y);
 }
-__device__ __forceinline__ float2 csub(float2 x, float2 y) {
-    return make_float2(__fsub_rn(x.x, y.x), __fsub_rn(x.y, y.y));
+__device__ __forceinline__ float2 csub(float2 x, float2 y, float one) {
+    return f2fma(y, make_float2(-one, -one), x);
 }
 
 template <int CLS>
-__device__ __forceinline__ void pair_cls(const float *m, float2 &va, float2 &vb) {
+__device__ __forceinline__ void pair_cls(const float *m, float one, float2 &va, float2 &vb) {
     if (CLS == kCplx) {
         float2 na = cadd(cmul(make_float2(m[0], m[1]), va), cmul(make_float2(m[2], m[3]), vb));
         float2 nb = cadd(cmul(make_float2(m[6], m[7]), vb), cmul(make_float2(m[4], m[5]), va));
         va = na;
         vb = nb;
     } else if (CLS == kReal) {
-        float2 na = cadd(rmul(m[0], va), rmul(m[2], vb));
-        float2 nb = cadd(rmul(m[6], vb), rmul(m[4], va));
+        float2 na = rsum(rmul(m[0], va), rmul(m[2], vb), one);
+        float2 nb = rsum(rmul(m[6], vb), rmul(m[4], va), one);
         va = na;
         vb = nb;
     } else if (CLS == kHlike) {
         // c == a, d == -b: c*va == a*va and d*vb == -(b*vb) exactly
         float2 p = rmul(m[0], va), q = rmul(m[2], vb);
-        va = cadd(p, q);
-        vb = csub(p, q);
+        va = rsum(p, q, one);
+        vb = csub(p, q, one);
     } else {  // X: a == d == 0, b == c == 1 -> values swap
         float2 t = va;
         va = vb;
@@ -222,6 +231,7 @@ template <int T, int CLS, bool NEED, int RB>
 __device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[1 << RB]) {
     const uint32_t need = NEED ? op.reg_need : 0u;
     const bool odd_only = NEED && op.half_need != 0;
+    const float one = op.one;
     float m[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) m[i] = (CLS == kSwap) ? 0.f : op.m[i];
@@ -231,13 +241,13 @@ __device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[1 << RB]) 
         if (NEED && (j & need) != need) continue;  // warp-uniform
         if (T < 0) {
             float2 a = lo2(v[j]), b = hi2(v[j]);
-            pair_cls<CLS>(m, a, b);
+            pair_cls<CLS>(m, one, a, b);
             v[j] = mk4(a, b);
         } else {
             const int k = j | (1 << (T < 0 ? 0 : T));
             float2 a0 = lo2(v[j]), a1 = hi2(v[j]), b0 = lo2(v[k]), b1 = hi2(v[k]);
-            if (!odd_only) pair_cls<CLS>(m, a0, b0);
-            pair_cls<CLS>(m, a1, b1);
+            if (!odd_only) pair_cls<CLS>(m, one, a0, b0);
+            pair_cls<CLS>(m, one, a1, b1);
             v[j] = mk4(a0, a1);
             v[k] = mk4(b0, b1);
         }
@@ -263,15 +273,37 @@ __device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[1 << RB])
 // bodies keep the per-j branch, which bounds ptxas' register demand there.
 __device__ constexpr bool kStraight[4] = {false, true, true, false};
 
+__device__ __forceinline__ bool op_ok(const FOp &op, uint32_t tid, uint64_t base) {
+    return (tid & op.tid_need) == op.tid_need && (base & op.ext_need) == op.ext_need;
+}
+
+template <int T, int C, bool NEED, int RB>
+__device__ __forceinline__ void run_pair(const FOp *ops, int len, uint32_t tid, uint64_t base,
+                                         float4 (&v)[1 << RB]) {
+    for (int k = 0; k < len; ++k)
+        if (op_ok(ops[k], tid, base)) apply_pair<T, C, NEED, RB>(ops[k], v);
+}
+
+template <int R, bool ODD, int RB>
+__device__ __forceinline__ void run_phase(const FOp *ops, int len, uint32_t tid, uint64_t base,
+                                          float4 (&v)[1 << RB]) {
+    for (int k = 0; k < len; ++k)
+        if (op_ok(ops[k], tid, base)) apply_phase<R, ODD, RB>(ops[k], v);
+}
+
+// One dispatch per RUN of consecutive ops with the same variant (the host
+// sets FOp::run at each run head): nvcc lowers the switch to a compare tree,
+// so QFT-style streams of same-pattern phase ops pay for it once per run.
 template <int RB>
-__device__ __forceinline__ void apply_op(const FOp &op, float4 (&v)[1 << RB]) {
-    switch (op.variant) {
-#define QSB_CASE(T, C)                                                                            \
-    case (((T) + 1) * 4 + (C)) * 2 + 0:                                                           \
-        if constexpr ((T) < RB) apply_pair<(T), (C), !kStraight[C], RB>(op, v);                    \
-        break;                                                                                    \
-    case (((T) + 1) * 4 + (C)) * 2 + 1:                                                           \
-        if constexpr ((T) < RB) apply_pair<(T), (C), true, RB>(op, v);                             \
+__device__ __forceinline__ void apply_run(int variant, const FOp *ops, int len, uint32_t tid,
+                                          uint64_t base, float4 (&v)[1 << RB]) {
+    switch (variant) {
+#define QSB_CASE(T, C)                                                                             \
+    case (((T) + 1) * 4 + (C)) * 2 + 0:                                                            \
+        if constexpr ((T) < RB) run_pair<(T), (C), !kStraight[C], RB>(ops, len, tid, base, v);      \
+        break;                                                                                     \
+    case (((T) + 1) * 4 + (C)) * 2 + 1:                                                            \
+        if constexpr ((T) < RB) run_pair<(T), (C), true, RB>(ops, len, tid, base, v);               \
         break;
 #define QSB_CASES(T) QSB_CASE(T, 0) QSB_CASE(T, 1) QSB_CASE(T, 2) QSB_CASE(T, 3)
         QSB_CASES(-1)
@@ -281,12 +313,12 @@ __device__ __forceinline__ void apply_op(const FOp &op, float4 (&v)[1 << RB]) {
         QSB_CASES(3)
 #undef QSB_CASES
 #undef QSB_CASE
-#define QSB_PH(R)                                                        \
-    case kPhaseVariant + (R) * 2 + 0:                                     \
-        if constexpr ((R) < (1 << RB)) apply_phase<(R), false, RB>(op, v); \
-        break;                                                            \
-    case kPhaseVariant + (R) * 2 + 1:                                     \
-        if constexpr ((R) < (1 << RB)) apply_phase<(R), true, RB>(op, v);  \
+#define QSB_PH(R)                                                                       \
+    case kPhaseVariant + (R) * 2 + 0:                                                    \
+        if constexpr ((R) < (1 << RB)) run_phase<(R), false, RB>(ops, len, tid, base, v); \
+        break;                                                                           \
+    case kPhaseVariant + (R) * 2 + 1:                                                    \
+        if constexpr ((R) < (1 << RB)) run_phase<(R), true, RB>(ops, len, tid, base, v);  \
         break;
         QSB_PH(0) QSB_PH(1) QSB_PH(2) QSB_PH(3) QSB_PH(4) QSB_PH(5) QSB_PH(6) QSB_PH(7)
         QSB_PH(8) QSB_PH(9) QSB_PH(10) QSB_PH(11) QSB_PH(12) QSB_PH(13) QSB_PH(14) QSB_PH(15)
@@ -312,7 +344,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 template <int K, int RB>
-__global__ void __maxnreg__(RB == 4 ? 128 : 96)
+__global__ void __maxnreg__(RB == 4 ? 168 : 96)
     k_fused(float4 *__restrict__ amps, const __grid_constant__ FParams p) {
     constexpr int kCompute = 1 << (K - 1 - RB);   // compute threads
     constexpr int kSegs = 1 << (K - kLow);        // 512-B segments per tile
@@ -413,13 +445,12 @@ __global__ void __maxnreg__(RB == 4 ? 128 : 96)
                     if (j & (1 << r)) a += rs[r];
                 v[j] = tile[a];
             }
-            for (int o = st.op_begin; o < st.op_end; ++o) {
-                const FOp &op = sops[o];
-                const int4 hdr = *reinterpret_cast<const int4 *>(&op);  // one LDS.128
-                const uint64_t ext = op.ext_need;
-                const bool ok = ((uint32_t)tid & (uint32_t)hdr.z) == (uint32_t)hdr.z &&
-                                (base & ext) == ext;
-                if (ok && !p.dry) apply_op<RB>(op, v);
+            if (!p.dry) {
+                for (int o = st.op_begin; o < st.op_end;) {
+                    const int variant = sops[o].variant, len = sops[o].run;
+                    apply_run<RB>(variant, sops + o, len, (uint32_t)tid, base, v);
+                    o += len;
+                }
             }
 #pragma unroll
             for (int j = 0; j < (1 << RB); ++j) {
@@ -749,6 +780,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
             FOp o;
             std::memset(&o, 0, sizeof o);
             std::memcpy(o.m, op.m, sizeof o.m);
+            o.one = 1.0f;
             uint64_t need = op.ctrl_mask;
             if (op.kind == QS_OP_PHASE) need |= 1ull << op.target;
             for (int q = 0; q < n; ++q) {
@@ -806,6 +838,15 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
             p.stages[k - si].op_end -= off;
         }
         std::memcpy(p.ops, fops.data() + off, (size_t)nop * sizeof(FOp));
+        for (int k = 0; k < p.nstages; ++k) {  // runs of equal variants, within a stage
+            const FStage &st = p.stages[k];
+            for (int o = st.op_begin; o < st.op_end;) {
+                int e = o + 1;
+                while (e < st.op_end && p.ops[e].variant == p.ops[o].variant) ++e;
+                p.ops[o].run = e - o;
+                o = e;
+            }
+        }
         int rc;
         switch (K) {
             case 10: rc = RB == 4 ? launch_fused_k<10, 4>(s, p) : launch_fused_k<10, 3>(s, p); break;

@@ -275,6 +275,55 @@ class TestFusedEqualsUnfused:
                 outs.append(st.amplitudes())
         assert same_values(outs[0], outs[1])
 
+    @pytest.mark.parametrize("rb", ["3", "4"])
+    @pytest.mark.parametrize("n,K", [(13, 13), (16, 12), (17, 13)])
+    def test_gate_classes_vs_oracle(self, n, K, rb):
+        """Every fused gate class (complex, real, H-like, X, phase) on every
+        tile target, plain and controlled, bit for bit against the oracle.
+        Real rotations and scaled H-like gates are the cases where a fused
+        multiply-add of two products would change the last bit."""
+        rng = np.random.default_rng(700 + n + K)
+        a0 = rand_amps(n, rng)
+
+        def real_rot():
+            th = float(rng.uniform(0, 2 * math.pi))
+            return M8Gate(np.array([math.cos(th), 0, -math.sin(th), 0,
+                                    math.sin(th), 0, math.cos(th), 0], dtype=np.float32))
+
+        def h_like():
+            a, b = (float(x) for x in rng.uniform(-1, 1, 2))
+            return M8Gate(np.array([a, 0, b, 0, a, 0, -b, 0], dtype=np.float32))
+
+        makers = [real_rot, h_like, lambda: M8Gate(H_M8), lambda: M8Gate(X_M8),
+                  lambda: random_unitary_gate(rng), lambda: u1(float(rng.uniform(0, 6.28)))]
+        ins = []
+        tile = list(range(6)) + list(range(n - (K - 6), n))
+        for rep in range(3):
+            for t in tile:
+                g = makers[int(rng.integers(len(makers)))]()
+                r = rng.random()
+                others = [q for q in range(n) if q != t]
+                if r < 0.5:
+                    ins.append(Apply(g, t))
+                elif r < 0.85:
+                    ins.append(ControlledApply(g, int(rng.choice(others)), t))
+                else:
+                    c1, c2 = (int(x) for x in rng.choice(others, 2, replace=False))
+                    ins.append(ControlledControlledApply(g, c1, c2, t))
+        circ = Circuit(n, tuple(ins))
+        ref = a0.copy()
+        for i in circ.instructions:
+            if isinstance(i, Apply):
+                oc.apply_gate(ref, i.target, i.gate)
+            elif isinstance(i, ControlledApply):
+                oc.apply_controlled_gate(ref, i.control, i.target, i.gate)
+            else:
+                oc.apply_cc_gate(ref, i.control1, i.control2, i.target, i.gate)
+        with env(QSB_FUSED_RB=rb):
+            st = load(n, a0)
+            execute(circ, st, fuse=True, tile_qubits=K)
+            assert same_values(st.amplitudes(), ref)
+
     @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 12, 13])
     def test_small_register_single_launch(self, n):
         """n < 10 fused passes run in one shared-memory launch (k_small)."""
