@@ -8,8 +8,10 @@
  * semantics it reproduces.
  *
  * Conventions
- *   - Amplitudes are complex64, interleaved (re, im) float32, qubit t = bit t
- *     of the basis index (pkg/src/pairsim/state.py:3-5).
+ *   - Amplitudes are complex64 (interleaved (re, im) float32) or, for
+ *     registers created with QS_DOUBLE, complex128 (interleaved float64) —
+ *     pairsim's Precision.SINGLE / DOUBLE (pkg/src/pairsim/state.py:25-42).
+ *     Qubit t = bit t of the basis index (pkg/src/pairsim/state.py:3-5).
  *   - A 2x2 gate [[a, b], [c, d]] is passed as float m[8] =
  *     {a.re, a.im, b.re, b.im, c.re, c.im, d.re, d.im}, already rounded to
  *     float32 exactly as `np.complex64(x)` rounds (pkg/src/pairsim/kernel.py:118-119).
@@ -29,7 +31,10 @@
 extern "C" {
 #endif
 
-#define QSB200_ABI_VERSION 1
+#define QSB200_ABI_VERSION 2
+
+/* Register precision (pkg/src/pairsim/state.py:25-42). */
+enum { QS_SINGLE = 0, QS_DOUBLE = 1 };
 
 /* Status codes.  The Python layer maps them onto the reference's exception
  * taxonomy (pkg/src/pairsim/errors.py:4-37). */
@@ -67,6 +72,14 @@ typedef struct {
     float m[8];         /* gate entries, as for qs_apply_gate                      */
 } qs_op;
 
+/* The same op with fp64 gate entries (complex128 registers). */
+typedef struct {
+    int32_t kind;
+    int32_t target;
+    uint64_t ctrl_mask;
+    double m[8];
+} qs_op64;
+
 /* ---- library ------------------------------------------------------------ */
 int qs_abi_version(void);
 const char *qs_last_error(void);
@@ -84,6 +97,10 @@ int qs_release_cached(int device);
  * Fails with QS_ERR_CAPACITY *before* allocating when over budget; a budget
  * equal to the need is allowed (pkg/tests/test_state.py:45-52). */
 int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out);
+/* As qs_create with an explicit precision (QS_SINGLE or QS_DOUBLE); a
+ * complex128 register needs 16 * 2^n bytes (memory_required, state.py:71-83). */
+int qs_create_ex(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out);
+int qs_precision(const qs_state *s, int *out);
 int qs_destroy(qs_state *s);
 int qs_num_qubits(const qs_state *s, int *out);
 int qs_device(const qs_state *s, int *out);
@@ -105,6 +122,13 @@ int qs_apply_controlled_gate(qs_state *s, int control, int target, const float m
 /* Doubly-controlled update (QCGPU's apply_controlled_controlled_gate; no
  * pairsim counterpart): the update where bits c1 and c2 are both 1. */
 int qs_apply_controlled_controlled_gate(qs_state *s, int c1, int c2, int target, const float m[8]);
+/* fp64 gate entries: exact on a complex128 register; rounded to float32 (as
+ * np.complex64(x) rounds, kernel.py:118-119) on a complex64 register.  The
+ * float32 entry points above widen exactly on a complex128 register. */
+int qs_apply_gate_f64(qs_state *s, int target, const double m[8]);
+int qs_apply_controlled_gate_f64(qs_state *s, int control, int target, const double m[8]);
+int qs_apply_controlled_controlled_gate_f64(qs_state *s, int c1, int c2, int target,
+                                            const double m[8]);
 /* Fused pass: one HBM read+write of the register applies `ops` in order,
  * bit-identical to applying them one by one.  `tile_qubits` (ntile entries,
  * must contain 0..5 when num_qubits >= 6) is the set of qubits held in each
@@ -112,18 +136,26 @@ int qs_apply_controlled_controlled_gate(qs_state *s, int c1, int c2, int target,
  * bits may be anywhere). */
 int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile,
                    const qs_op *ops, int nops);
+/* Fused pass with fp64 gate entries (the form a complex128 register takes;
+ * on a complex64 register the entries are rounded to float32 and the call
+ * is qs_apply_fused). */
+int qs_apply_fused_f64(qs_state *s, const int32_t *tile_qubits, int ntile,
+                       const qs_op64 *ops, int nops);
 /* Swap qubits q1 and q2 (a basis permutation; used by the sharded layer). */
 int qs_swap_qubits(qs_state *s, int q1, int q2);
 
 /* ---- readout: state.py:146-161, measure.py:29-99 ------------------------- */
-int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, float *host);
-int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const float *host);
+/* `host` holds `count` amplitudes of the register's precision (float pairs
+ * for QS_SINGLE, double pairs for QS_DOUBLE). */
+int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, void *host);
+int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const void *host);
 /* Asynchronous variants: enqueue the copy on the handle's stream and return.
  * `host` must stay valid (and, for full overlap, be pinned) until the next
  * qs_synchronize on this handle. */
-int qs_set_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, const float *host);
-int qs_get_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, float *host);
-/* probabilities (measure.py:29-34): p[j] = re^2 + im^2 in fp64, bit-exact. */
+int qs_set_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, const void *host);
+int qs_get_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, void *host);
+/* probabilities (measure.py:29-34): p[j] = re^2 + im^2 in fp64, bit-exact
+ * (complex128: rn(rn(re*re) + rn(im*im)), numpy's three separate roundings). */
 int qs_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
 /* norm_squared (state.py:146-151): fp64 sum of |a|^2 (tree order). */
 int qs_norm_squared(qs_state *s, double *out);

@@ -21,13 +21,16 @@ if os.environ.get("QSB_LIB"):  # A/B experiments with an alternative in-tree bui
 
 QS_OK, QS_ERR_INDEX, QS_ERR_VALUE, QS_ERR_CAPACITY, QS_ERR_DEGENERATE, QS_ERR_CUDA, QS_ERR_NULL = range(7)
 QS_OP_PAIR, QS_OP_PHASE = 0, 1
+QS_SINGLE, QS_DOUBLE = 0, 1
 
 # Every symbol include/qsb200.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
-    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_release_cached", "qs_create", "qs_destroy",
+    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_release_cached", "qs_create", "qs_create_ex",
+    "qs_precision", "qs_destroy",
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
-    "qs_apply_controlled_controlled_gate", "qs_apply_fused", "qs_swap_qubits",
+    "qs_apply_controlled_controlled_gate", "qs_apply_gate_f64", "qs_apply_controlled_gate_f64",
+    "qs_apply_controlled_controlled_gate_f64", "qs_apply_fused", "qs_apply_fused_f64", "qs_swap_qubits",
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
@@ -44,9 +47,17 @@ class qs_op(ctypes.Structure):
                 ("ctrl_mask", ctypes.c_uint64), ("m", ctypes.c_float * 8)]
 
 
+class qs_op64(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("target", ctypes.c_int32),
+                ("ctrl_mask", ctypes.c_uint64), ("m", ctypes.c_double * 8)]
+
+
 OP_DTYPE = np.dtype([("kind", np.int32), ("target", np.int32), ("ctrl_mask", np.uint64),
                      ("m", np.float32, 8)])
+OP64_DTYPE = np.dtype([("kind", np.int32), ("target", np.int32), ("ctrl_mask", np.uint64),
+                       ("m", np.float64, 8)])
 assert OP_DTYPE.itemsize == ctypes.sizeof(qs_op)
+assert OP64_DTYPE.itemsize == ctypes.sizeof(qs_op64)
 
 _lib = None
 
@@ -55,12 +66,15 @@ def _declare(L):
     vp = ctypes.c_void_p
     i32, u64, i64 = ctypes.c_int, ctypes.c_uint64, ctypes.c_int64
     f32p = ctypes.POINTER(ctypes.c_float)
+    f64p = ctypes.POINTER(ctypes.c_double)
     sig = {
         "qs_abi_version": ([], i32),
         "qs_last_error": ([], ctypes.c_char_p),
         "qs_device_count": ([ctypes.POINTER(i32)], i32),
         "qs_release_cached": ([i32], i32),
         "qs_create": ([i32, i32, u64, ctypes.POINTER(vp)], i32),
+        "qs_create_ex": ([i32, i32, u64, i32, ctypes.POINTER(vp)], i32),
+        "qs_precision": ([vp, ctypes.POINTER(i32)], i32),
         "qs_destroy": ([vp], i32),
         "qs_num_qubits": ([vp, ctypes.POINTER(i32)], i32),
         "qs_device": ([vp, ctypes.POINTER(i32)], i32),
@@ -71,7 +85,11 @@ def _declare(L):
         "qs_apply_gate": ([vp, i32, f32p], i32),
         "qs_apply_controlled_gate": ([vp, i32, i32, f32p], i32),
         "qs_apply_controlled_controlled_gate": ([vp, i32, i32, i32, f32p], i32),
+        "qs_apply_gate_f64": ([vp, i32, f64p], i32),
+        "qs_apply_controlled_gate_f64": ([vp, i32, i32, f64p], i32),
+        "qs_apply_controlled_controlled_gate_f64": ([vp, i32, i32, i32, f64p], i32),
         "qs_apply_fused": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
+        "qs_apply_fused_f64": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
         "qs_swap_qubits": ([vp, i32, i32], i32),
         "qs_get_amplitudes": ([vp, u64, u64, vp], i32),
         "qs_set_amplitudes": ([vp, u64, u64, vp], i32),
@@ -139,3 +157,7 @@ def pcg_from_seed(seed) -> qs_pcg64:
 
 def f32ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def f64ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))

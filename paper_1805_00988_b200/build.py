@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libqsb200.so"
-SOURCES = ["runtime.cu", "pool.cu", "gates.cu", "measure.cu", "fused.cu"]
+SOURCES = ["runtime.cu", "pool.cu", "gates.cu", "gates64.cu", "measure.cu", "fused.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -156,15 +156,17 @@ def layered_random_circuit(num_qubits: int, depth: int, seed: int) -> Circuit:
     return Circuit(num_qubits, tuple(ins))
 
 
-def lower_ops(circuit: Circuit) -> list:
+def lower_ops(circuit: Circuit, double: bool = False) -> list:
+    """(kind, target, ctrl_mask, m) per gate instruction; m holds the entries
+    rounded to the register precision (float32, or float64 when `double`)."""
     ops = []
     for ins in circuit.instructions:
         if isinstance(ins, Apply):
-            ops.append(fusion.lower(ins.gate, ins.target))
+            ops.append(fusion.lower(ins.gate, ins.target, (), double))
         elif isinstance(ins, ControlledApply):
-            ops.append(fusion.lower(ins.gate, ins.target, (ins.control,)))
+            ops.append(fusion.lower(ins.gate, ins.target, (ins.control,), double))
         elif isinstance(ins, ControlledControlledApply):
-            ops.append(fusion.lower(ins.gate, ins.target, (ins.control1, ins.control2)))
+            ops.append(fusion.lower(ins.gate, ins.target, (ins.control1, ins.control2), double))
     return ops
 
 
@@ -173,7 +175,7 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
     of a trailing SampleMeasure (or None)."""
     if circuit.num_qubits != state.num_qubits:
         raise ValueError("circuit and state widths differ")
-    ops = lower_ops(circuit)
+    ops = lower_ops(circuit, double=getattr(state, "is_double", False))
     if fuse:
         fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits))
     else:

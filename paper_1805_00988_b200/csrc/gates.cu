@@ -258,6 +258,7 @@ int launch_low(qs_state *s, int t, uint64_t nitems, FixedBits fb, uint64_t row_s
 }  // namespace
 
 int launch_reset(qs_state *s, uint64_t basis) {
+    if (s->prec == QS_DOUBLE) return launch_reset_d(s, basis);
     QS_CUDA(cudaMemsetAsync(s->amps, 0, 8ull << s->num_qubits, s->stream));
     k_set_one<<<1, 1, 0, s->stream>>>(s->amps, basis);
     QS_CUDA(cudaGetLastError());

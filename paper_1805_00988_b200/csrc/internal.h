@@ -11,7 +11,8 @@
 struct qs_state {
     int num_qubits;
     int device;
-    float2 *amps;          // 2^n complex64, 256-B aligned (cudaMalloc)
+    float2 *amps;          // 2^n amplitudes, 256-B aligned (cudaMalloc); double2 when prec == 1
+    int prec;              // QS_SINGLE (complex64) or QS_DOUBLE (complex128)
     cudaStream_t stream;   // all work on this handle is ordered on it
     int num_sms;
     // measurement scratch (lazily grown; freed with the handle)
@@ -27,6 +28,11 @@ struct qs_state {
 namespace qsb {
 
 int set_error(int code, const std::string &msg);
+
+// bytes per amplitude: 8 (complex64) or 16 (complex128)
+inline uint64_t amp_bytes(const qs_state *s) { return s->prec == QS_DOUBLE ? 16ull : 8ull; }
+inline uint64_t state_bytes(const qs_state *s) { return amp_bytes(s) << s->num_qubits; }
+inline double2 *amps_d(const qs_state *s) { return reinterpret_cast<double2 *>(s->amps); }
 int cuda_fail(cudaError_t e, const char *what);
 
 // RAII guard: switch to the handle's device for the duration of a call.
@@ -59,6 +65,12 @@ int launch_sweep(qs_state *s, int target, uint64_t ctrl_mask, const float m[8]);
 int launch_phase(qs_state *s, uint64_t mask, float2 d);
 int launch_swap(qs_state *s, int q1, int q2);
 int launch_reset(qs_state *s, uint64_t basis);
+// complex128 registers (gates64.cu)
+int launch_sweep_d(qs_state *s, int target, uint64_t ctrl_mask, const double m[8]);
+int launch_phase_d(qs_state *s, uint64_t mask, double2 d);
+int launch_swap_d(qs_state *s, int q1, int q2);
+int launch_reset_d(qs_state *s, uint64_t basis);
+int run_fused_d(qs_state *s, const qs_op64 *ops, int nops);
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
 int run_norm(qs_state *s, double *out);
 int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);

@@ -52,8 +52,15 @@ __device__ __forceinline__ double prob(float2 a) {
     double re = (double)a.x, im = (double)a.y;
     return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
 }
+// complex128 (measure.py:31-34 on a complex128 array): re*re, im*im and their
+// sum are three separately rounded numpy passes.
+__device__ __forceinline__ double prob(double2 a) {
+    return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+}
 
-__global__ void k_probs(const float2 *__restrict__ amps, double *__restrict__ out, uint64_t count) {
+// A = float2 (complex64 register) or double2 (complex128 register)
+template <class A>
+__global__ void k_probs(const A *__restrict__ amps, double *__restrict__ out, uint64_t count) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x)
         out[i] = prob(amps[i]);
@@ -77,7 +84,8 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return v;
 }
 
-__global__ void k_norm_partial(const float2 *__restrict__ amps, uint64_t n, double *partial) {
+template <class A>
+__global__ void k_norm_partial(const A *__restrict__ amps, uint64_t n, double *partial) {
     __shared__ double sh[32];
     double acc = 0.0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -96,11 +104,12 @@ __global__ void k_norm_final(const double *partial, int n, double *out) {
 }
 
 // ---- M1: chunk sums ---------------------------------------------------------
-__global__ void k_chunk_sums(const float2 *__restrict__ amps, int clog, double *__restrict__ csum) {
+template <class A>
+__global__ void k_chunk_sums(const A *__restrict__ amps, int clog, double *__restrict__ csum) {
     __shared__ double sh[32];
     const uint64_t c = blockIdx.x;
     const uint64_t C = 1ull << clog;
-    const float2 *p = amps + (c << clog);
+    const A *p = amps + (c << clog);
     double acc = 0.0;
     for (uint64_t j = threadIdx.x; j < C; j += blockDim.x) acc += prob(p[j]);
     acc = block_sum(acc, sh);
@@ -155,8 +164,9 @@ enum : int { kFlagOk = 1, kFlagExact0 = 2 };
 // 256-B read), converts to probabilities in shared memory, and lane L walks
 // row L sequentially with both chains.
 constexpr int kTrajWarps = 4;
+template <class A>
 __global__ void __launch_bounds__(kTrajWarps * 32)
-    k_trajectories(const float2 *__restrict__ amps, uint64_t nch, int clog, double start,
+    k_trajectories(const A *__restrict__ amps, uint64_t nch, int clog, double start,
                    const double *__restrict__ g, double *__restrict__ g0out,
                    double *__restrict__ d0, double *__restrict__ d1, double *__restrict__ hiout,
                    int *__restrict__ flags) {
@@ -219,6 +229,12 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
 }
 
 // sequential re-sum of one chunk from an exact start (the reference's loop)
+__device__ double walk_chunk(const double2 *__restrict__ amps, uint64_t chunk, int clog, double s) {
+    const uint64_t C = 1ull << clog;
+    const double2 *p = amps + (chunk << clog);
+    for (uint64_t j = 0; j < C; ++j) s = __dadd_rn(s, prob(p[j]));
+    return s;
+}
 __device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, int clog, double s) {
     const uint64_t C = 1ull << clog;
     const float2 *p = amps + (chunk << clog);
@@ -243,7 +259,8 @@ __device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, in
 }
 
 // ---- M4: resolve true chunk starts (single thread) ---------------------------
-__global__ void k_resolve(const float2 *__restrict__ amps, uint64_t nch, int clog,
+template <class A>
+__global__ void k_resolve(const A *__restrict__ amps, uint64_t nch, int clog,
                           double s_start, const double *__restrict__ g0, const double *__restrict__ d0,
                           const double *__restrict__ d1, const double *__restrict__ hi,
                           const int *__restrict__ flags, double *__restrict__ start,
@@ -319,7 +336,8 @@ __device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
 // register holds a value above u) and u < last[nch-1] (or this is the last
 // register); otherwise out[i] = -1.  Outcomes are offset by `base` and
 // clamped to `gdim - 1` (measure.py:83).
-__global__ void k_draws(const float2 *__restrict__ amps, uint64_t nch, int clog, uint64_t dim,
+template <class A>
+__global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint64_t dim,
                         const double *__restrict__ start, const double *__restrict__ last,
                         const double *__restrict__ end, double gtotal, double s_start,
                         uint64_t base, uint64_t gdim, int is_last, qs_pcg64 rng, int64_t k,
@@ -348,7 +366,7 @@ __global__ void k_draws(const float2 *__restrict__ amps, uint64_t nch, int clog,
         uint64_t idx = dim;  // searchsorted returns dim when every value <= u
         if (lo < nch) {
             const uint64_t C = 1ull << clog;
-            const float2 *p = amps + (lo << clog);
+            const A *p = amps + (lo << clog);
             double s = start[lo];
             // s below `thr` cannot satisfy fl(s / t) > u; skip the division there
             const double thr = __dmul_rn(__dmul_rn(u, t), 1.0 - 0x1p-50);
@@ -407,7 +425,10 @@ int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host
         const uint64_t m = (count - done) < step ? (count - done) : step;
         unsigned grid = (unsigned)((m + 255) / 256);
         if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
-        k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, dev[b], m);
+        if (s->prec == QS_DOUBLE)
+            k_probs<<<grid, 256, 0, s->stream>>>(amps_d(s) + offset + done, dev[b], m);
+        else
+            k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, dev[b], m);
         QS_CUDA(cudaGetLastError());
         QS_CUDA(cudaMemcpyAsync(pin[b], dev[b], m * sizeof(double), cudaMemcpyDeviceToHost,
                                 s->stream));
@@ -431,7 +452,10 @@ int run_norm(qs_state *s, double *out) {
     if (rc) return rc;
     double *partial = (double *)s->scratch;
     const uint64_t n = 1ull << s->num_qubits;
-    k_norm_partial<<<kNormBlocks, kNormThreads, 0, s->stream>>>(s->amps, n, partial);
+    if (s->prec == QS_DOUBLE)
+        k_norm_partial<<<kNormBlocks, kNormThreads, 0, s->stream>>>(amps_d(s), n, partial);
+    else
+        k_norm_partial<<<kNormBlocks, kNormThreads, 0, s->stream>>>(s->amps, n, partial);
     k_norm_final<<<1, kNormThreads, 0, s->stream>>>(partial, kNormBlocks, partial + kNormBlocks);
     QS_CUDA(cudaGetLastError());
     rc = ensure_pinned(s, sizeof(double));
@@ -481,19 +505,25 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
 
 // M1..M4: exact sequential running sum over the register, continuing from
 // `s_start`; leaves chunk starts in c.start and the final value in *c.end.
-static int cdf_chain(qs_state *s, const CdfScratch &c, double s_start) {
-    k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(s->amps, c.clog, c.csum);
+template <class A>
+static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s_start) {
+    k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(amps, c.clog, c.csum);
     k_scan_guess<<<1, 1024, 0, s->stream>>>(c.csum, c.nch, c.start);  // prefixes -> start[]
     {
         const uint64_t warps = (c.nch + 31) / 32;
         const unsigned blocks = (unsigned)((warps + kTrajWarps - 1) / kTrajWarps);
         k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
-            s->amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags);
+            amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags);
     }
-    k_resolve<<<1, 1, 0, s->stream>>>(s->amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi,
+    k_resolve<<<1, 1, 0, s->stream>>>(amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi,
                                       c.flags, c.start, c.end, c.nslow);
     QS_CUDA(cudaGetLastError());
     return QS_OK;
+}
+
+static int cdf_chain(qs_state *s, const CdfScratch &c, double s_start) {
+    return s->prec == QS_DOUBLE ? cdf_chain_t(s, (const double2 *)amps_d(s), c, s_start)
+                                : cdf_chain_t(s, (const float2 *)s->amps, c, s_start);
 }
 
 // M5 + M6 and the copy-out shared by qs_sample / qs_sample_shard.
@@ -508,9 +538,14 @@ static int draw(qs_state *s, const CdfScratch &c, const qs_pcg64 *rng, int64_t k
     {
         unsigned grid = (unsigned)((k + 127) / 128);
         if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
-        k_draws<<<grid, 128, 0, s->stream>>>(s->amps, c.nch, c.clog, 1ull << s->num_qubits, c.start,
-                                             c.last, c.end, gtotal, s_start, base, gdim, is_last,
-                                             *rng, k, c.dout);
+        if (s->prec == QS_DOUBLE)
+            k_draws<<<grid, 128, 0, s->stream>>>(amps_d(s), c.nch, c.clog, 1ull << s->num_qubits,
+                                                 c.start, c.last, c.end, gtotal, s_start, base, gdim,
+                                                 is_last, *rng, k, c.dout);
+        else
+            k_draws<<<grid, 128, 0, s->stream>>>(s->amps, c.nch, c.clog, 1ull << s->num_qubits,
+                                                 c.start, c.last, c.end, gtotal, s_start, base, gdim,
+                                                 is_last, *rng, k, c.dout);
     }
     QS_CUDA(cudaGetLastError());
     int rc = ensure_pinned(s, sizeof(double));

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -107,9 +108,16 @@ int qs_device_count(int *out) {
 
 // new_state: pkg/src/pairsim/state.py:122-143
 int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out) {
+    return qs_create_ex(num_qubits, device, memory_budget, QS_SINGLE, out);
+}
+
+int qs_create_ex(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out) {
     if (!out) return set_error(QS_ERR_NULL, "null output pointer");
     *out = nullptr;
     if (num_qubits < 1) return set_error(QS_ERR_VALUE, "num_qubits must be >= 1");
+    if (precision != QS_SINGLE && precision != QS_DOUBLE)
+        return set_error(QS_ERR_VALUE, "precision must be QS_SINGLE or QS_DOUBLE");
+    const int shift = precision == QS_DOUBLE ? 4 : 3;  // log2 bytes per amplitude
     if (num_qubits > 300)
         return set_error(QS_ERR_CAPACITY, std::to_string(num_qubits) +
                                               " qubits is past the supported limit of 300");
@@ -132,11 +140,12 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
             budget = (unsigned long long)(free_b + pool_cached(device)) * 3 / 4;
         }
     }
-    // need_bytes = memory_required // 8 = 8 * 2^n (state.py:71-83, 134)
-    if (num_qubits > 60 || (8ull << num_qubits) > budget) {
-        std::string need = num_qubits > 60 ? std::string("more than 2^63 bytes")
-                                           : format_bytes(8ull << num_qubits) + " (" +
-                                                 std::to_string(8ull << num_qubits) + " bytes)";
+    // need_bytes = memory_required // 8 = (8 or 16) * 2^n (state.py:71-83, 134)
+    const unsigned long long need_b = num_qubits > 59 ? 0ull : (1ull << (num_qubits + shift));
+    if (num_qubits > 59 || need_b > budget) {
+        std::string need = num_qubits > 59 ? std::string("more than 2^63 bytes")
+                                           : format_bytes(need_b) + " (" + std::to_string(need_b) +
+                                                 " bytes)";
         return set_error(QS_ERR_CAPACITY, std::to_string(num_qubits) + " qubits need " + need +
                                               "; memory budget is " + format_bytes(budget));
     }
@@ -144,17 +153,17 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
     std::memset(s, 0, sizeof *s);
     s->num_qubits = num_qubits;
     s->device = device;
-    cudaError_t e = pool_alloc(device, 8ull << num_qubits, (void **)&s->amps);
+    s->prec = precision;
+    cudaError_t e = pool_alloc(device, need_b, (void **)&s->amps);
     if (e != cudaSuccess) {
         delete s;
         cudaGetLastError();
-        return set_error(QS_ERR_CAPACITY, std::string("cudaMalloc of ") +
-                                              std::to_string(8ull << num_qubits) +
+        return set_error(QS_ERR_CAPACITY, std::string("cudaMalloc of ") + std::to_string(need_b) +
                                               " bytes failed: " + cudaGetErrorString(e));
     }
     e = stream_acquire(device, &s->stream);
     if (e != cudaSuccess) {
-        pool_free(device, s->amps, 8ull << num_qubits);
+        pool_free(device, s->amps, need_b);
         delete s;
         return cuda_fail(e, "cudaStreamCreateWithFlags");
     }
@@ -162,7 +171,7 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
     int rc = launch_reset(s, 0);
     if (rc != QS_OK) {
         stream_release(device, s->stream);
-        pool_free(device, s->amps, 8ull << num_qubits);
+        pool_free(device, s->amps, need_b);
         delete s;
         return rc;
     }
@@ -174,7 +183,7 @@ int qs_destroy(qs_state *s) {
     if (!s) return QS_OK;
     DeviceGuard guard(s->device);
     cudaStreamSynchronize(s->stream);  // the buffers may be recycled right away
-    pool_free(s->device, s->amps, 8ull << s->num_qubits);
+    pool_free(s->device, s->amps, state_bytes(s));
     pool_free(s->device, s->scratch, s->scratch_bytes);
     if (s->ops_dev) cudaFree(s->ops_dev);
     if (s->pinned) cudaFreeHost(s->pinned);
@@ -187,6 +196,13 @@ int qs_num_qubits(const qs_state *s, int *out) {
     CHECK_HANDLE(s);
     if (!out) return set_error(QS_ERR_NULL, "null output pointer");
     *out = s->num_qubits;
+    return QS_OK;
+}
+
+int qs_precision(const qs_state *s, int *out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = s->prec;
     return QS_OK;
 }
 
@@ -229,44 +245,76 @@ int qs_synchronize(qs_state *s) {
     return QS_OK;
 }
 
-// apply_gate: pkg/src/pairsim/kernel.py:108-132
-int qs_apply_gate(qs_state *s, int target, const float m[8]) {
+// Gate entry points share the reference's check order (kernel.py:115-116,
+// 145-150) and dispatch on the register's precision: complex64 sweeps take
+// float32 entries (np.complex64-rounded), complex128 sweeps fp64 entries.
+static int check_gate(const qs_state *s, const void *m, int target, int nctrl, const int *ctrl) {
     CHECK_HANDLE(s);
     if (!m) return set_error(QS_ERR_NULL, "null gate matrix");
     int rc = check_qubit(s, target, "target");
     if (rc) return rc;
+    for (int i = 0; i < nctrl; ++i) {
+        rc = check_qubit(s, ctrl[i], "control");
+        if (rc) return rc;
+    }
+    for (int i = 0; i < nctrl; ++i)
+        if (ctrl[i] == target) return set_error(QS_ERR_VALUE, "control and target must differ");
+    if (nctrl == 2 && ctrl[0] == ctrl[1]) return set_error(QS_ERR_VALUE, "the two controls must differ");
+    return QS_OK;
+}
+
+static int sweep_f32(qs_state *s, int target, uint64_t cmask, const float m[8]) {
     DeviceGuard guard(s->device);
-    return launch_sweep(s, target, 0ull, m);
+    if (s->prec == QS_DOUBLE) {
+        double md[8];
+        for (int i = 0; i < 8; ++i) md[i] = (double)m[i];  // exact widening
+        return launch_sweep_d(s, target, cmask, md);
+    }
+    return launch_sweep(s, target, cmask, m);
+}
+
+static int sweep_f64(qs_state *s, int target, uint64_t cmask, const double m[8]) {
+    DeviceGuard guard(s->device);
+    if (s->prec == QS_DOUBLE) return launch_sweep_d(s, target, cmask, m);
+    float mf[8];
+    for (int i = 0; i < 8; ++i) mf[i] = (float)m[i];  // round to nearest, as np.complex64(x)
+    return launch_sweep(s, target, cmask, mf);
+}
+
+// apply_gate: pkg/src/pairsim/kernel.py:108-132
+int qs_apply_gate(qs_state *s, int target, const float m[8]) {
+    int rc = check_gate(s, m, target, 0, nullptr);
+    return rc ? rc : sweep_f32(s, target, 0ull, m);
+}
+
+int qs_apply_gate_f64(qs_state *s, int target, const double m[8]) {
+    int rc = check_gate(s, m, target, 0, nullptr);
+    return rc ? rc : sweep_f64(s, target, 0ull, m);
 }
 
 // apply_controlled_gate: pkg/src/pairsim/kernel.py:135-165 (same check order)
 int qs_apply_controlled_gate(qs_state *s, int control, int target, const float m[8]) {
-    CHECK_HANDLE(s);
-    if (!m) return set_error(QS_ERR_NULL, "null gate matrix");
-    int rc = check_qubit(s, target, "target");
-    if (rc) return rc;
-    rc = check_qubit(s, control, "control");
-    if (rc) return rc;
-    if (control == target) return set_error(QS_ERR_VALUE, "control and target must differ");
-    DeviceGuard guard(s->device);
-    return launch_sweep(s, target, 1ull << control, m);
+    int rc = check_gate(s, m, target, 1, &control);
+    return rc ? rc : sweep_f32(s, target, 1ull << control, m);
+}
+
+int qs_apply_controlled_gate_f64(qs_state *s, int control, int target, const double m[8]) {
+    int rc = check_gate(s, m, target, 1, &control);
+    return rc ? rc : sweep_f64(s, target, 1ull << control, m);
 }
 
 int qs_apply_controlled_controlled_gate(qs_state *s, int c1, int c2, int target,
                                         const float m[8]) {
-    CHECK_HANDLE(s);
-    if (!m) return set_error(QS_ERR_NULL, "null gate matrix");
-    int rc = check_qubit(s, target, "target");
-    if (rc) return rc;
-    rc = check_qubit(s, c1, "control");
-    if (rc) return rc;
-    rc = check_qubit(s, c2, "control");
-    if (rc) return rc;
-    if (c1 == target || c2 == target)
-        return set_error(QS_ERR_VALUE, "control and target must differ");
-    if (c1 == c2) return set_error(QS_ERR_VALUE, "the two controls must differ");
-    DeviceGuard guard(s->device);
-    return launch_sweep(s, target, (1ull << c1) | (1ull << c2), m);
+    const int c[2] = {c1, c2};
+    int rc = check_gate(s, m, target, 2, c);
+    return rc ? rc : sweep_f32(s, target, (1ull << c1) | (1ull << c2), m);
+}
+
+int qs_apply_controlled_controlled_gate_f64(qs_state *s, int c1, int c2, int target,
+                                            const double m[8]) {
+    const int c[2] = {c1, c2};
+    int rc = check_gate(s, m, target, 2, c);
+    return rc ? rc : sweep_f64(s, target, (1ull << c1) | (1ull << c2), m);
 }
 
 int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops,
@@ -275,7 +323,34 @@ int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_
     if (nops == 0) return QS_OK;
     if (!ops || !tile_qubits) return set_error(QS_ERR_NULL, "null op list or tile qubit list");
     DeviceGuard guard(s->device);
+    if (s->prec == QS_DOUBLE) {  // exact widening of the float32 entries
+        std::vector<qs_op64> wide((size_t)nops);
+        for (int i = 0; i < nops; ++i) {
+            wide[i].kind = ops[i].kind;
+            wide[i].target = ops[i].target;
+            wide[i].ctrl_mask = ops[i].ctrl_mask;
+            for (int k = 0; k < 8; ++k) wide[i].m[k] = (double)ops[i].m[k];
+        }
+        return run_fused_d(s, wide.data(), nops);
+    }
     return run_fused(s, tile_qubits, ntile, ops, nops);
+}
+
+int qs_apply_fused_f64(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops,
+                       int nops) {
+    CHECK_HANDLE(s);
+    if (nops == 0) return QS_OK;
+    if (!ops || !tile_qubits) return set_error(QS_ERR_NULL, "null op list or tile qubit list");
+    DeviceGuard guard(s->device);
+    if (s->prec == QS_DOUBLE) return run_fused_d(s, ops, nops);
+    std::vector<qs_op> narrow((size_t)nops);
+    for (int i = 0; i < nops; ++i) {
+        narrow[i].kind = ops[i].kind;
+        narrow[i].target = ops[i].target;
+        narrow[i].ctrl_mask = ops[i].ctrl_mask;
+        for (int k = 0; k < 8; ++k) narrow[i].m[k] = (float)ops[i].m[k];
+    }
+    return run_fused(s, tile_qubits, ntile, narrow.data(), nops);
 }
 
 int qs_swap_qubits(qs_state *s, int q1, int q2) {
@@ -286,7 +361,8 @@ int qs_swap_qubits(qs_state *s, int q1, int q2) {
     if (rc) return rc;
     if (q1 == q2) return QS_OK;
     DeviceGuard guard(s->device);
-    return launch_swap(s, q1 < q2 ? q1 : q2, q1 < q2 ? q2 : q1);
+    const int lo = q1 < q2 ? q1 : q2, hi = q1 < q2 ? q2 : q1;
+    return s->prec == QS_DOUBLE ? launch_swap_d(s, lo, hi) : launch_swap(s, lo, hi);
 }
 
 static int check_range(const qs_state *s, uint64_t offset, uint64_t count) {
@@ -298,53 +374,53 @@ static int check_range(const qs_state *s, uint64_t offset, uint64_t count) {
     return QS_OK;
 }
 
-int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, float *host) {
+int qs_get_amplitudes(qs_state *s, uint64_t offset, uint64_t count, void *host) {
     CHECK_HANDLE(s);
     int rc = check_range(s, offset, count);
     if (rc) return rc;
     if (count == 0) return QS_OK;
     if (!host) return set_error(QS_ERR_NULL, "null host buffer");
     DeviceGuard guard(s->device);
-    QS_CUDA(cudaMemcpyAsync(host, s->amps + offset, count * 8ull, cudaMemcpyDeviceToHost,
+    QS_CUDA(cudaMemcpyAsync(host, (char *)s->amps + offset * amp_bytes(s), count * amp_bytes(s), cudaMemcpyDeviceToHost,
                             s->stream));
     QS_CUDA(cudaStreamSynchronize(s->stream));
     return QS_OK;
 }
 
-int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const float *host) {
+int qs_set_amplitudes(qs_state *s, uint64_t offset, uint64_t count, const void *host) {
     CHECK_HANDLE(s);
     int rc = check_range(s, offset, count);
     if (rc) return rc;
     if (count == 0) return QS_OK;
     if (!host) return set_error(QS_ERR_NULL, "null host buffer");
     DeviceGuard guard(s->device);
-    QS_CUDA(cudaMemcpyAsync(s->amps + offset, host, count * 8ull, cudaMemcpyHostToDevice,
+    QS_CUDA(cudaMemcpyAsync((char *)s->amps + offset * amp_bytes(s), host, count * amp_bytes(s), cudaMemcpyHostToDevice,
                             s->stream));
     // the caller may reuse `host` as soon as we return
     QS_CUDA(cudaStreamSynchronize(s->stream));
     return QS_OK;
 }
 
-int qs_set_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, const float *host) {
+int qs_set_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, const void *host) {
     CHECK_HANDLE(s);
     int rc = check_range(s, offset, count);
     if (rc) return rc;
     if (count == 0) return QS_OK;
     if (!host) return set_error(QS_ERR_NULL, "null host buffer");
     DeviceGuard guard(s->device);
-    QS_CUDA(cudaMemcpyAsync(s->amps + offset, host, count * 8ull, cudaMemcpyHostToDevice,
+    QS_CUDA(cudaMemcpyAsync((char *)s->amps + offset * amp_bytes(s), host, count * amp_bytes(s), cudaMemcpyHostToDevice,
                             s->stream));
     return QS_OK;
 }
 
-int qs_get_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, float *host) {
+int qs_get_amplitudes_async(qs_state *s, uint64_t offset, uint64_t count, void *host) {
     CHECK_HANDLE(s);
     int rc = check_range(s, offset, count);
     if (rc) return rc;
     if (count == 0) return QS_OK;
     if (!host) return set_error(QS_ERR_NULL, "null host buffer");
     DeviceGuard guard(s->device);
-    QS_CUDA(cudaMemcpyAsync(host, s->amps + offset, count * 8ull, cudaMemcpyDeviceToHost,
+    QS_CUDA(cudaMemcpyAsync(host, (char *)s->amps + offset * amp_bytes(s), count * amp_bytes(s), cudaMemcpyDeviceToHost,
                             s->stream));
     return QS_OK;
 }

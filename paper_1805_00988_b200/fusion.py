@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .gates import is_phase, m8
+from .gates import is_phase, m8_for
 
 LOW = 6
 
@@ -33,7 +33,9 @@ class Pass:
     ops: list[tuple[int, int, int, np.ndarray]] = field(default_factory=list)  # (kind, target, ctrl_mask, m8)
 
     def op_array(self) -> np.ndarray:
-        arr = np.zeros(len(self.ops), dtype=N.OP_DTYPE)
+        """qs_op records (float32 entries) or qs_op64 (float64, complex128 registers)."""
+        double = bool(self.ops) and self.ops[0][3].dtype == np.float64
+        arr = np.zeros(len(self.ops), dtype=N.OP64_DTYPE if double else N.OP_DTYPE)
         for i, (kind, t, cm, m) in enumerate(self.ops):
             arr[i]["kind"] = kind
             arr[i]["target"] = t
@@ -42,8 +44,8 @@ class Pass:
         return arr
 
 
-def lower(gate, target: int, controls=()) -> tuple[int, int, int, np.ndarray]:
-    m = m8(gate)
+def lower(gate, target: int, controls=(), double: bool = False) -> tuple[int, int, int, np.ndarray]:
+    m = m8_for(gate, double)
     cm = 0
     for c in controls:
         cm |= 1 << int(c)
@@ -95,14 +97,19 @@ def _single(state, kind, t, cm, m) -> None:
     """One op: the dedicated sweep kernels (the phase kernel for diagonal ops)."""
     L = N.lib()
     ctrls = [q for q in range(64) if (cm >> q) & 1]
-    mp = N.f32ptr(np.ascontiguousarray(m, dtype=np.float32))
+    if m.dtype == np.float64:  # fp64 entries (complex128 registers)
+        mp = N.f64ptr(np.ascontiguousarray(m))
+        g1, g2, g3 = L.qs_apply_gate_f64, L.qs_apply_controlled_gate_f64, L.qs_apply_controlled_controlled_gate_f64
+    else:
+        mp = N.f32ptr(np.ascontiguousarray(m, dtype=np.float32))
+        g1, g2, g3 = L.qs_apply_gate, L.qs_apply_controlled_gate, L.qs_apply_controlled_controlled_gate
     if not ctrls:
-        N.check(L.qs_apply_gate(state.handle, t, mp))
+        N.check(g1(state.handle, t, mp))
     elif len(ctrls) == 1:
-        N.check(L.qs_apply_controlled_gate(state.handle, ctrls[0], t, mp))
+        N.check(g2(state.handle, ctrls[0], t, mp))
     elif len(ctrls) == 2:
-        N.check(L.qs_apply_controlled_controlled_gate(state.handle, ctrls[0], ctrls[1], t, mp))
+        N.check(g3(state.handle, ctrls[0], ctrls[1], t, mp))
     else:  # >2 controls: a one-op pass (the library dispatches it to the sweep kernel)
-        op = np.zeros(1, dtype=N.OP_DTYPE)
+        op = np.zeros(1, dtype=N.OP64_DTYPE if m.dtype == np.float64 else N.OP_DTYPE)
         op[0]["kind"], op[0]["target"], op[0]["ctrl_mask"], op[0]["m"] = kind, t, cm, m
         state.apply_fused([t], op)

@@ -14,8 +14,9 @@ every device operation, so in-place edits such as ``state.amps[:] = v``
 (pkg/tests/test_kernel.py:37) behave exactly as with a numpy-resident
 register.  Code that never touches ``.amps`` never pays a host copy.
 
-Only complex64 (Precision.SINGLE) registers exist on the device; the
-reference's DOUBLE precision is rejected with ValueError.
+Both reference precisions live on the device: Precision.SINGLE registers are
+complex64, Precision.DOUBLE registers complex128 (gates64.cu), so the
+reference's fp64 acceptance criteria (1e-10 vs the dense oracle) apply too.
 """
 
 from __future__ import annotations
@@ -65,7 +66,7 @@ MAX_SUPPORTED_QUBITS = 300  # state.py:20
 
 
 class Precision(enum.Enum):
-    """state.py:25-42; the device stores SINGLE (complex64) only."""
+    """state.py:25-42; SINGLE = complex64, DOUBLE = complex128 in HBM."""
 
     SINGLE = "single"
     DOUBLE = "double"
@@ -132,9 +133,7 @@ class StateVector:
             raise ValueError(f"expected {dim} amplitudes, got shape {arr.shape}")
         if arr.dtype not in (np.complex64, np.complex128):
             raise ValueError(f"unsupported amplitude dtype {arr.dtype}")
-        if arr.dtype != np.complex64:
-            raise ValueError("the B200 backend stores complex64 amplitudes only")
-        self._dev = State(self.num_qubits, _device())
+        self._dev = State(self.num_qubits, _device(), precision=arr.dtype)
         self._dev.set_amplitudes(arr)
 
     @property
@@ -143,7 +142,7 @@ class StateVector:
 
     @property
     def precision(self) -> Precision:
-        return Precision.SINGLE
+        return Precision.DOUBLE if self._dev.is_double else Precision.SINGLE
 
     @property
     def device_state(self) -> State:
@@ -158,8 +157,8 @@ class StateVector:
     @amps.setter
     def amps(self, value) -> None:
         arr = np.asarray(value)
-        if arr.shape != (self.dim,) or arr.dtype != np.complex64:
-            raise ValueError("amps must be a complex64 array of length 2^n")
+        if arr.shape != (self.dim,) or arr.dtype != self._dev.dtype:
+            raise ValueError(f"amps must be a {self._dev.dtype} array of length 2^n")
         self._mirror = arr
         self._dev.set_amplitudes(arr)
 
@@ -178,14 +177,12 @@ def new_state(num_qubits: int, precision: Precision = Precision.SINGLE, memory_b
     """|0...0> on the device; CapacityError before allocation (state.py:122-143)."""
     if num_qubits < 1:
         raise ValueError("num_qubits must be >= 1")
-    if precision is not Precision.SINGLE:
-        raise ValueError("the B200 backend stores complex64 (Precision.SINGLE) only")
     need = memory_required(num_qubits, precision) // 8
     if memory_budget is not None and need > memory_budget:
         raise CapacityError(
             f"{num_qubits} qubits need {format_bytes(need)} ({need} bytes); "
             f"memory budget is {format_bytes(memory_budget)}")
-    dev = State(num_qubits, _device(), memory_budget=memory_budget)
+    dev = State(num_qubits, _device(), memory_budget=memory_budget, precision=precision.value)
     return StateVector(num_qubits, _dev=dev)
 
 

@@ -2,12 +2,13 @@
 
 API (north_star; PAPER.md:668-678, 949-970):
     s = State(n)                        # |0...0>, complex64 in HBM
+    s = State(n, precision="double")    # complex128 (pairsim Precision.DOUBLE)
     s.apply_gate(gate, target)
     s.apply_controlled_gate(gate, control, target)
     s.apply_controlled_controlled_gate(gate, c1, c2, target)
     s.h(t) s.x(t) s.y(t) s.z(t) s.s(t) s.t(t) s.u1(t, theta)
     s.cx(c, t) s.cu1(c, t, theta) s.ccx(c1, c2, t)  # control(s) first
-    s.amplitudes() -> complex64 ndarray
+    s.amplitudes() -> complex64 (complex128) ndarray
     s.probabilities() -> float64 ndarray
     s.measure(samples=1000, seed=None) -> {basis_index: count}
     s.flush(); s.backend.queue.finish()  # device barrier
@@ -24,7 +25,7 @@ import math
 import numpy as np
 
 from . import _native as N
-from .gates import FIXED_GATES, Gate, m8, u1 as _u1
+from .gates import FIXED_GATES, Gate, m8_for, u1 as _u1
 
 
 class _Queue:
@@ -42,17 +43,39 @@ class _Backend:
         self.queue = _Queue(state)
 
 
+def _precision_code(precision) -> int:
+    """'single' / 'double', numpy complex dtypes, or pairsim Precision members."""
+    v = getattr(precision, "value", precision)
+    if isinstance(v, str) and v.lower() in ("single", "complex64", "c64"):
+        return N.QS_SINGLE
+    if isinstance(v, str) and v.lower() in ("double", "complex128", "c128"):
+        return N.QS_DOUBLE
+    try:
+        dt = np.dtype(v)
+    except TypeError:
+        dt = None
+    if dt == np.complex64:
+        return N.QS_SINGLE
+    if dt == np.complex128:
+        return N.QS_DOUBLE
+    raise ValueError(f"unsupported precision {precision!r}")
+
+
 class State:
-    def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None):
+    def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None,
+                 precision="single"):
         if not isinstance(num_qubits, (int, np.integer)):
             raise TypeError("num_qubits must be an integer")
         if num_qubits < 1:
             raise ValueError("num_qubits must be >= 1")
+        prec = _precision_code(precision)
         self._h = ctypes.c_void_p()
-        N.check(N.lib().qs_create(int(num_qubits), int(device), int(memory_budget or 0),
-                                  ctypes.byref(self._h)))
+        N.check(N.lib().qs_create_ex(int(num_qubits), int(device), int(memory_budget or 0), prec,
+                                     ctypes.byref(self._h)))
         self.num_qubits = int(num_qubits)
         self.device = int(device)
+        self.is_double = prec == N.QS_DOUBLE
+        self.dtype = np.dtype(np.complex128 if self.is_double else np.complex64)
         self.backend = _Backend(self)
 
     # -- lifecycle ------------------------------------------------------------
@@ -101,28 +124,44 @@ class State:
         return self
 
     # -- gates ----------------------------------------------------------------
+    # Gate entries are rounded to the register's precision first
+    # (kernel.py:118-119): float32 entry points for complex64, fp64 for complex128.
+    def _m(self, gate):
+        m = m8_for(gate, self.is_double)
+        return N.f64ptr(m) if self.is_double else N.f32ptr(m), m
+
     def apply_gate(self, gate, target: int) -> "State":
-        m = m8(gate)
-        N.check(N.lib().qs_apply_gate(self.handle, int(target), N.f32ptr(m)))
+        mp, _keep = self._m(gate)
+        L = N.lib()
+        fn = L.qs_apply_gate_f64 if self.is_double else L.qs_apply_gate
+        N.check(fn(self.handle, int(target), mp))
         return self
 
     def apply_controlled_gate(self, gate, control: int, target: int) -> "State":
-        m = m8(gate)
-        N.check(N.lib().qs_apply_controlled_gate(self.handle, int(control), int(target), N.f32ptr(m)))
+        mp, _keep = self._m(gate)
+        L = N.lib()
+        fn = L.qs_apply_controlled_gate_f64 if self.is_double else L.qs_apply_controlled_gate
+        N.check(fn(self.handle, int(control), int(target), mp))
         return self
 
     def apply_controlled_controlled_gate(self, gate, control1: int, control2: int, target: int) -> "State":
-        m = m8(gate)
-        N.check(N.lib().qs_apply_controlled_controlled_gate(
-            self.handle, int(control1), int(control2), int(target), N.f32ptr(m)))
+        mp, _keep = self._m(gate)
+        L = N.lib()
+        fn = (L.qs_apply_controlled_controlled_gate_f64 if self.is_double
+              else L.qs_apply_controlled_controlled_gate)
+        N.check(fn(self.handle, int(control1), int(control2), int(target), mp))
         return self
 
     def apply_fused(self, tile_qubits, ops: np.ndarray) -> "State":
-        """One fused HBM pass (see fusion.py for the planner)."""
+        """One fused HBM pass (see fusion.py for the planner).  `ops` is an
+        OP_DTYPE (float32 entries) or OP64_DTYPE (fp64 entries) record array."""
         tq = np.ascontiguousarray(np.asarray(tile_qubits, dtype=np.int32))
-        ops = np.ascontiguousarray(ops, dtype=N.OP_DTYPE)
-        N.check(N.lib().qs_apply_fused(self.handle, tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                       int(tq.size), ops.ctypes.data, int(ops.size)))
+        wide = np.asarray(ops).dtype == N.OP64_DTYPE
+        ops = np.ascontiguousarray(ops, dtype=N.OP64_DTYPE if wide else N.OP_DTYPE)
+        L = N.lib()
+        fn = L.qs_apply_fused_f64 if wide else L.qs_apply_fused
+        N.check(fn(self.handle, tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                   int(tq.size), ops.ctypes.data, int(ops.size)))
         return self
 
     def swap_qubits(self, q1: int, q2: int) -> "State":
@@ -165,12 +204,12 @@ class State:
     # -- readout ----------------------------------------------------------------
     def amplitudes(self, offset: int = 0, count: int | None = None) -> np.ndarray:
         count = self.dim - offset if count is None else count
-        out = np.empty(count, dtype=np.complex64)
+        out = np.empty(count, dtype=self.dtype)
         N.check(N.lib().qs_get_amplitudes(self.handle, int(offset), int(count), out.ctypes.data))
         return out
 
     def set_amplitudes(self, values, offset: int = 0) -> "State":
-        v = np.ascontiguousarray(np.asarray(values), dtype=np.complex64)
+        v = np.ascontiguousarray(np.asarray(values), dtype=self.dtype)
         N.check(N.lib().qs_set_amplitudes(self.handle, int(offset), int(v.size), v.ctypes.data))
         return self
 
@@ -244,4 +283,5 @@ class State:
         return int(out.value)
 
     def __repr__(self) -> str:
-        return f"State(num_qubits={self.num_qubits}, device={self.device})"
+        prec = ", precision='double'" if self.is_double else ""
+        return f"State(num_qubits={self.num_qubits}, device={self.device}{prec})"

@@ -59,7 +59,7 @@ def m8(gate) -> np.ndarray:
 
 
 def digest(arr: np.ndarray) -> str:
-    if arr.dtype in (np.complex64, np.float32):
+    if arr.dtype in (np.complex64, np.float32, np.complex128, np.float64):
         arr = arr + arr.dtype.type(0)  # canonical zero sign
     return hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
 

@@ -8,21 +8,32 @@ from pathlib import Path
 import numpy as np
 
 GOLDEN = Path(__file__).resolve().parent / "golden" / "pairsim_golden.npz"
+GOLDEN_DOUBLE = Path(__file__).resolve().parent / "golden" / "pairsim_golden_double.npz"
 
-_cache = None
+_cache = {}
+
+
+def _load(path):
+    if path not in _cache:
+        z = np.load(path)
+        d = {k: z[k] for k in z.files}
+        d["meta"] = dict(zip(d["meta_keys"].tolist(), d["meta_vals"].tolist()))
+        _cache[path] = d
+    return _cache[path]
 
 
 def golden():
-    global _cache
-    if _cache is None:
-        z = np.load(GOLDEN)
-        _cache = {k: z[k] for k in z.files}
-        _cache["meta"] = dict(zip(_cache["meta_keys"].tolist(), _cache["meta_vals"].tolist()))
-    return _cache
+    """complex64 (Precision.SINGLE) fixtures: tests/golden/make_golden.py"""
+    return _load(GOLDEN)
+
+
+def golden_double():
+    """complex128 (Precision.DOUBLE) fixtures: tests/golden/make_golden_double.py"""
+    return _load(GOLDEN_DOUBLE)
 
 
 def digest(arr: np.ndarray) -> str:
-    if arr.dtype in (np.complex64, np.float32):
+    if arr.dtype in (np.complex64, np.float32, np.complex128, np.float64):
         arr = arr + arr.dtype.type(0)
     return hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
 
@@ -32,6 +43,18 @@ class M8Gate:
 
     def __init__(self, m8):
         m8 = np.asarray(m8, np.float32)
+        self.m8 = m8
+        self.a = complex(m8[0], m8[1])
+        self.b = complex(m8[2], m8[3])
+        self.c = complex(m8[4], m8[5])
+        self.d = complex(m8[6], m8[7])
+
+
+class M8DGate:
+    """Gate view over fp64 (a, b, c, d) entries (complex128 registers)."""
+
+    def __init__(self, m8):
+        m8 = np.asarray(m8, np.float64)
         self.m8 = m8
         self.a = complex(m8[0], m8[1])
         self.b = complex(m8[2], m8[3])

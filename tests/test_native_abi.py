@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert N.lib().qs_abi_version() == 1
+    assert N.lib().qs_abi_version() == 2
 
 
 def test_sm100a_cubin_embedded():

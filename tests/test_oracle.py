@@ -14,7 +14,7 @@ import math
 import numpy as np
 import pytest
 
-from golden_util import H_M8, X_M8, M8Gate, digest, golden, hist_from_outcomes
+from golden_util import H_M8, X_M8, M8DGate, M8Gate, digest, golden, golden_double, hist_from_outcomes
 from oracle import c as oc
 from oracle import port
 
@@ -186,3 +186,64 @@ class TestDoublyControlled:
         amps = g[f"{key}_in"].copy()
         oc.apply_cc_gate(amps, c1, c2, t, M8Gate(X_M8))
         np.testing.assert_allclose(amps, g[f"{key}_out"], atol=2e-6)
+
+
+# ---- complex128 (Precision.DOUBLE) restatement vs pairsim DOUBLE outputs ----
+def replay_c_double(amps, ops, mats):
+    for (kind, c1, c2, t), m in zip(ops, mats):
+        g = M8DGate(m)
+        if kind == 0:
+            oc.apply_gate(amps, int(t), g)
+        elif kind == 1:
+            oc.apply_controlled_gate(amps, int(c1), int(t), g)
+        else:
+            oc.apply_cc_gate(amps, int(c1), int(c2), int(t), g)
+        yield amps
+
+
+class TestDoublePrecision:
+    """tests/golden/make_golden_double.py: the reference on complex128 registers."""
+
+    @pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 7, 8, 10])
+    def test_c_oracle_every_op(self, n):
+        g = golden_double()
+        states = g[f"trace{n}_states"]
+        assert states.dtype == np.complex128
+        amps = states[0].copy()
+        for k, cur in enumerate(replay_c_double(amps, g[f"trace{n}_ops"], g[f"trace{n}_mats"])):
+            assert cur.tobytes() == states[k + 1].tobytes(), f"op {k}"
+
+    @pytest.mark.parametrize("n", [12, 14])
+    def test_c_oracle_big_digest(self, n):
+        g = golden_double()
+        amps = g[f"tracebig{n}_in"].copy()
+        for _ in replay_c_double(amps, g[f"tracebig{n}_ops"], g[f"tracebig{n}_mats"]):
+            pass
+        assert digest(amps) == g["meta"][f"tracebig{n}_final"]
+
+    def test_probabilities(self):
+        g = golden_double()
+        assert oc.probabilities(g["probs10_amps"]).tobytes() == g["probs10"].tobytes()
+
+    @pytest.mark.parametrize("name", ["rand10", "decay13"])
+    @pytest.mark.parametrize("seed", [0, 7, 12345])
+    def test_sample_histograms(self, name, seed):
+        g = golden_double()
+        keys, counts = hist_from_outcomes(oc.sample_outcomes(g[f"samp_{name}_amps"], 5000, seed))
+        assert np.array_equal(keys, g[f"samp_{name}_s{seed}_keys"])
+        assert np.array_equal(counts, g[f"samp_{name}_s{seed}_counts"])
+
+    @pytest.mark.parametrize("name", ["rand10", "decay13"])
+    def test_collapse_outcomes(self, name):
+        g = golden_double()
+        amps = g[f"samp_{name}_amps"]
+        got = [int(oc.sample_outcomes(amps, 1, seed)[0]) for seed in range(20)]
+        assert got == g[f"samp_{name}_collapse"].tolist()
+
+    @pytest.mark.parametrize("key", ["tof_012", "tof_402"])
+    def test_cc_x_matches_toffoli_decomposition(self, key):
+        g = golden_double()
+        c1, c2, t = (int(ch) for ch in key[4:])
+        amps = g[f"{key}_in"].copy()
+        oc.apply_cc_gate(amps, c1, c2, t, M8DGate(np.array([0, 0, 1, 0, 1, 0, 0, 0], np.float64)))
+        np.testing.assert_allclose(amps, g[f"{key}_out"], atol=1e-14)

@@ -214,9 +214,15 @@ class TestState:  # pkg/tests/test_state.py
         for n, text in [(5, "256 B"), (10, "8.192 kB"), (20, "8.389 MB"), (25, "268.4 MB"), (30, "8.59 GB")]:
             assert ps.format_bytes(ps.memory_required(n) // 8) == text
 
-    def test_double_rejected(self):
-        with pytest.raises(ValueError):
-            ps.new_state(2, ps.Precision.DOUBLE)
+    def test_double_register(self):
+        """Precision.DOUBLE lives on the device as complex128 (state.py:25-42);
+        its budget check counts 16 bytes per amplitude (state.py:71-83)."""
+        sv = ps.new_state(2, ps.Precision.DOUBLE)
+        assert sv.precision is ps.Precision.DOUBLE
+        assert sv.amps.dtype == np.complex128 and sv.amps[0] == 1
+        with pytest.raises(ps.CapacityError):
+            ps.new_state(10, ps.Precision.DOUBLE, memory_budget=16 * 1024 - 1)
+        ps.new_state(10, ps.Precision.DOUBLE, memory_budget=16 * 1024)
 
     def test_amplitude_out_of_range(self):
         with pytest.raises(IndexError):
