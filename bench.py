@@ -371,7 +371,10 @@ def run_sharded(args):
     rank, world, local = _dist_env()
     local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only in tests
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import datetime
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                            timeout=datetime.timedelta(minutes=10))
     g = int(round(math.log2(world)))
     if 1 << g != world:
         raise SystemExit("--gpus must be a power of two")
@@ -436,8 +439,12 @@ def run_sharded(args):
         e2e = {"value": k2 * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": (8 << L) * world,
                "d2h_bytes_per_step": (8 << L) * world, "steps": k2,
                "timing": "host wall clock, every rank uploads/downloads its shard around the layer, max over ranks"}
+    extras = {}
+    if world >= 4 and not args.no_extras:
+        extras["config5_hlayer_qft36"] = run_config5(st, eng, local, world)
     if rank == 0:
         print(json.dumps({
+            "extras": extras,
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
@@ -452,6 +459,58 @@ def run_sharded(args):
             "cpu_baseline": None,
         }))
     dist.destroy_process_group()
+
+
+def run_config5(st_main, eng_main, local, world):
+    """BASELINE config 5: a 36-qubit register sharded over the N GPUs (top
+    log2 N qubits), H on every qubit then build_qft(36), through
+    ShardedState.run (fused local passes + NCCL qubit swaps).  Device time on
+    every rank's stream, max over ranks.  Analytic check: QFT (no swaps) of the
+    uniform state is |0>, so amplitude 0 must be ~1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_00988_b200 import _native as N
+    from paper_1805_00988_b200 import build_hadamard_layer, build_qft
+    from paper_1805_00988_b200.sharded import ShardedState
+
+    n = 36
+    out = {"n_qubits": n, "shards": world}
+    try:
+        # free the headline registers (and the pool's cached buffers) first
+        eng_main.state.close()
+        N.lib().qs_release_cached(-1)
+        torch.cuda.synchronize(local)
+        st = ShardedState.distributed(n, device=local)
+        eng = st.engines[0]
+        stream = torch.cuda.ExternalStream(eng.state.stream(), device=torch.device("cuda", local))
+        torch.cuda.synchronize(local)
+        dist.barrier()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        evs[0].record(stream)
+        st.run(build_hadamard_layer(n))
+        evs[1].record(stream)
+        st.run(build_qft(n))
+        evs[2].record(stream)
+        torch.cuda.synchronize(local)
+        dist.barrier()
+        t = torch.tensor([evs[0].elapsed_time(evs[1]), evs[1].elapsed_time(evs[2])], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        h_ms, q_ms = (float(x) for x in t.tolist())
+        swaps = st.swaps
+        a0 = None
+        st.canonicalize()  # identity qubit map, so amplitude 0 is rank 0's first
+        if st.ranks[0] == 0:
+            a0 = complex(eng.state.amplitude(0))
+        out.update({"hlayer_s": h_ms / 1e3, "qft_s": q_ms / 1e3, "total_s": (h_ms + q_ms) / 1e3,
+                    "qft_gates": build_qft(n).gate_count(), "global_qubit_swaps": swaps,
+                    "shard_bytes": 8 << (n - int(math.log2(world)))})
+        if a0 is not None:
+            out["amp0_after_qft"] = [a0.real, a0.imag]
+            out["analytic_check_ok"] = bool(abs(abs(a0) - 1.0) < 1e-2)
+    except Exception as exc:  # noqa: BLE001
+        out["error"] = f"{type(exc).__name__}: {exc}"
+    return out
 
 
 def run_extras(st, stream, n, cpu=True):
@@ -525,6 +584,32 @@ def run_extras(st, stream, n, cpu=True):
     res["config3_qft28_fused"] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
                                   "effective_gates_per_s": circ.gate_count() / (ms / 1e3)}
     s28.close()
+
+    # complex128 (Precision.DOUBLE) sweeps: a 29-qubit register is 8 GiB like
+    # the headline one; each sweep moves 32 * 2^29 algorithmic bytes
+    from paper_1805_00988_b200.gates import H as _H
+
+    sd = State(29, precision="double")
+    sd_stream = torch.cuda.ExternalStream(sd.stream())
+    for q in range(29):
+        sd.apply_gate(_H, q)
+    sd.flush()
+    per = []
+    for q in range(29):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(sd_stream)
+        for _ in range(3):
+            sd.apply_gate(_H, q)
+        b.record(sd_stream)
+        sd.flush()
+        per.append(a.elapsed_time(b) / 3)
+    avg = sum(per) / len(per)
+    res["c128_hsweep29"] = {"ms_per_sweep_avg": avg, "ms_per_target": [round(x, 4) for x in per],
+                            "algorithmic_bytes_per_sweep": 32 << 29,
+                            "achieved_GBps": (32 << 29) / (avg / 1e3) / 1e9,
+                            "note": "complex128 register (8 GiB), H on every target, 3 reps each, CUDA events"}
+    sd.close()
 
     # config 4: 32-qubit layered random H/T/CX circuit, depth 20, fused
     try:

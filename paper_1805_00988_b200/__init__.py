@@ -5,6 +5,7 @@ Public surface:
   * :mod:`paper_1805_00988_b200.pairsim` — pairsim-compatible function API
   * circuits / fusion — IR, builders and the fused-pass planner
   * sharded — registers sharded over P GPUs on their top log2(P) qubits
+  * qc / cli — the reference's .qc text format and run/state/bv front-end
 
 All compute runs in libqsb200.so (hand-written sm_100a CUDA behind the C ABI
 in include/qsb200.h); there is no CPU fallback.
@@ -26,5 +27,7 @@ from .circuits import (  # noqa: F401
     layered_random_circuit,
     random_circuit,
 )
+
+from .qc import format_circuit, parse_circuit  # noqa: F401
 
 __version__ = "0.1.0"

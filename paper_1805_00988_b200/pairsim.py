@@ -60,6 +60,7 @@ from .gates import (  # noqa: F401
     std_gate,
     u1,
 )
+from .qc import format_circuit, parse_circuit  # noqa: F401  (circuits.py:86-168)
 from .state import State
 
 MAX_SUPPORTED_QUBITS = 300  # state.py:20
