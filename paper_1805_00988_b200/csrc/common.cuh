@@ -11,10 +11,16 @@
 // the expression.
 #pragma once
 
+#ifdef __CUDACC_RTC__  // NVRTC (run-time compiled pass kernels): no host headers
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#else
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "qsb200.h"
+#endif
 
 namespace qsb {
 

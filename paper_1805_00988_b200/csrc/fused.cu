@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -47,430 +48,27 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "fused_dev.cuh"
 #include "internal.h"
 
 namespace qsb {
 
+int jit_launch(qs_state *s, const FParams &p, int K, int RB, size_t bufs_bytes, unsigned grid,
+               unsigned block);
+
 namespace {
-
-constexpr int kLow = 6;      // local qubits 0..5 form one 512-B segment
-constexpr int kMaxRegBits = 4;  // RB: 2^RB float4 per thread (RB = 3 or 4)
-constexpr int kMaxK = 14;
-constexpr int kMaxWarpBits = 5;
-
-enum : int { kCplx = 0, kReal = 1, kHlike = 2, kSwap = 3 };
-
-// One op, lowered to the layout of the stage it runs in (48 bytes, staged
-// into shared memory once per CTA).
-struct __align__(16) FOp {
-    int variant;         // see kPhaseVariant
-    uint32_t reg_need;   // register-index bits that must be set (warp-uniform)
-    uint32_t tid_need;   // thread-id bits (lane | warp << 5) that must be set
-    uint32_t half_need;  // odd half only (control / phase bit on local qubit 0)
-    uint64_t ext_need;   // global qubits outside the tile that must be 1
-    float one;           // == 1.0f, loaded at run time (see rsum / csub)
-    int run;             // at a run head: number of consecutive ops with this variant
-    float m[8];
-};
-// pair variants: ((slot + 1) * 4 + class) * 2 + has_need, slot -1 = half;
-// phase variants: kPhaseVariant + reg_need * 2 + half_need
-constexpr int kPhaseVariant = 40;
-
-struct FStage {
-    int rf[kMaxRegBits];   // f-bit (f = local >> 1) of register bit r
-    int lf[5];             // f-bit of lane bit i
-    int wf[kMaxWarpBits];  // f-bit of warp bit w
-    int op_begin, op_end;
-};
-
-// Tile index -> global base: contiguous runs of non-tile qubits.
-constexpr int kMaxRuns = 16;
-struct Run {
-    int src, dst, len;
-};
-
-constexpr int kMaxOps = 320;
-constexpr int kNB = 3;  // tile buffers in the TMA ring
-constexpr int kMaxStages = 48;
-struct FParams {
-    CUtensorMap tmap;  // 64-B aligned, first member
-    int ncopies;       // TMA copies per tile (2^(K-9))
-    int crow[4];       // row-index bit of copy-index bit i
-    int n, K, nwbits, nstages, nruns, nops;
-    int dry;  // QSB_FUSED_DRY=1: move the tiles, skip the math (ring probe)
-    uint64_t ntiles;
-    int qpos[kMaxK];  // global qubit of local bit i
-    Run runs[kMaxRuns];
-    FStage stages[kMaxStages];
-    FOp ops[kMaxOps];  // copied to shared memory once per CTA
-};
-// The whole table travels as the kernel parameter block (<= 32764 bytes since
-// CUDA 12.1), so consecutive passes need no host synchronisation.
-static_assert(sizeof(FParams) < 32000, "kernel parameter block too large");
-
-// ---- PTX wrappers -----------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-// try_wait suspends in hardware between polls; after ~2^22 failed polls (far
-// beyond any legitimate TMA latency) the kernel traps instead of hanging.
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    const uint32_t addr = smem_u32(bar);
-    for (uint32_t spins = 0;; ++spins) {
-        uint32_t ok;
-        asm volatile(
-            "{\n"
-            ".reg .pred P;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, P;\n"
-            "}\n"
-            : "=r"(ok)
-            : "r"(addr), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (spins > (1u << 22)) __trap();
-    }
-}
-__device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes,
-                                          uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(smem_dst)),
-        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_store(void *gdst, const void *smem_src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-                 "r"(smem_u32(smem_src)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void tma_load_5d(void *smem_dst, const CUtensorMap *map, int row,
-                                            uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %2, %2, %2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
-        "l"(map), "r"(0), "r"(row), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, int row, const void *smem_src) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %1, %1, %1, %2}], [%3];" ::"l"(map),
-        "r"(0), "r"(row), "r"(smem_u32(smem_src))
-        : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-// ---- exact pair updates per gate class ----------------------------------------
-// real entry g (g.im == 0): fma(g, v.re, -rn(0*v.im)) == rn(g*v.re) and
-// fma(g, v.im, rn(0*v.re)) == rn(g*v.im) for every nonzero result.
-// ptxas (CUDA 12.9) contracts mul.rn.f32x2 feeding add.rn.f32x2 (and even
-// fma.rn.f32x2(x, 1.0, y), which it first folds to an add) into one FFMA2,
-// which would round a sum of two products once instead of three times.  The
-// sums below are fma(x, one, y) / fma(y, -one, x) with `one` == 1.0f loaded
-// from the op table at run time, so ptxas cannot fold them: exactly
-// rn(x + y) / rn(x - y), and the products stay separately rounded.  The GPU
-// parity tests compare every gate class bit for bit against the oracle.
-__device__ __forceinline__ float2 rmul(float g, float2 v) { return f2mul(make_float2(g, g), v); }
-__device__ __forceinline__ float2 rsum(float2 x, float2 y, float one) {
-    return f2fma(x, make_float2(one, one), y);
-}
-__device__ __forceinline__ float2 csub(float2 x, float2 y, float one) {
-    return f2fma(y, make_float2(-one, -one), x);
-}
-
-template <int CLS>
-__device__ __forceinline__ void pair_cls(const float *m, float one, float2 &va, float2 &vb) {
-    if (CLS == kCplx) {
-        float2 na = cadd(cmul(make_float2(m[0], m[1]), va), cmul(make_float2(m[2], m[3]), vb));
-        float2 nb = cadd(cmul(make_float2(m[6], m[7]), vb), cmul(make_float2(m[4], m[5]), va));
-        va = na;
-        vb = nb;
-    } else if (CLS == kReal) {
-        float2 na = rsum(rmul(m[0], va), rmul(m[2], vb), one);
-        float2 nb = rsum(rmul(m[6], vb), rmul(m[4], va), one);
-        va = na;
-        vb = nb;
-    } else if (CLS == kHlike) {
-        // c == a, d == -b: c*va == a*va and d*vb == -(b*vb) exactly
-        float2 p = rmul(m[0], va), q = rmul(m[2], vb);
-        va = rsum(p, q, one);
-        vb = csub(p, q, one);
-    } else {  // X: a == d == 0, b == c == 1 -> values swap
-        float2 t = va;
-        va = vb;
-        vb = t;
-    }
-}
-
-__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
-__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
-__device__ __forceinline__ float4 mk4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
-
-// T = register bit of the target (-1: the float4 half, local qubit 0);
-// NEED: the op has a control / phase bit on the register index or the half
-// (per-j warp-uniform tests); !NEED is the straight-line common case.
-template <int T, int CLS, bool NEED, int RB>
-__device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[1 << RB]) {
-    const uint32_t need = NEED ? op.reg_need : 0u;
-    const bool odd_only = NEED && op.half_need != 0;
-    const float one = op.one;
-    float m[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m[i] = (CLS == kSwap) ? 0.f : op.m[i];
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (T >= 0 && (j & (1 << T))) continue;
-        if (NEED && (j & need) != need) continue;  // warp-uniform
-        if (T < 0) {
-            float2 a = lo2(v[j]), b = hi2(v[j]);
-            pair_cls<CLS>(m, one, a, b);
-            v[j] = mk4(a, b);
-        } else {
-            const int k = j | (1 << (T < 0 ? 0 : T));
-            float2 a0 = lo2(v[j]), a1 = hi2(v[j]), b0 = lo2(v[k]), b1 = hi2(v[k]);
-            if (!odd_only) pair_cls<CLS>(m, one, a0, b0);
-            pair_cls<CLS>(m, one, a1, b1);
-            v[j] = mk4(a0, a1);
-            v[k] = mk4(b0, b1);
-        }
-    }
-}
-
-// Diagonal op: multiply the registers whose index has every bit of RNEED set
-// (compile-time pattern) by d; ODD: only the odd half (phase bit on local 0).
-template <int RNEED, bool ODD, int RB>
-__device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[1 << RB]) {
-    const float2 d = make_float2(op.m[6], op.m[7]);
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if ((j & RNEED) != RNEED) continue;
-        float2 a = lo2(v[j]), b = hi2(v[j]);
-        if (!ODD) a = cmul(d, a);
-        b = cmul(d, b);
-        v[j] = mk4(a, b);
-    }
-}
-
-// Classes with a straight-line (no per-j test) body; the complex and swap
-// bodies keep the per-j branch, which bounds ptxas' register demand there.
-__device__ constexpr bool kStraight[4] = {false, true, true, false};
-
-__device__ __forceinline__ bool op_ok(const FOp &op, uint32_t tid, uint64_t base) {
-    return (tid & op.tid_need) == op.tid_need && (base & op.ext_need) == op.ext_need;
-}
-
-template <int T, int C, bool NEED, int RB>
-__device__ __forceinline__ void run_pair(const FOp *ops, int len, uint32_t tid, uint64_t base,
-                                         float4 (&v)[1 << RB]) {
-    for (int k = 0; k < len; ++k)
-        if (op_ok(ops[k], tid, base)) apply_pair<T, C, NEED, RB>(ops[k], v);
-}
-
-template <int R, bool ODD, int RB>
-__device__ __forceinline__ void run_phase(const FOp *ops, int len, uint32_t tid, uint64_t base,
-                                          float4 (&v)[1 << RB]) {
-    for (int k = 0; k < len; ++k)
-        if (op_ok(ops[k], tid, base)) apply_phase<R, ODD, RB>(ops[k], v);
-}
-
-// One dispatch per RUN of consecutive ops with the same variant (the host
-// sets FOp::run at each run head): nvcc lowers the switch to a compare tree,
-// so QFT-style streams of same-pattern phase ops pay for it once per run.
-template <int RB>
-__device__ __forceinline__ void apply_run(int variant, const FOp *ops, int len, uint32_t tid,
-                                          uint64_t base, float4 (&v)[1 << RB]) {
-    switch (variant) {
-#define QSB_CASE(T, C)                                                                             \
-    case (((T) + 1) * 4 + (C)) * 2 + 0:                                                            \
-        if constexpr ((T) < RB) run_pair<(T), (C), !kStraight[C], RB>(ops, len, tid, base, v);      \
-        break;                                                                                     \
-    case (((T) + 1) * 4 + (C)) * 2 + 1:                                                            \
-        if constexpr ((T) < RB) run_pair<(T), (C), true, RB>(ops, len, tid, base, v);               \
-        break;
-#define QSB_CASES(T) QSB_CASE(T, 0) QSB_CASE(T, 1) QSB_CASE(T, 2) QSB_CASE(T, 3)
-        QSB_CASES(-1)
-        QSB_CASES(0)
-        QSB_CASES(1)
-        QSB_CASES(2)
-        QSB_CASES(3)
-#undef QSB_CASES
-#undef QSB_CASE
-#define QSB_PH(R)                                                                       \
-    case kPhaseVariant + (R) * 2 + 0:                                                    \
-        if constexpr ((R) < (1 << RB)) run_phase<(R), false, RB>(ops, len, tid, base, v); \
-        break;                                                                           \
-    case kPhaseVariant + (R) * 2 + 1:                                                    \
-        if constexpr ((R) < (1 << RB)) run_phase<(R), true, RB>(ops, len, tid, base, v);  \
-        break;
-        QSB_PH(0) QSB_PH(1) QSB_PH(2) QSB_PH(3) QSB_PH(4) QSB_PH(5) QSB_PH(6) QSB_PH(7)
-        QSB_PH(8) QSB_PH(9) QSB_PH(10) QSB_PH(11) QSB_PH(12) QSB_PH(13) QSB_PH(14) QSB_PH(15)
-#undef QSB_PH
-        default: break;
-    }
-}
-
-__device__ __forceinline__ uint64_t tile_base(uint64_t t, const FParams &p) {
-    uint64_t r = 0;
-    for (int i = 0; i < p.nruns; ++i)
-        r |= ((t >> p.runs[i].src) & ((1ull << p.runs[i].len) - 1ull)) << p.runs[i].dst;
-    return r;
-}
-
-__device__ __forceinline__ uint32_t padded(uint32_t f) { return f + (f >> 5); }
-
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <int K, int RB>
-__global__ void __maxnreg__(RB == 4 ? 168 : 96)
-    k_fused(float4 *__restrict__ amps, const __grid_constant__ FParams p) {
-    constexpr int kCompute = 1 << (K - 1 - RB);   // compute threads
-    constexpr int kSegs = 1 << (K - kLow);        // 512-B segments per tile
-    constexpr int kBufF4 = kSegs * 33;            // padded float4 per buffer
-    extern __shared__ __align__(128) float4 smem[];
-    float4 *buf0 = smem;
-    FOp *sops = (FOp *)(smem + kNB * kBufF4);
-    __shared__ uint64_t full[kNB], done[kNB];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        for (int b = 0; b < kNB; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&done[b], 1);
-        }
-        fence_mbar_init();
-    }
-    {  // stage the op table in shared memory
-        const int4 *src = (const int4 *)p.ops;
-        int4 *dst = (int4 *)sops;
-        const int words = p.nops * (int)(sizeof(FOp) / 16);
-        for (int i = tid; i < words; i += blockDim.x) dst[i] = src[i];
-    }
-    __syncthreads();
-
-    if (warp == kCompute / 32) {
-        // ---------------- producer warp: TMA loads and stores ----------------
-        const CUtensorMap *map = &p.tmap;
-        constexpr int kCopyF4 = 8 * 33;  // one 5-D box: 8 padded segments
-        constexpr uint32_t kBoxBytes = 8u * 66u * 8u;
-        uint64_t pending[kNB];
-        int i = 0;
-        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
-            const int b = i % kNB;
-            float4 *buf = buf0 + b * kBufF4;
-            if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
-                mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
-                const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
-                for (int c = lane; c < p.ncopies; c += 32) {
-                    uint32_t row = row0;
-                    for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
-                    tma_store_5d(map, (int)row, buf + c * kCopyF4);
-                }
-                bulk_commit();
-                bulk_wait_read0();  // buffer b may be overwritten
-                __syncwarp();
-            }
-            const uint64_t base = tile_base(t, p);
-            pending[b] = base;
-            if (lane == 0) mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
-            __syncwarp();
-            const uint32_t row0 = (uint32_t)(base >> kLow);
-            for (int c = lane; c < p.ncopies; c += 32) {
-                uint32_t row = row0;
-                for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
-                tma_load_5d(buf + c * kCopyF4, map, (int)row, &full[b]);
-            }
-        }
-        // drain the last (up to) kNB tiles
-        for (int k = (i >= kNB ? i - kNB : 0); k < i; ++k) {
-            const int b = k % kNB;
-            mbar_wait(&done[b], (k / kNB) & 1);
-            const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
-            for (int c = lane; c < p.ncopies; c += 32) {
-                uint32_t row = row0;
-                for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
-                tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4);
-            }
-            bulk_commit();
-        }
-        bulk_wait0();
-        return;
-    }
-
-    // -------------------- compute warps: register stages --------------------
-    int i = 0;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
-        const int b = i % kNB;
-        float4 *tile = buf0 + b * kBufF4;
-        const uint64_t base = tile_base(t, p);
-        mbar_wait(&full[b], (i / kNB) & 1);
-        for (int s = 0; s < p.nstages; ++s) {
-            const FStage &st = p.stages[s];
-            uint32_t fb = 0;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) fb |= (uint32_t)((lane >> q) & 1) << st.lf[q];
-            for (int q = 0; q < p.nwbits; ++q) fb |= (uint32_t)((warp >> q) & 1) << st.wf[q];
-            const uint32_t pb = padded(fb);
-            uint32_t rs[RB];
-#pragma unroll
-            for (int r = 0; r < RB; ++r) rs[r] = padded(1u << st.rf[r]);
-            float4 v[1 << RB];
-#pragma unroll
-            for (int j = 0; j < (1 << RB); ++j) {
-                uint32_t a = pb;
-#pragma unroll
-                for (int r = 0; r < RB; ++r)
-                    if (j & (1 << r)) a += rs[r];
-                v[j] = tile[a];
-            }
-            if (!p.dry) {
-                for (int o = st.op_begin; o < st.op_end;) {
-                    const int variant = sops[o].variant, len = sops[o].run;
-                    apply_run<RB>(variant, sops + o, len, (uint32_t)tid, base, v);
-                    o += len;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < (1 << RB); ++j) {
-                uint32_t a = pb;
-#pragma unroll
-                for (int r = 0; r < RB; ++r)
-                    if (j & (1 << r)) a += rs[r];
-                tile[a] = v[j];
-            }
-            if (s + 1 < p.nstages) named_sync(1, kCompute);
-        }
-        fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
-        named_sync(1, kCompute);
-        if (tid == 0) mbar_arrive(&done[b]);
-    }
-}
 
 template <int K, int RB>
 int launch_fused_k(qs_state *s, const FParams &p) {
     const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
+    {  // run-time compiled straight-line program for this pass (jit.cu)
+        uint64_t g = (uint64_t)s->num_sms;
+        if (g > p.ntiles) g = p.ntiles;
+        const int rc = jit_launch(s, p, K, RB, bufs + (size_t)p.nops * sizeof(FOp), (unsigned)g,
+                                  (1u << (K - 1 - RB)) + 32u);
+        if (rc < 0) return -rc;
+        if (rc == 1) return QS_OK;
+    }
     const size_t smem = bufs + (size_t)p.nops * sizeof(FOp);
     static int configured = -1;
     if (configured < (int)smem) {
@@ -571,45 +169,11 @@ int gate_class(const float m[8]) {
 // Register layouts (f = local bit - 1; f has K-1 bits; RB register bits).
 // An LDS/STS.128 phase serves 8 lanes; with the padded address f + (f >> 5)
 // those 8 lanes hit 8 distinct bank quads iff lanes 0..2 vary f0..f2 (same
-// padded row) or f5..f7 (distinct padding offsets).
-//   LOW : regs f0..f(RB-1), lanes (f5, f6, f7, then the two lowest free bits),
-//         warps = the remaining bits
-//   HIGH: regs = RB chosen f-bits >= RB, lanes (f0, f1, f2, then the two
-//         lowest free bits), warps = the remaining bits
-void fill_lanes_warps(FStage &st, int K, int RB, const int *first3) {
-    bool used[32] = {false};
-    for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
-    for (int i = 0; i < 3; ++i) {
-        st.lf[i] = first3[i];
-        used[first3[i]] = true;
-    }
-    int nl = 3, nw = 0;
-    for (int f = 0; f < K - 1; ++f) {
-        if (used[f]) continue;
-        if (nl < 5)
-            st.lf[nl++] = f;
-        else
-            st.wf[nw++] = f;
-    }
-}
-
-FStage make_low_stage(int K, int RB) {
-    FStage st;
-    std::memset(&st, 0, sizeof st);
-    for (int r = 0; r < RB; ++r) st.rf[r] = r;
-    const int first3[3] = {5, 6, 7};
-    fill_lanes_warps(st, K, RB, first3);
-    return st;
-}
-
-FStage make_high_stage(int K, int RB, const std::vector<int> &rbits_f) {
-    FStage st;
-    std::memset(&st, 0, sizeof st);
-    for (int r = 0; r < RB; ++r) st.rf[r] = rbits_f[r];
-    const int first3[3] = {0, 1, 2};
-    fill_lanes_warps(st, K, RB, first3);
-    return st;
-}
+// padded row) or f5..f7 (distinct padding offsets); lanes 3 and 4 are free.
+//   LOW : regs f0..f(RB-1), lanes (f5, f6, f7, two free bits), warps = the rest
+//   HIGH: regs = RB chosen f-bits >= RB, lanes (f0, f1, f2, two free bits),
+//         warps = the rest
+// (run_fused picks the two free lane bits per stage.)
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
 // link dependency, so the library still loads on a GPU-less build host).
@@ -697,6 +261,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     }
     p.nwbits = K - 6 - RB;
     p.ntiles = 1ull << (n - K);
+    p.one = 1.0f;
     {
         const char *d = std::getenv("QSB_FUSED_DRY");
         p.dry = d && *d == '1';
@@ -738,33 +303,121 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         *fbit = lb - 1;
         return 2;
     };
+    // (1) stage layouts and op ranges: greedy over the PAIR ops in circuit
+    // order; the layout follows the first op that constrains it.
+    struct Plan {
+        int kind;               // 1 = LOW, 2 = HIGH
+        std::vector<int> rb;    // HIGH: register f-bits
+        int begin, end, first;  // op range; first constraining op
+    };
+    std::vector<Plan> plans;
+    {
+        int i = 0;
+        while (i < nops) {
+            Plan pl;
+            pl.kind = 1;
+            pl.begin = i;
+            pl.first = nops;
+            for (int j = i; j < nops; ++j) {
+                int f = -1, nd = need_of(ops[j], &f);
+                if (nd) {
+                    pl.kind = nd;
+                    pl.first = j;
+                    break;
+                }
+            }
+            if (pl.kind == 2) {
+                for (int j = i; j < nops && (int)pl.rb.size() < RB; ++j) {
+                    int f = -1, nd = need_of(ops[j], &f);
+                    if (nd == 1) break;
+                    if (nd == 2 && std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
+                }
+                for (int f = RB; f < K - 1 && (int)pl.rb.size() < RB; ++f)
+                    if (std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
+                std::sort(pl.rb.begin(), pl.rb.end());
+            } else {
+                for (int r = 0; r < RB; ++r) pl.rb.push_back(r);
+            }
+            for (; i < nops; ++i) {
+                int f = -1, nd = need_of(ops[i], &f);
+                if (nd == 1 && pl.kind != 1) break;
+                if (nd == 2 && (pl.kind != 2 || std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end())) break;
+            }
+            pl.end = i;
+            plans.push_back(pl);
+        }
+    }
+    // local f-bits an op tests (controls / phase bits; the half bit is free)
+    auto test_fbits = [&](const qs_op &op) -> uint32_t {
+        uint64_t need = op.ctrl_mask;
+        if (op.kind == QS_OP_PHASE) need |= 1ull << op.target;
+        uint32_t fb = 0;
+        for (int q = 0; q < n; ++q)
+            if (((need >> q) & 1ull) && local_of[q] > 0) fb |= 1u << (local_of[q] - 1);
+        return fb;
+    };
+    auto in_regs = [&](const Plan &pl, uint32_t fb) -> int {
+        int c = 0;
+        for (int f : pl.rb) c += (fb >> f) & 1u;
+        return c;
+    };
+    // (2) the unconstrained ops (phases, half-bit targets) between the last
+    // pair op of stage s-1 and the first of stage s may run in either stage
+    // (order is kept).  Move the trailing run to stage s when its bits are
+    // register bits there more often: a register-bit test is free (compile-
+    // time register mask), a lane-bit test costs a divergent full body.
+    for (size_t s = 1; s < plans.size(); ++s) {
+        Plan &a = plans[s - 1], &b = plans[s];
+        int split = b.begin;
+        while (split > a.begin && split - 1 >= a.first) {
+            int f = -1;
+            if (need_of(ops[split - 1], &f)) break;
+            --split;
+        }
+        if (split < a.first) split = a.first + 1;
+        if (split >= b.begin) continue;
+        int score_a = 0, score_b = 0;
+        for (int j = split; j < b.begin; ++j) {
+            const uint32_t fb = test_fbits(ops[j]);
+            score_a += in_regs(a, fb);
+            score_b += in_regs(b, fb);
+        }
+        if (score_b > score_a) {
+            a.end = split;
+            b.begin = split;
+        }
+    }
+    // (3) per stage: lanes 3 and 4 take the free f-bits its ops test least
+    // (whole warps skip a failed warp-bit test; lanes diverge)
     std::vector<FStage> stages;
     std::vector<FOp> fops;
-    int i = 0;
-    while (i < nops) {
-        // the layout follows the first op that constrains it
-        int kind = 1;
-        for (int j = i; j < nops; ++j) {
-            int f = -1, nd = need_of(ops[j], &f);
-            if (nd) {
-                kind = nd;
-                break;
-            }
+    for (const Plan &pl : plans) {
+        int uses[32] = {0};
+        for (int j = pl.begin; j < pl.end; ++j) {
+            const uint32_t fb = test_fbits(ops[j]);
+            for (int f = 0; f < K - 1; ++f) uses[f] += (fb >> f) & 1u;
         }
         FStage st;
-        if (kind == 1) {
-            st = make_low_stage(K, RB);
-        } else {
-            std::vector<int> rb;
-            for (int j = i; j < nops && (int)rb.size() < RB; ++j) {
-                int f = -1, nd = need_of(ops[j], &f);
-                if (nd == 1) break;
-                if (nd == 2 && std::find(rb.begin(), rb.end(), f) == rb.end()) rb.push_back(f);
+        std::memset(&st, 0, sizeof st);
+        for (int r = 0; r < RB; ++r) st.rf[r] = pl.rb[r];
+        {
+            const int low3[3] = {5, 6, 7}, high3[3] = {0, 1, 2};
+            const int *first3 = pl.kind == 1 ? low3 : high3;
+            bool used[32] = {false};
+            for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
+            for (int l = 0; l < 3; ++l) {
+                st.lf[l] = first3[l];
+                used[first3[l]] = true;
             }
-            for (int f = RB; f < K - 1 && (int)rb.size() < RB; ++f)
-                if (std::find(rb.begin(), rb.end(), f) == rb.end()) rb.push_back(f);
-            std::sort(rb.begin(), rb.end());
-            st = make_high_stage(K, RB, rb);
+            std::vector<int> fr;
+            for (int f = 0; f < K - 1; ++f)
+                if (!used[f]) fr.push_back(f);
+            std::stable_sort(fr.begin(), fr.end(), [&](int x, int y) { return uses[x] < uses[y]; });
+            st.lf[3] = fr[0];
+            st.lf[4] = fr[1];
+            std::vector<int> wb(fr.begin() + 2, fr.end());
+            std::sort(wb.begin(), wb.end());
+            for (int w = 0; w < (int)wb.size(); ++w) st.wf[w] = wb[w];
         }
         int reg_of[kMaxK], lane_of[kMaxK], warp_of[kMaxK];
         for (int f = 0; f < kMaxK; ++f) reg_of[f] = lane_of[f] = warp_of[f] = -1;
@@ -772,11 +425,8 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         for (int l = 0; l < 5; ++l) lane_of[st.lf[l]] = l;
         for (int w = 0; w < p.nwbits; ++w) warp_of[st.wf[w]] = w;
         st.op_begin = (int)fops.size();
-        for (; i < nops; ++i) {
+        for (int i = pl.begin; i < pl.end; ++i) {
             const qs_op &op = ops[i];
-            int f = -1, nd = need_of(op, &f);
-            if (nd == 1 && kind != 1) break;
-            if (nd == 2 && (kind != 2 || reg_of[f] < 0)) break;
             FOp o;
             std::memset(&o, 0, sizeof o);
             std::memcpy(o.m, op.m, sizeof o.m);
@@ -845,6 +495,20 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
                 while (e < st.op_end && p.ops[e].variant == p.ops[o].variant) ++e;
                 p.ops[o].run = e - o;
                 o = e;
+            }
+        }
+        if (const char *dump = std::getenv("QSB_FUSED_DUMP")) {  // planner debugging
+            if (FILE *f = std::fopen(dump, "a")) {
+                std::fprintf(f, "pass K=%d RB=%d nstages=%d nops=%d\n", K, RB, p.nstages, p.nops);
+                for (int k = 0; k < p.nstages; ++k) {
+                    const FStage &st = p.stages[k];
+                    std::fprintf(f, "stage %d %d %d\n", k, st.op_begin, st.op_end);
+                    for (int o = st.op_begin; o < st.op_end; ++o)
+                        std::fprintf(f, "op %d %d %u %u %u %llu\n", o, p.ops[o].variant, p.ops[o].reg_need,
+                                     p.ops[o].tid_need, p.ops[o].half_need,
+                                     (unsigned long long)p.ops[o].ext_need);
+                }
+                std::fclose(f);
             }
         }
         int rc;

@@ -1,0 +1,489 @@
+// Device side of the K5 fused tile pass (see fused.cu for the design notes).
+// Compiled twice: ahead of time into libqsb200.so (nvcc, the interpreter
+// kernel k_fused) and at run time by NVRTC as the prelude of generated
+// straight-line pass kernels (fused.cu: JIT).  Keep it NVRTC-clean: no host
+// headers under __CUDACC_RTC__.
+#pragma once
+
+#include "common.cuh"
+
+#ifdef __CUDACC_RTC__
+typedef struct __align__(64) {
+    unsigned long long opaque[16];
+} CUtensorMap;
+#else
+#include <cuda.h>
+#endif
+
+namespace qsb {
+
+constexpr int kLow = 6;      // local qubits 0..5 form one 512-B segment
+constexpr int kMaxRegBits = 4;  // RB: 2^RB float4 per thread (RB = 3 or 4)
+constexpr int kMaxK = 14;
+constexpr int kMaxWarpBits = 5;
+
+enum : int { kCplx = 0, kReal = 1, kHlike = 2, kSwap = 3 };
+
+// One op, lowered to the layout of the stage it runs in (48 bytes, staged
+// into shared memory once per CTA).
+struct __align__(16) FOp {
+    int variant;         // see kPhaseVariant
+    uint32_t reg_need;   // register-index bits that must be set (warp-uniform)
+    uint32_t tid_need;   // thread-id bits (lane | warp << 5) that must be set
+    uint32_t half_need;  // odd half only (control / phase bit on local qubit 0)
+    uint64_t ext_need;   // global qubits outside the tile that must be 1
+    float one;           // == 1.0f, loaded at run time (see rsum / csub)
+    int run;             // at a run head: number of consecutive ops with this variant
+    float m[8];
+};
+// pair variants: ((slot + 1) * 4 + class) * 2 + has_need, slot -1 = half;
+// phase variants: kPhaseVariant + reg_need * 2 + half_need
+constexpr int kPhaseVariant = 40;
+
+struct FStage {
+    int rf[kMaxRegBits];   // f-bit (f = local >> 1) of register bit r
+    int lf[5];             // f-bit of lane bit i
+    int wf[kMaxWarpBits];  // f-bit of warp bit w
+    int op_begin, op_end;
+};
+
+// Tile index -> global base: contiguous runs of non-tile qubits.
+constexpr int kMaxRuns = 16;
+struct Run {
+    int src, dst, len;
+};
+
+constexpr int kMaxOps = 320;
+constexpr int kNB = 3;  // tile buffers in the TMA ring
+constexpr int kMaxStages = 48;
+struct FParams {
+    CUtensorMap tmap;  // 64-B aligned, first member
+    int ncopies;       // TMA copies per tile (2^(K-9))
+    int crow[4];       // row-index bit of copy-index bit i
+    int n, K, nwbits, nstages, nruns, nops;
+    int dry;    // QSB_FUSED_DRY=1: move the tiles, skip the math (ring probe)
+    float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
+    uint64_t ntiles;
+    int qpos[kMaxK];  // global qubit of local bit i
+    Run runs[kMaxRuns];
+    FStage stages[kMaxStages];
+    FOp ops[kMaxOps];  // copied to shared memory once per CTA
+};
+// The whole table travels as the kernel parameter block (<= 32764 bytes since
+// CUDA 12.1), so consecutive passes need no host synchronisation.
+static_assert(sizeof(FParams) < 32000, "kernel parameter block too large");
+
+// ---- PTX wrappers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// try_wait suspends in hardware between polls; after ~2^22 failed polls (far
+// beyond any legitimate TMA latency) the kernel traps instead of hanging.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (spins > (1u << 22)) __trap();
+    }
+}
+__device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes,
+                                          uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_store(void *gdst, const void *smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(smem_src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_5d(void *smem_dst, const CUtensorMap *map, int row,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %2, %2, %2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(0), "r"(row), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, int row, const void *smem_src) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %1, %1, %1, %2}], [%3];" ::"l"(map),
+        "r"(0), "r"(row), "r"(smem_u32(smem_src))
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ---- exact pair updates per gate class ----------------------------------------
+// real entry g (g.im == 0): fma(g, v.re, -rn(0*v.im)) == rn(g*v.re) and
+// fma(g, v.im, rn(0*v.re)) == rn(g*v.im) for every nonzero result.
+// ptxas (CUDA 12.9) contracts mul.rn.f32x2 feeding add.rn.f32x2 (and even
+// fma.rn.f32x2(x, 1.0, y), which it first folds to an add) into one FFMA2,
+// which would round a sum of two products once instead of three times.  The
+// sums below are fma(x, one, y) / fma(y, -one, x) with `one` == 1.0f loaded
+// from the op table at run time, so ptxas cannot fold them: exactly
+// rn(x + y) / rn(x - y), and the products stay separately rounded.  The GPU
+// parity tests compare every gate class bit for bit against the oracle.
+__device__ __forceinline__ float2 rmul(float g, float2 v) { return f2mul(make_float2(g, g), v); }
+__device__ __forceinline__ float2 rsum(float2 x, float2 y, float one) {
+    return f2fma(x, make_float2(one, one), y);
+}
+__device__ __forceinline__ float2 csub(float2 x, float2 y, float one) {
+    return f2fma(y, make_float2(-one, -one), x);
+}
+
+template <int CLS>
+__device__ __forceinline__ void pair_cls(const float *m, float one, float2 &va, float2 &vb) {
+    if (CLS == kCplx) {
+        float2 na = cadd(cmul(make_float2(m[0], m[1]), va), cmul(make_float2(m[2], m[3]), vb));
+        float2 nb = cadd(cmul(make_float2(m[6], m[7]), vb), cmul(make_float2(m[4], m[5]), va));
+        va = na;
+        vb = nb;
+    } else if (CLS == kReal) {
+        float2 na = rsum(rmul(m[0], va), rmul(m[2], vb), one);
+        float2 nb = rsum(rmul(m[6], vb), rmul(m[4], va), one);
+        va = na;
+        vb = nb;
+    } else if (CLS == kHlike) {
+        // c == a, d == -b: c*va == a*va and d*vb == -(b*vb) exactly
+        float2 p = rmul(m[0], va), q = rmul(m[2], vb);
+        va = rsum(p, q, one);
+        vb = csub(p, q, one);
+    } else {  // X: a == d == 0, b == c == 1 -> values swap
+        float2 t = va;
+        va = vb;
+        vb = t;
+    }
+}
+
+__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float4 mk4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+
+// T = register bit of the target (-1: the float4 half, local qubit 0);
+// NEED: the op has a control / phase bit on the register index or the half
+// (per-j warp-uniform tests); !NEED is the straight-line common case.
+template <int T, int CLS, bool NEED, int RB>
+__device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[1 << RB]) {
+    const uint32_t need = NEED ? op.reg_need : 0u;
+    const bool odd_only = NEED && op.half_need != 0;
+    const float one = op.one;
+    float m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = (CLS == kSwap) ? 0.f : op.m[i];
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (T >= 0 && (j & (1 << T))) continue;
+        if (NEED && (j & need) != need) continue;  // warp-uniform
+        if (T < 0) {
+            float2 a = lo2(v[j]), b = hi2(v[j]);
+            pair_cls<CLS>(m, one, a, b);
+            v[j] = mk4(a, b);
+        } else {
+            const int k = j | (1 << (T < 0 ? 0 : T));
+            float2 a0 = lo2(v[j]), a1 = hi2(v[j]), b0 = lo2(v[k]), b1 = hi2(v[k]);
+            if (!odd_only) pair_cls<CLS>(m, one, a0, b0);
+            pair_cls<CLS>(m, one, a1, b1);
+            v[j] = mk4(a0, a1);
+            v[k] = mk4(b0, b1);
+        }
+    }
+}
+
+// Diagonal op: multiply the registers whose index has every bit of RNEED set
+// (compile-time pattern) by d; ODD: only the odd half (phase bit on local 0).
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[1 << RB]) {
+    const float2 d = make_float2(op.m[6], op.m[7]);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if ((j & RNEED) != RNEED) continue;
+        float2 a = lo2(v[j]), b = hi2(v[j]);
+        if (!ODD) a = cmul(d, a);
+        b = cmul(d, b);
+        v[j] = mk4(a, b);
+    }
+}
+
+// Classes with a straight-line (no per-j test) body; the complex and swap
+// bodies keep the per-j branch, which bounds ptxas' register demand there.
+__device__ constexpr bool kStraight[4] = {false, true, true, false};
+
+__device__ __forceinline__ bool op_ok(const FOp &op, uint32_t tid, uint64_t base) {
+    return (tid & op.tid_need) == op.tid_need && (base & op.ext_need) == op.ext_need;
+}
+
+template <int T, int C, bool NEED, int RB>
+__device__ __forceinline__ void run_pair(const FOp *ops, int len, uint32_t tid, uint64_t base,
+                                         float4 (&v)[1 << RB]) {
+    for (int k = 0; k < len; ++k)
+        if (op_ok(ops[k], tid, base)) apply_pair<T, C, NEED, RB>(ops[k], v);
+}
+
+template <int R, bool ODD, int RB>
+__device__ __forceinline__ void run_phase(const FOp *ops, int len, uint32_t tid, uint64_t base,
+                                          float4 (&v)[1 << RB]) {
+    for (int k = 0; k < len; ++k)
+        if (op_ok(ops[k], tid, base)) apply_phase<R, ODD, RB>(ops[k], v);
+}
+
+// One dispatch per RUN of consecutive ops with the same variant (the host
+// sets FOp::run at each run head): nvcc lowers the switch to a compare tree,
+// so QFT-style streams of same-pattern phase ops pay for it once per run.
+template <int RB>
+__device__ __forceinline__ void apply_run(int variant, const FOp *ops, int len, uint32_t tid,
+                                          uint64_t base, float4 (&v)[1 << RB]) {
+    switch (variant) {
+#define QSB_CASE(T, C)                                                                             \
+    case (((T) + 1) * 4 + (C)) * 2 + 0:                                                            \
+        if constexpr ((T) < RB) run_pair<(T), (C), !kStraight[C], RB>(ops, len, tid, base, v);      \
+        break;                                                                                     \
+    case (((T) + 1) * 4 + (C)) * 2 + 1:                                                            \
+        if constexpr ((T) < RB) run_pair<(T), (C), true, RB>(ops, len, tid, base, v);               \
+        break;
+#define QSB_CASES(T) QSB_CASE(T, 0) QSB_CASE(T, 1) QSB_CASE(T, 2) QSB_CASE(T, 3)
+        QSB_CASES(-1)
+        QSB_CASES(0)
+        QSB_CASES(1)
+        QSB_CASES(2)
+        QSB_CASES(3)
+#undef QSB_CASES
+#undef QSB_CASE
+#define QSB_PH(R)                                                                       \
+    case kPhaseVariant + (R) * 2 + 0:                                                    \
+        if constexpr ((R) < (1 << RB)) run_phase<(R), false, RB>(ops, len, tid, base, v); \
+        break;                                                                           \
+    case kPhaseVariant + (R) * 2 + 1:                                                    \
+        if constexpr ((R) < (1 << RB)) run_phase<(R), true, RB>(ops, len, tid, base, v);  \
+        break;
+        QSB_PH(0) QSB_PH(1) QSB_PH(2) QSB_PH(3) QSB_PH(4) QSB_PH(5) QSB_PH(6) QSB_PH(7)
+        QSB_PH(8) QSB_PH(9) QSB_PH(10) QSB_PH(11) QSB_PH(12) QSB_PH(13) QSB_PH(14) QSB_PH(15)
+#undef QSB_PH
+        default: break;
+    }
+}
+
+// Ahead-of-time program: walks the op table staged in shared memory.
+struct Interp {
+    template <int RB>
+    static __device__ __forceinline__ void run(int, const FStage &st, const FOp *sops, uint32_t tid,
+                                               uint64_t base, float, float4 (&v)[1 << RB]) {
+        for (int o = st.op_begin; o < st.op_end;) {
+            const int variant = sops[o].variant, len = sops[o].run;
+            apply_run<RB>(variant, sops + o, len, tid, base, v);
+            o += len;
+        }
+    }
+};
+
+// Compile-time forms for generated programs: target slot T (-1 = half),
+// class, register-bit test RNEED and odd-half-only are template constants,
+// the gate entries literals of the generated source.
+template <int T, int CLS, int RNEED, bool ODD_ONLY, int RB>
+__device__ __forceinline__ void pair_ct(const float (&m)[8], float one, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (T >= 0 && (j & (1 << T))) continue;
+        if ((j & RNEED) != RNEED) continue;
+        if (T < 0) {
+            float2 a = lo2(v[j]), b = hi2(v[j]);
+            pair_cls<CLS>(m, one, a, b);
+            v[j] = mk4(a, b);
+        } else {
+            const int k = j | (1 << (T < 0 ? 0 : T));
+            float2 a0 = lo2(v[j]), a1 = hi2(v[j]), b0 = lo2(v[k]), b1 = hi2(v[k]);
+            if (!ODD_ONLY) pair_cls<CLS>(m, one, a0, b0);
+            pair_cls<CLS>(m, one, a1, b1);
+            v[j] = mk4(a0, a1);
+            v[k] = mk4(b0, b1);
+        }
+    }
+}
+
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void phase_ct(float2 d, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if ((j & RNEED) != RNEED) continue;
+        float2 a = lo2(v[j]), b = hi2(v[j]);
+        if (!ODD) a = cmul(d, a);
+        b = cmul(d, b);
+        v[j] = mk4(a, b);
+    }
+}
+
+__device__ __forceinline__ uint64_t tile_base(uint64_t t, const FParams &p) {
+    uint64_t r = 0;
+    for (int i = 0; i < p.nruns; ++i)
+        r |= ((t >> p.runs[i].src) & ((1ull << p.runs[i].len) - 1ull)) << p.runs[i].dst;
+    return r;
+}
+
+__device__ __forceinline__ uint32_t padded(uint32_t f) { return f + (f >> 5); }
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// The kernel body, shared by the ahead-of-time interpreter kernel (Prog =
+// Interp: op table in shared memory, one dispatch per run of ops) and the
+// run-time compiled pass kernels (Prog = a generated straight-line program,
+// fused.cu: JIT).  Everything but the op application is identical, so both
+// give the same bits.
+template <int K, int RB, class Prog>
+__device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FParams &p) {
+    constexpr int kCompute = 1 << (K - 1 - RB);   // compute threads
+    constexpr int kSegs = 1 << (K - kLow);        // 512-B segments per tile
+    constexpr int kBufF4 = kSegs * 33;            // padded float4 per buffer
+    extern __shared__ __align__(128) float4 smem[];
+    float4 *buf0 = smem;
+    FOp *sops = (FOp *)(smem + kNB * kBufF4);
+    __shared__ uint64_t full[kNB], done[kNB];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int b = 0; b < kNB; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&done[b], 1);
+        }
+        fence_mbar_init();
+    }
+    {  // stage the op table in shared memory
+        const int4 *src = (const int4 *)p.ops;
+        int4 *dst = (int4 *)sops;
+        const int words = p.nops * (int)(sizeof(FOp) / 16);
+        for (int i = tid; i < words; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+
+    if (warp == kCompute / 32) {
+        // ---------------- producer warp: TMA loads and stores ----------------
+        const CUtensorMap *map = &p.tmap;
+        constexpr int kCopyF4 = 8 * 33;  // one 5-D box: 8 padded segments
+        constexpr uint32_t kBoxBytes = 8u * 66u * 8u;
+        uint64_t pending[kNB];
+        int i = 0;
+        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+            const int b = i % kNB;
+            float4 *buf = buf0 + b * kBufF4;
+            if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
+                mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
+                const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
+                for (int c = lane; c < p.ncopies; c += 32) {
+                    uint32_t row = row0;
+                    for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
+                    tma_store_5d(map, (int)row, buf + c * kCopyF4);
+                }
+                bulk_commit();
+                bulk_wait_read0();  // buffer b may be overwritten
+                __syncwarp();
+            }
+            const uint64_t base = tile_base(t, p);
+            pending[b] = base;
+            if (lane == 0) mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
+            __syncwarp();
+            const uint32_t row0 = (uint32_t)(base >> kLow);
+            for (int c = lane; c < p.ncopies; c += 32) {
+                uint32_t row = row0;
+                for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
+                tma_load_5d(buf + c * kCopyF4, map, (int)row, &full[b]);
+            }
+        }
+        // drain the last (up to) kNB tiles
+        for (int k = (i >= kNB ? i - kNB : 0); k < i; ++k) {
+            const int b = k % kNB;
+            mbar_wait(&done[b], (k / kNB) & 1);
+            const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
+            for (int c = lane; c < p.ncopies; c += 32) {
+                uint32_t row = row0;
+                for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
+                tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4);
+            }
+            bulk_commit();
+        }
+        bulk_wait0();
+        return;
+    }
+
+    // -------------------- compute warps: register stages --------------------
+    int i = 0;
+    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+        const int b = i % kNB;
+        float4 *tile = buf0 + b * kBufF4;
+        const uint64_t base = tile_base(t, p);
+        mbar_wait(&full[b], (i / kNB) & 1);
+        for (int s = 0; s < p.nstages; ++s) {
+            const FStage &st = p.stages[s];
+            uint32_t fb = 0;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) fb |= (uint32_t)((lane >> q) & 1) << st.lf[q];
+            for (int q = 0; q < p.nwbits; ++q) fb |= (uint32_t)((warp >> q) & 1) << st.wf[q];
+            const uint32_t pb = padded(fb);
+            uint32_t rs[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) rs[r] = padded(1u << st.rf[r]);
+            float4 v[1 << RB];
+#pragma unroll
+            for (int j = 0; j < (1 << RB); ++j) {
+                uint32_t a = pb;
+#pragma unroll
+                for (int r = 0; r < RB; ++r)
+                    if (j & (1 << r)) a += rs[r];
+                v[j] = tile[a];
+            }
+            if (!p.dry) Prog::template run<RB>(s, st, sops, (uint32_t)tid, base, p.one, v);
+#pragma unroll
+            for (int j = 0; j < (1 << RB); ++j) {
+                uint32_t a = pb;
+#pragma unroll
+                for (int r = 0; r < RB; ++r)
+                    if (j & (1 << r)) a += rs[r];
+                tile[a] = v[j];
+            }
+            if (s + 1 < p.nstages) named_sync(1, kCompute);
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+        named_sync(1, kCompute);
+        if (tid == 0) mbar_arrive(&done[b]);
+    }
+}
+
+template <int K, int RB>
+__global__ void __maxnreg__(RB == 4 ? 168 : 96)
+    k_fused(float4 *__restrict__ amps, const __grid_constant__ FParams p) {
+    fused_body<K, RB, Interp>(amps, p);
+}
+
+}  // namespace qsb

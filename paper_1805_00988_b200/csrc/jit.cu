@@ -1,0 +1,307 @@
+// Run-time specialised fused-pass kernels (the K5 pass without an interpreter).
+//
+// The ahead-of-time kernel k_fused walks an op table in shared memory and
+// dispatches every run of ops through a switch over ~70 template bodies; the
+// dispatch (a compare tree plus an indirect branch, taken by every warp for
+// every op of every tile) costs several hundred cycles per op, more than the
+// op's arithmetic.  A pass's op sequence is identical for all 2^(n-K) tiles,
+// so this file turns the planned pass (FParams: stages, lowered ops) into a
+// straight-line program — every op a call of pair_ct / phase_ct with its
+// slot, class, register mask and gate entries as compile-time constants and
+// its thread / tile predicate as a literal mask test — compiles it with NVRTC
+// for sm_100a, and launches it with the same kernel body (fused_body), grid,
+// ring and register layouts as k_fused.  Same layouts, same per-pair
+// arithmetic, same `one` opaque to ptxas: the results are the interpreter's
+// bit for bit (tests run every fused case both ways).
+//
+// Policy (QSB_FUSED_JIT): 0 = off; 1 (default) = compile a pass program the
+// second time it is launched (repeated circuits, benchmarks), interpret it
+// the first time; 2 = always.  Compiled programs are cached per device for
+// the life of the process.  NVRTC is loaded with dlopen; without it the
+// interpreter kernel runs (same device code path, no CPU fallback).
+
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "fused_dev.cuh"
+#include "internal.h"
+
+namespace qsb {
+
+namespace {
+
+#include "_jit_headers.inc"  // kJitCommon, kJitFusedDev: the two headers as text (build.py)
+
+// ---- NVRTC, loaded lazily ---------------------------------------------------
+typedef int nvrtcResult_t;
+typedef struct _nvrtcProgram *nvrtcProgram_t;
+struct Nvrtc {
+    bool ok = false;
+    nvrtcResult_t (*create)(nvrtcProgram_t *, const char *, const char *, int, const char *const *,
+                            const char *const *);
+    nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char *const *);
+    nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t *);
+    nvrtcResult_t (*log)(nvrtcProgram_t, char *);
+    nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t *);
+    nvrtcResult_t (*cubin)(nvrtcProgram_t, char *);
+    nvrtcResult_t (*destroy)(nvrtcProgram_t *);
+};
+
+const Nvrtc &nvrtc() {
+    static Nvrtc n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    const char *names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+    void *h = nullptr;
+    for (const char *nm : names)
+        if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+    if (!h) return n;
+    n.create = (decltype(n.create))dlsym(h, "nvrtcCreateProgram");
+    n.compile = (decltype(n.compile))dlsym(h, "nvrtcCompileProgram");
+    n.log_size = (decltype(n.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+    n.log = (decltype(n.log))dlsym(h, "nvrtcGetProgramLog");
+    n.cubin_size = (decltype(n.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+    n.cubin = (decltype(n.cubin))dlsym(h, "nvrtcGetCUBIN");
+    n.destroy = (decltype(n.destroy))dlsym(h, "nvrtcDestroyProgram");
+    n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.destroy;
+    return n;
+}
+
+// ---- driver entry points ------------------------------------------------------
+struct Driver {
+    bool ok = false;
+    PFN_cuModuleLoadData_v2000 load;
+    PFN_cuModuleGetFunction_v2000 get;
+    PFN_cuFuncSetAttribute_v9000 set_attr;
+    PFN_cuLaunchKernel_v4000 launch;
+};
+
+const Driver &driver() {
+    static Driver d;
+    static bool tried = false;
+    if (tried) return d;
+    tried = true;
+    auto sym = [](const char *name) -> void * {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return fn;
+    };
+    d.load = (PFN_cuModuleLoadData_v2000)sym("cuModuleLoadData");
+    d.get = (PFN_cuModuleGetFunction_v2000)sym("cuModuleGetFunction");
+    d.set_attr = (PFN_cuFuncSetAttribute_v9000)sym("cuFuncSetAttribute");
+    d.launch = (PFN_cuLaunchKernel_v4000)sym("cuLaunchKernel");
+    d.ok = d.load && d.get && d.set_attr && d.launch;
+    return d;
+}
+
+// ---- code generation -----------------------------------------------------------
+constexpr int kJitLoopRun = 3;      // runs at least this long stay loops ...
+constexpr int kJitLoopMinRegs = 8;  // ... when each op touches at least 8 float4 registers
+void hexf(std::string &out, float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "__int_as_float(0x%08x)", b);
+    out += buf;
+}
+
+std::string generate(const FParams &p, int K, int RB) {
+    std::string src;
+    src.reserve(8192 + (size_t)p.nops * 200);
+    src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
+           "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *ops, uint32_t tid,\n"
+           "      uint64_t base, float one, float4 (&v)[1 << RB]) {\n    switch (s) {\n";
+    char buf[256];
+    for (int k = 0; k < p.nstages; ++k) {
+        const FStage &st = p.stages[k];
+        std::snprintf(buf, sizeof buf, "    case %d: {\n", k);
+        src += buf;
+        for (int o = st.op_begin; o < st.op_end;) {
+            const FOp &op = p.ops[o];
+            // a long run of one variant (the QFT's controlled phases on
+            // non-register bits) stays a loop over the shared-memory op
+            // table: straight-line copies of a 32-amplitude body per op would
+            // overflow the instruction cache
+            int e = o + 1;
+            while (e < st.op_end && p.ops[e].variant == op.variant && p.ops[e].reg_need == op.reg_need &&
+                   p.ops[e].half_need == op.half_need)
+                ++e;
+            // registers an op of this run touches (of 2^RB float4 per thread)
+            const int touched = (1 << RB) >> __builtin_popcount(op.reg_need);
+            if (e - o >= kJitLoopRun && touched >= kJitLoopMinRegs) {
+                if (op.variant >= kPhaseVariant) {
+                    const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
+                    std::snprintf(buf, sizeof buf, "      run_phase<%d, %s, RB>(ops + %d, %d, tid, base, v);\n", R,
+                                  odd ? "true" : "false", o, e - o);
+                } else {
+                    const int cls = (op.variant / 2) % 4, slot = (op.variant / 2) / 4 - 1;
+                    const bool need = (op.variant % 2) || cls == kCplx || cls == kSwap;
+                    std::snprintf(buf, sizeof buf, "      run_pair<%d, %d, %s, RB>(ops + %d, %d, tid, base, v);\n",
+                                  slot, cls, need ? "true" : "false", o, e - o);
+                }
+                src += buf;
+                o = e;
+                continue;
+            }
+            for (; o < e; ++o) {
+                const FOp &op = p.ops[o];
+                std::string test;
+                if (op.tid_need) {
+                    std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need, op.tid_need);
+                    test += buf;
+                }
+                if (op.ext_need) {
+                    std::snprintf(buf, sizeof buf, "%s(base & 0x%llxull) == 0x%llxull", test.empty() ? "" : " && ",
+                                  (unsigned long long)op.ext_need, (unsigned long long)op.ext_need);
+                    test += buf;
+                }
+                src += test.empty() ? "      {" : "      if (" + test + ") {";
+                if (op.variant >= kPhaseVariant) {
+                    const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
+                    std::snprintf(buf, sizeof buf, " phase_ct<%d, %s, RB>(make_float2(", R, odd ? "true" : "false");
+                    src += buf;
+                    hexf(src, op.m[6]);
+                    src += ", ";
+                    hexf(src, op.m[7]);
+                    src += "), v); }\n";
+                } else {
+                    const int cls = (op.variant / 2) % 4, slot = (op.variant / 2) / 4 - 1;
+                    src += " const float m[8] = {";
+                    for (int i = 0; i < 8; ++i) {
+                        if (i) src += ", ";
+                        hexf(src, op.m[i]);
+                    }
+                    std::snprintf(buf, sizeof buf, "}; pair_ct<%d, %d, %u, %s, RB>(m, one, v); }\n", slot, cls,
+                                  op.reg_need, op.half_need ? "true" : "false");
+                    src += buf;
+                }
+            }
+        }
+        src += "    } break;\n";
+    }
+    std::snprintf(buf, sizeof buf,
+                  "    default: break;\n    }\n  }\n};\n"
+                  "extern \"C\" __global__ void __maxnreg__(%d) qsb_pass(float4 *__restrict__ amps,\n"
+                  "    const __grid_constant__ FParams p) {\n  fused_body<%d, %d, GenProg>(amps, p);\n}\n",
+                  RB == 4 ? 168 : 96, K, RB);
+    src += buf;
+    return src;
+}
+
+struct Entry {
+    int seen = 0;
+    CUfunction fn = nullptr;
+    bool failed = false;
+};
+std::mutex g_mu;
+std::map<std::pair<int, std::string>, Entry> g_cache;
+
+int jit_mode() {
+    const char *e = std::getenv("QSB_FUSED_JIT");
+    if (!e || !*e) return 1;
+    return std::atoi(e);
+}
+
+CUfunction compile(const std::string &src, int device, std::string &err) {
+    const Nvrtc &nv = nvrtc();
+    if (!nv.ok) {
+        err = "libnvrtc not available";
+        return nullptr;
+    }
+    const Driver &dr = driver();
+    if (!dr.ok) {
+        err = "driver entry points not available";
+        return nullptr;
+    }
+    const char *hdrs[2] = {kJitCommon, kJitFusedDev};
+    const char *names[2] = {"common.cuh", "fused_dev.cuh"};
+    nvrtcProgram_t prog = nullptr;
+    if (nv.create(&prog, src.c_str(), "qsb_pass.cu", 2, hdrs, names) != 0) {
+        err = "nvrtcCreateProgram failed";
+        return nullptr;
+    }
+    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DQSB_JIT=1"};
+    const int rc = nv.compile(prog, 4, opts);
+    if (rc != 0) {
+        size_t n = 0;
+        nv.log_size(prog, &n);
+        std::string log(n, '\0');
+        nv.log(prog, &log[0]);
+        err = "NVRTC compile failed: " + log.substr(0, 2000);
+        nv.destroy(&prog);
+        return nullptr;
+    }
+    size_t n = 0;
+    nv.cubin_size(prog, &n);
+    std::vector<char> cubin(n);
+    nv.cubin(prog, cubin.data());
+    nv.destroy(&prog);
+    CUmodule mod = nullptr;
+    CUfunction fn = nullptr;
+    if (dr.load(&mod, cubin.data()) != CUDA_SUCCESS || dr.get(&fn, mod, "qsb_pass") != CUDA_SUCCESS) {
+        err = "cuModuleLoadData / cuModuleGetFunction failed";
+        return nullptr;
+    }
+    (void)device;
+    return fn;
+}
+
+}  // namespace
+
+// Returns 1 if the pass was launched through a compiled program, 0 if the
+// caller should run the interpreter kernel, or a negative QS_ERR_* code.
+int jit_launch(qs_state *s, const FParams &p, int K, int RB, size_t bufs_bytes, unsigned grid,
+               unsigned block) {
+    const int mode = jit_mode();
+    if (mode <= 0) return 0;
+    std::string src = generate(p, K, RB);
+    CUfunction fn = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        Entry &e = g_cache[{s->device, src}];
+        ++e.seen;
+        if (e.failed || (mode == 1 && e.seen < 2 && !e.fn)) return 0;
+        if (!e.fn) {
+            std::string err;
+            e.fn = compile(src, s->device, err);
+            if (!e.fn) {
+                e.failed = true;
+                if (std::getenv("QSB_FUSED_JIT_VERBOSE")) std::fprintf(stderr, "qsb jit: %s\n", err.c_str());
+                return 0;
+            }
+            if (driver().set_attr(e.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)bufs_bytes) !=
+                CUDA_SUCCESS) {
+                e.failed = true;
+                e.fn = nullptr;
+                return 0;
+            }
+        }
+        fn = e.fn;
+    }
+    float4 *amps = (float4 *)s->amps;
+    void *args[2] = {(void *)&amps, (void *)&p};
+    if (driver().launch(fn, grid, 1, 1, block, 1, 1, (unsigned)bufs_bytes, (CUstream)s->stream, args,
+                        nullptr) != CUDA_SUCCESS)
+        return -set_error(QS_ERR_CUDA, "cuLaunchKernel of a compiled pass failed");
+    return 1;
+}
+
+// Test / tooling hook: the generated source of the next pass (QSB_FUSED_JIT_DUMP).
+std::string jit_source(const FParams &p, int K, int RB) { return generate(p, K, RB); }
+
+}  // namespace qsb

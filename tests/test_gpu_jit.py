@@ -1,0 +1,138 @@
+"""Run-time compiled fused-pass programs (csrc/jit.cu) against the interpreter
+kernel and the oracle.
+
+QSB_FUSED_JIT=2 compiles every pass with NVRTC, 0 runs the ahead-of-time
+interpreter; 1 (the default) interprets a pass the first time and compiles it
+when it is launched again.  All three must give the same bits.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from contextlib import contextmanager
+
+import numpy as np
+import pytest
+
+from golden_util import same_values
+from oracle import c as oc
+from paper_1805_00988_b200 import (
+    State,
+    build_hadamard_layer,
+    build_qft,
+    execute,
+    layered_random_circuit,
+    random_circuit,
+    random_unitary_gate,
+    u1,
+)
+from paper_1805_00988_b200.circuits import Apply, Circuit, ControlledApply, ControlledControlledApply
+from paper_1805_00988_b200.gates import FIXED_GATES
+
+pytestmark = pytest.mark.gpu
+
+
+@contextmanager
+def jit(mode):
+    old = os.environ.get("QSB_FUSED_JIT")
+    os.environ["QSB_FUSED_JIT"] = str(mode)
+    try:
+        yield
+    finally:
+        if old is None:
+            os.environ.pop("QSB_FUSED_JIT", None)
+        else:
+            os.environ["QSB_FUSED_JIT"] = old
+
+
+def rand_amps(n, rng):
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return (v / np.linalg.norm(v)).astype(np.complex64)
+
+
+def run(circ, a0, mode, K=None, rb="4"):
+    old = os.environ.get("QSB_FUSED_RB")
+    os.environ["QSB_FUSED_RB"] = rb
+    try:
+        with jit(mode):
+            st = State(circ.num_qubits)
+            st.set_amplitudes(a0)
+            execute(circ, st, fuse=True, tile_qubits=K)
+            return st.amplitudes()
+    finally:
+        if old is None:
+            os.environ.pop("QSB_FUSED_RB", None)
+        else:
+            os.environ["QSB_FUSED_RB"] = old
+
+
+def mixed(n, count, rng):
+    lib = list(FIXED_GATES.values())
+    ins = []
+    for _ in range(count):
+        t = int(rng.integers(n))
+        r = rng.random()
+        g = (random_unitary_gate(rng) if r < 0.3 else u1(float(rng.uniform(0, 2 * math.pi))) if r < 0.5
+             else lib[int(rng.integers(len(lib)))])
+        others = [q for q in range(n) if q != t]
+        k = rng.random()
+        if k < 0.5:
+            ins.append(Apply(g, t))
+        elif k < 0.85:
+            ins.append(ControlledApply(g, int(rng.choice(others)), t))
+        else:
+            c1, c2 = (int(x) for x in rng.choice(others, 2, replace=False))
+            ins.append(ControlledControlledApply(g, c1, c2, t))
+    return Circuit(n, tuple(ins))
+
+
+@pytest.mark.parametrize("name,n", [("hlayer", 20), ("qft", 18), ("qft", 24), ("layered", 22), ("mixed", 16)])
+def test_compiled_equals_interpreted(name, n):
+    rng = np.random.default_rng(1000 + n)
+    a0 = rand_amps(n, rng)
+    circ = {"hlayer": lambda: build_hadamard_layer(n), "qft": lambda: build_qft(n),
+            "layered": lambda: layered_random_circuit(n, 4, seed=n),
+            "mixed": lambda: mixed(n, 150, rng)}[name]()
+    interp = run(circ, a0, 0)
+    compiled = run(circ, a0, 2)
+    assert same_values(interp, compiled)
+
+
+@pytest.mark.parametrize("rb", ["3", "4"])
+@pytest.mark.parametrize("K", [10, 12, 13])
+def test_compiled_vs_oracle_all_tile_shapes(K, rb):
+    n = 15
+    rng = np.random.default_rng(77 + K)
+    a0 = rand_amps(n, rng)
+    circ = mixed(n, 90, rng)
+    ref = a0.copy()
+    for i in circ.instructions:
+        if isinstance(i, Apply):
+            oc.apply_gate(ref, i.target, i.gate)
+        elif isinstance(i, ControlledApply):
+            oc.apply_controlled_gate(ref, i.control, i.target, i.gate)
+        else:
+            oc.apply_cc_gate(ref, i.control1, i.control2, i.target, i.gate)
+    assert same_values(run(circ, a0, 2, K=K, rb=rb), ref)
+
+
+def test_second_launch_policy():
+    """Mode 1: the first launch of a pass is interpreted, the repeat compiled;
+    the register evolves identically either way."""
+    n = 19
+    rng = np.random.default_rng(5)
+    a0 = rand_amps(n, rng)
+    circ = build_qft(n)
+    with jit(1):
+        st = State(n)
+        st.set_amplitudes(a0)
+        for _ in range(3):
+            execute(circ, st, fuse=True)
+        got = st.amplitudes()
+    with jit(0):
+        ref = State(n)
+        ref.set_amplitudes(a0)
+        for _ in range(3):
+            execute(circ, ref, fuse=True)
+        assert same_values(got, ref.amplitudes())
