@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -53,22 +54,17 @@
 
 namespace qsb {
 
-int jit_launch(qs_state *s, const FParams &p, int K, int RB, size_t bufs_bytes, unsigned grid,
-               unsigned block);
+// run-time compiled pass programs (jit.cu)
+bool jit_wanted(int device, uint64_t sig);
+int jit_rb();
+void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max);
+int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned grid, unsigned block);
 
 namespace {
 
 template <int K, int RB>
 int launch_fused_k(qs_state *s, const FParams &p) {
     const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
-    {  // run-time compiled straight-line program for this pass (jit.cu)
-        uint64_t g = (uint64_t)s->num_sms;
-        if (g > p.ntiles) g = p.ntiles;
-        const int rc = jit_launch(s, p, K, RB, bufs + (size_t)p.nops * sizeof(FOp), (unsigned)g,
-                                  (1u << (K - 1 - RB)) + 32u);
-        if (rc < 0) return -rc;
-        if (rc == 1) return QS_OK;
-    }
     const size_t smem = bufs + (size_t)p.nops * sizeof(FOp);
     static int configured = -1;
     if (configured < (int)smem) {
@@ -204,61 +200,18 @@ int encode_tile_map(qs_state *s, FParams &p) {
 
 }  // namespace
 
-int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops) {
+// Plan a validated pass (tile qubit set, ops in order) for RB register bits
+// per thread: stage layouts and lowered ops, split into launch groups within
+// the op / stage limits of one kernel parameter block.
+static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops, int RB,
+                     std::vector<FParams> &groups) {
     const int n = s->num_qubits;
-    uint64_t tile_mask = 0;
-    for (int i = 0; i < ntile; ++i) {
-        if (tile_qubits[i] < 0 || tile_qubits[i] >= n)
-            return set_error(QS_ERR_INDEX, "tile qubit " + std::to_string(tile_qubits[i]) +
-                                               " out of range");
-        tile_mask |= 1ull << tile_qubits[i];
-    }
-    for (int i = 0; i < nops; ++i) {
-        const qs_op &op = ops[i];
-        if (op.kind != QS_OP_PAIR && op.kind != QS_OP_PHASE)
-            return set_error(QS_ERR_VALUE, "unknown op kind");
-        if (op.target < 0 || op.target >= n) return set_error(QS_ERR_INDEX, "op target out of range");
-        if (n < 64 && (op.ctrl_mask >> n)) return set_error(QS_ERR_INDEX, "op control out of range");
-        if ((op.ctrl_mask >> op.target) & 1ull)
-            return set_error(QS_ERR_VALUE, "control and target must differ");
-        if (op.kind == QS_OP_PAIR && !((tile_mask >> op.target) & 1ull))
-            return set_error(QS_ERR_VALUE, "pair-op target " + std::to_string(op.target) +
-                                               " is not a tile qubit");
-        if (op.kind == QS_OP_PHASE &&
-            !(op.m[0] == 1.f && op.m[1] == 0.f && op.m[2] == 0.f && op.m[3] == 0.f &&
-              op.m[4] == 0.f && op.m[5] == 0.f))
-            return set_error(QS_ERR_VALUE, "phase op needs a == 1 and b == c == 0");
-    }
     const int K = __builtin_popcountll(tile_mask);
-    const uint64_t low_mask = (1ull << kLow) - 1ull;
-    const bool kernel_ok = n >= 10 && K >= 10 && K <= 13 && (tile_mask & low_mask) == low_mask;
-    if (!kernel_ok && n <= kSmallMaxQubits) return run_small(s, ops, nops);
-    if (!kernel_ok) {
-        // Unsupported tile shape on a large register: one sweep per op — the
-        // same arithmetic, one HBM pass per op.
-        for (int i = 0; i < nops; ++i) {
-            const qs_op &op = ops[i];
-            int rc = op.kind == QS_OP_PHASE
-                         ? launch_phase(s, op.ctrl_mask | (1ull << op.target),
-                                        make_float2(op.m[6], op.m[7]))
-                         : launch_sweep(s, op.target, op.ctrl_mask, op.m);
-            if (rc) return rc;
-        }
-        return QS_OK;
-    }
-
-    FParams p;
+    std::unique_ptr<FParams> holder(new FParams);  // ~28 KB: off the stack
+    FParams &p = *holder;
     std::memset(&p, 0, sizeof p);
     p.n = n;
     p.K = K;
-    // RB = register bits per thread: 4 (16 float4 per thread) by default; 3
-    // (8 float4, twice the compute warps) with QSB_FUSED_RB=3 — measured
-    // slower on B200 because the per-op overhead scales with the thread count.
-    int RB = 4;
-    {
-        const char *r = std::getenv("QSB_FUSED_RB");
-        if (r && *r == '3') RB = 3;
-    }
     p.nwbits = K - 6 - RB;
     p.ntiles = 1ull << (n - K);
     p.one = 1.0f;
@@ -511,15 +464,108 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
                 std::fclose(f);
             }
         }
+        groups.push_back(p);
+        si = sj;
+    }
+    return QS_OK;
+}
+
+int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops) {
+    const int n = s->num_qubits;
+    uint64_t tile_mask = 0;
+    for (int i = 0; i < ntile; ++i) {
+        if (tile_qubits[i] < 0 || tile_qubits[i] >= n)
+            return set_error(QS_ERR_INDEX, "tile qubit " + std::to_string(tile_qubits[i]) +
+                                               " out of range");
+        tile_mask |= 1ull << tile_qubits[i];
+    }
+    for (int i = 0; i < nops; ++i) {
+        const qs_op &op = ops[i];
+        if (op.kind != QS_OP_PAIR && op.kind != QS_OP_PHASE)
+            return set_error(QS_ERR_VALUE, "unknown op kind");
+        if (op.target < 0 || op.target >= n) return set_error(QS_ERR_INDEX, "op target out of range");
+        if (n < 64 && (op.ctrl_mask >> n)) return set_error(QS_ERR_INDEX, "op control out of range");
+        if ((op.ctrl_mask >> op.target) & 1ull)
+            return set_error(QS_ERR_VALUE, "control and target must differ");
+        if (op.kind == QS_OP_PAIR && !((tile_mask >> op.target) & 1ull))
+            return set_error(QS_ERR_VALUE, "pair-op target " + std::to_string(op.target) +
+                                               " is not a tile qubit");
+        if (op.kind == QS_OP_PHASE &&
+            !(op.m[0] == 1.f && op.m[1] == 0.f && op.m[2] == 0.f && op.m[3] == 0.f &&
+              op.m[4] == 0.f && op.m[5] == 0.f))
+            return set_error(QS_ERR_VALUE, "phase op needs a == 1 and b == c == 0");
+    }
+    const int K = __builtin_popcountll(tile_mask);
+    const uint64_t low_mask = (1ull << kLow) - 1ull;
+    const bool kernel_ok = n >= 10 && K >= 10 && K <= 13 && (tile_mask & low_mask) == low_mask;
+    if (!kernel_ok && n <= kSmallMaxQubits) return run_small(s, ops, nops);
+    if (!kernel_ok) {
+        // Unsupported tile shape on a large register: one sweep per op — the
+        // same arithmetic, one HBM pass per op.
+        for (int i = 0; i < nops; ++i) {
+            const qs_op &op = ops[i];
+            int rc = op.kind == QS_OP_PHASE
+                         ? launch_phase(s, op.ctrl_mask | (1ull << op.target),
+                                        make_float2(op.m[6], op.m[7]))
+                         : launch_sweep(s, op.target, op.ctrl_mask, op.m);
+            if (rc) return rc;
+        }
+        return QS_OK;
+    }
+
+    // Compiled straight-line programs (jit.cu) when the policy asks for them
+    // and every launch group compiles; otherwise the interpreter kernel.
+    uint64_t sig = 1469598103934665603ull ^ tile_mask ^ ((uint64_t)n << 56);
+    {
+        const unsigned char *b = (const unsigned char *)ops;
+        for (size_t i = 0; i < (size_t)nops * sizeof(qs_op); ++i) sig = (sig ^ b[i]) * 1099511628211ull;
+    }
+    const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
+    uint64_t grid = (uint64_t)s->num_sms;
+    if (grid > (1ull << (n - K))) grid = 1ull << (n - K);
+    if (jit_wanted(s->device, sig)) {
+        const int jrb = jit_rb();
+        std::vector<FParams> groups;
+        if (plan_pass(s, tile_mask, ops, nops, jrb, groups) == QS_OK) {
+            std::vector<void *> fns;
+            for (const FParams &g : groups) {
+                void *fn = jit_get(s->device, g, K, jrb, bufs + kMaxOps * sizeof(FOp));
+                if (!fn) break;
+                fns.push_back(fn);
+            }
+            if (fns.size() == groups.size()) {
+                for (size_t i = 0; i < groups.size(); ++i) {
+                    const int rc = jit_launch(s, fns[i], groups[i], bufs + (size_t)groups[i].nops * sizeof(FOp),
+                                              (unsigned)grid, (1u << (K - 1 - jrb)) + 32u);
+                    if (rc) return rc;
+                }
+                return QS_OK;
+            }
+        }
+    }
+    // RB = register bits per thread of the interpreter: 4 (16 float4 per
+    // thread) by default; 3 (8 float4, twice the compute warps) with
+    // QSB_FUSED_RB=3 — measured slower because the per-op overhead scales
+    // with the thread count.
+    int RB = 4;
+    {
+        const char *r = std::getenv("QSB_FUSED_RB");
+        if (r && *r == '3') RB = 3;
+    }
+    std::vector<FParams> groups;
+    {
+        const int rc = plan_pass(s, tile_mask, ops, nops, RB, groups);
+        if (rc) return rc;
+    }
+    for (const FParams &g : groups) {
         int rc;
         switch (K) {
-            case 10: rc = RB == 4 ? launch_fused_k<10, 4>(s, p) : launch_fused_k<10, 3>(s, p); break;
-            case 11: rc = RB == 4 ? launch_fused_k<11, 4>(s, p) : launch_fused_k<11, 3>(s, p); break;
-            case 12: rc = RB == 4 ? launch_fused_k<12, 4>(s, p) : launch_fused_k<12, 3>(s, p); break;
-            default: rc = RB == 4 ? launch_fused_k<13, 4>(s, p) : launch_fused_k<13, 3>(s, p); break;
+            case 10: rc = RB == 4 ? launch_fused_k<10, 4>(s, g) : launch_fused_k<10, 3>(s, g); break;
+            case 11: rc = RB == 4 ? launch_fused_k<11, 4>(s, g) : launch_fused_k<11, 3>(s, g); break;
+            case 12: rc = RB == 4 ? launch_fused_k<12, 4>(s, g) : launch_fused_k<12, 3>(s, g); break;
+            default: rc = RB == 4 ? launch_fused_k<13, 4>(s, g) : launch_fused_k<13, 3>(s, g); break;
         }
         if (rc) return rc;
-        si = sj;
     }
     return QS_OK;
 }

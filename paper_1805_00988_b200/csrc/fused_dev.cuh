@@ -38,7 +38,7 @@ struct __align__(16) FOp {
 };
 // pair variants: ((slot + 1) * 4 + class) * 2 + has_need, slot -1 = half;
 // phase variants: kPhaseVariant + reg_need * 2 + half_need
-constexpr int kPhaseVariant = 40;
+constexpr int kPhaseVariant = 64;
 
 struct FStage {
     int rf[kMaxRegBits];   // f-bit (f = local >> 1) of register bit r

@@ -110,6 +110,7 @@ const Driver &driver() {
 }
 
 // ---- code generation -----------------------------------------------------------
+constexpr int kJitDefaultRB = 4;    // register bits per thread of compiled programs
 constexpr int kJitLoopRun = 3;      // runs at least this long stay loops ...
 constexpr int kJitLoopMinRegs = 8;  // ... when each op touches at least 8 float4 registers
 void hexf(std::string &out, float x) {
@@ -203,13 +204,10 @@ std::string generate(const FParams &p, int K, int RB) {
     return src;
 }
 
-struct Entry {
-    int seen = 0;
-    CUfunction fn = nullptr;
-    bool failed = false;
-};
 std::mutex g_mu;
-std::map<std::pair<int, std::string>, Entry> g_cache;
+std::map<std::pair<int, std::string>, CUfunction> g_fns;  // compiled programs
+std::map<std::pair<int, std::string>, bool> g_failed;
+std::map<std::pair<int, uint64_t>, int> g_seen;            // launches per op-list signature
 
 int jit_mode() {
     const char *e = std::getenv("QSB_FUSED_JIT");
@@ -217,7 +215,7 @@ int jit_mode() {
     return std::atoi(e);
 }
 
-CUfunction compile(const std::string &src, int device, std::string &err) {
+CUfunction compile(const std::string &src, std::string &err) {
     const Nvrtc &nv = nvrtc();
     if (!nv.ok) {
         err = "libnvrtc not available";
@@ -257,48 +255,61 @@ CUfunction compile(const std::string &src, int device, std::string &err) {
         err = "cuModuleLoadData / cuModuleGetFunction failed";
         return nullptr;
     }
-    (void)device;
     return fn;
 }
 
 }  // namespace
 
-// Returns 1 if the pass was launched through a compiled program, 0 if the
-// caller should run the interpreter kernel, or a negative QS_ERR_* code.
-int jit_launch(qs_state *s, const FParams &p, int K, int RB, size_t bufs_bytes, unsigned grid,
-               unsigned block) {
+// Should a pass with op-list signature `sig` run as a compiled program?
+// Counts launches per signature (policy 1 compiles from the second).
+bool jit_wanted(int device, uint64_t sig) {
     const int mode = jit_mode();
-    if (mode <= 0) return 0;
+    if (mode <= 0 || !nvrtc().ok || !driver().ok) return false;
+    std::lock_guard<std::mutex> lock(g_mu);
+    const int seen = ++g_seen[{device, sig}];
+    return mode >= 2 || seen >= 2;
+}
+
+// Register bits per thread of compiled programs (QSB_FUSED_JIT_RB, 3 or 4;
+// 5 bits = 4 compute warps per SM measured slower: too little latency hiding).
+int jit_rb() {
+    const char *e = std::getenv("QSB_FUSED_JIT_RB");
+    if (e && *e == '3') return 3;
+    return kJitDefaultRB;
+}
+
+// The compiled program for one planned launch group (compiling it on first
+// use), or nullptr when it cannot be built.
+void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max) {
     std::string src = generate(p, K, RB);
-    CUfunction fn = nullptr;
-    {
-        std::lock_guard<std::mutex> lock(g_mu);
-        Entry &e = g_cache[{s->device, src}];
-        ++e.seen;
-        if (e.failed || (mode == 1 && e.seen < 2 && !e.fn)) return 0;
-        if (!e.fn) {
-            std::string err;
-            e.fn = compile(src, s->device, err);
-            if (!e.fn) {
-                e.failed = true;
-                if (std::getenv("QSB_FUSED_JIT_VERBOSE")) std::fprintf(stderr, "qsb jit: %s\n", err.c_str());
-                return 0;
-            }
-            if (driver().set_attr(e.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)bufs_bytes) !=
-                CUDA_SUCCESS) {
-                e.failed = true;
-                e.fn = nullptr;
-                return 0;
-            }
-        }
-        fn = e.fn;
+    std::lock_guard<std::mutex> lock(g_mu);
+    const auto key = std::make_pair(device, src);
+    auto it = g_fns.find(key);
+    if (it != g_fns.end()) return (void *)it->second;
+    if (g_failed.count(key)) return nullptr;
+    std::string err;
+    CUfunction fn = compile(src, err);
+    if (fn && driver().set_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem_max) !=
+                  CUDA_SUCCESS) {
+        err = "cuFuncSetAttribute(max dynamic smem) failed";
+        fn = nullptr;
     }
+    if (!fn) {
+        g_failed[key] = true;
+        if (std::getenv("QSB_FUSED_JIT_VERBOSE")) std::fprintf(stderr, "qsb jit: %s\n", err.c_str());
+        return nullptr;
+    }
+    g_fns[key] = fn;
+    return (void *)fn;
+}
+
+int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned grid, unsigned block) {
     float4 *amps = (float4 *)s->amps;
     void *args[2] = {(void *)&amps, (void *)&p};
-    if (driver().launch(fn, grid, 1, 1, block, 1, 1, (unsigned)bufs_bytes, (CUstream)s->stream, args,
+    if (driver().launch((CUfunction)fn, grid, 1, 1, block, 1, 1, (unsigned)smem, (CUstream)s->stream, args,
                         nullptr) != CUDA_SUCCESS)
-        return -set_error(QS_ERR_CUDA, "cuLaunchKernel of a compiled pass failed");
-    return 1;
+        return set_error(QS_ERR_CUDA, "cuLaunchKernel of a compiled pass failed");
+    return QS_OK;
 }
 
 // Test / tooling hook: the generated source of the next pass (QSB_FUSED_JIT_DUMP).
