@@ -24,7 +24,7 @@
 //   M2 k_scan_guess   exclusive scan of the sums -> guessed chunk starts
 //   M3 k_trajectories both guessed trajectories per chunk (warp-transposed
 //                     through shared memory so HBM reads stay coalesced)
-//   M4 k_resolve      one thread walks the chunks: true start s, parity of
+//   M4 k_resolve_warp one thread walks the chunks (its warp stages the data): true start s, parity of
 //                     s's mantissa selects the trajectory, end = s + D exactly;
 //                     chunks that cross a binade (or whose guess fell in the
 //                     wrong binade) are re-summed sequentially from s
@@ -258,39 +258,133 @@ __device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, in
     return s;
 }
 
-// ---- M4: resolve true chunk starts (single thread) ---------------------------
+// ---- M4: resolve true chunk starts ------------------------------------------
+// M4 with the per-chunk data staged by a warp: the walk is a dependent chain
+// through s (the parity of s picks the trajectory), but the data it reads are
+// not, so 31 idle lanes are better spent fetching the next batch.  Each
+// iteration the warp issues the global loads of batch b+1 into registers,
+// lane 0 walks batch b out of shared memory (one DADD + a select on the
+// critical path per chunk), then the registers land in shared memory for
+// the next walk.  Same arithmetic and order as a single-thread walk.
+constexpr int kResolveBatch = 256;
 template <class A>
-__global__ void k_resolve(const A *__restrict__ amps, uint64_t nch, int clog,
-                          double s_start, const double *__restrict__ g0, const double *__restrict__ d0,
-                          const double *__restrict__ d1, const double *__restrict__ hi,
-                          const int *__restrict__ flags, double *__restrict__ start,
-                          double *__restrict__ total, unsigned long long *__restrict__ nslow) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(32)
+    k_resolve_warp(const A *__restrict__ amps, uint64_t nch, int clog, double s_start,
+                   const double *__restrict__ g0, const double *__restrict__ d0,
+                   const double *__restrict__ d1, const double *__restrict__ hi,
+                   const int *__restrict__ flags, double *__restrict__ start,
+                   double *__restrict__ total, unsigned long long *__restrict__ nslow) {
+    constexpr int kPer = kResolveBatch / 32;
+    __shared__ double sd0[kResolveBatch], sd1[kResolveBatch], shi[kResolveBatch], slo[kResolveBatch];
+    __shared__ int sfl[kResolveBatch];
+    __shared__ double sst[kResolveBatch];
+    const int lane = threadIdx.x;
+    double r0[kPer], r1[kPer], rh[kPer], rl[kPer];
+    int rf[kPer];
+    auto fetch = [&](uint64_t b0) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const uint64_t k = b0 + (uint64_t)(lane + 32 * i);
+            if (k < nch) {
+                r0[i] = d0[k];
+                r1[i] = d1[k];
+                rh[i] = hi[k];
+                rl[i] = binade_lo(g0[k]);
+                rf[i] = flags[k];
+            }
+        }
+    };
+    auto land = [&]() {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int j = lane + 32 * i;
+            sd0[j] = r0[i];
+            sd1[j] = r1[i];
+            shi[j] = rh[i];
+            slo[j] = rl[i];
+            sfl[j] = rf[i];
+        }
+    };
+    fetch(0);
+    land();
+    __syncwarp();
     double s = s_start;
     unsigned long long slow = 0;
-    for (uint64_t k = 0; k < nch; ++k) {
-        start[k] = s;
-        const int f = flags[k];
-        double e;
-        bool valid;
-        if (f & kFlagExact0) {
-            valid = (s == s_start);
-            e = d0[k];
-        } else {
-            const double h = hi[k];
-            const double lo = binade_lo(g0[k]);
-            const bool odd = (__double_as_longlong(s) & 1ll) != 0;
-            e = __dadd_rn(s, odd ? d1[k] : d0[k]);
-            valid = (f & kFlagOk) && s >= lo && s < h && e < h;
+    for (uint64_t b0 = 0; b0 < nch; b0 += kResolveBatch) {
+        const uint64_t nb = b0 + kResolveBatch;
+        if (nb < nch) fetch(nb);  // in flight during the walk below
+        const int cnt = (int)((nch - b0) < (uint64_t)kResolveBatch ? (nch - b0) : kResolveBatch);
+        if (lane == 0) {
+            // speculative walk: no data-dependent branch on the chain (the
+            // parity select and one DADD per chunk); validity is accumulated
+            // and the batch is re-walked with the exact slow path if any
+            // chunk failed (a binade crossing: a handful per register)
+            const double s0 = s;
+            bool all_ok = true;
+            for (int j0 = 0; j0 < cnt; j0 += 16) {
+                // 16 chunks' data into registers first: nothing on the chain
+                // waits for a shared-memory load
+                double a[16], b[16], h[16], lo[16], ss[16];
+                int fl[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    a[i] = sd0[j0 + i];
+                    b[i] = sd1[j0 + i];
+                    h[i] = shi[j0 + i];
+                    lo[i] = slo[j0 + i];
+                    fl[i] = sfl[j0 + i];
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    if (j0 + i >= cnt) break;  // only in the last, partial batch
+                    ss[i] = s;
+                    const bool odd = (__double_as_longlong(s) & 1ll) != 0;
+                    const double e_traj = __dadd_rn(s, odd ? b[i] : a[i]);
+                    const bool ex0 = (fl[i] & kFlagExact0) != 0;
+                    const bool ok_traj = ((fl[i] & kFlagOk) != 0) & (s >= lo[i]) & (s < h[i]) & (e_traj < h[i]);
+                    const bool ok_ex0 = s == s_start;
+                    all_ok &= ex0 ? ok_ex0 : ok_traj;
+                    s = ex0 ? a[i] : e_traj;
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (j0 + i < cnt) sst[j0 + i] = ss[i];
+            }
+            if (!all_ok) {
+                s = s0;
+                for (int j = 0; j < cnt; ++j) {
+                    const uint64_t k = b0 + j;
+                    sst[j] = s;
+                    const int f = sfl[j];
+                    double e;
+                    bool valid;
+                    if (f & kFlagExact0) {
+                        valid = (s == s_start);
+                        e = sd0[j];
+                    } else {
+                        const bool odd = (__double_as_longlong(s) & 1ll) != 0;
+                        e = __dadd_rn(s, odd ? sd1[j] : sd0[j]);
+                        const double h = shi[j];
+                        valid = (f & kFlagOk) && s >= slo[j] && s < h && e < h;
+                    }
+                    if (!valid) {
+                        e = walk_chunk(amps, k, clog, s);
+                        ++slow;
+                    }
+                    s = e;
+                }
+            }
         }
-        if (!valid) {
-            e = walk_chunk(amps, k, clog, s);
-            ++slow;
-        }
-        s = e;
+        __syncwarp();
+        for (int j = lane; j < cnt; j += 32) start[b0 + j] = sst[j];  // coalesced
+        __syncwarp();
+        if (nb < nch) land();
+        __syncwarp();
     }
-    *total = s;
-    *nslow = slow;
+    if (lane == 0) {
+        *total = s;
+        *nslow = slow;
+    }
 }
 
 // ---- M5: normalised CDF value at each chunk end --------------------------------
@@ -515,8 +609,8 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
         k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
             amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags);
     }
-    k_resolve<<<1, 1, 0, s->stream>>>(amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi,
-                                      c.flags, c.start, c.end, c.nslow);
+    k_resolve_warp<<<1, 32, 0, s->stream>>>(amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi,
+                                            c.flags, c.start, c.end, c.nslow);
     QS_CUDA(cudaGetLastError());
     return QS_OK;
 }
