@@ -110,7 +110,6 @@ const Driver &driver() {
 }
 
 // ---- code generation -----------------------------------------------------------
-constexpr int kJitDefaultRB = 4;    // register bits per thread of compiled programs
 constexpr int kJitLoopRun = 3;      // runs at least this long stay loops ...
 constexpr int kJitLoopMinRegs = 8;  // ... when each op touches at least 8 float4 registers
 void hexf(std::string &out, float x) {
@@ -270,12 +269,13 @@ bool jit_wanted(int device, uint64_t sig) {
     return mode >= 2 || seen >= 2;
 }
 
-// Register bits per thread of compiled programs (QSB_FUSED_JIT_RB, 3 or 4;
-// 5 bits = 4 compute warps per SM measured slower: too little latency hiding).
-int jit_rb() {
+// Register bits per thread of compiled programs: QSB_FUSED_JIT_RB (3 or 4)
+// or the caller's choice (5 bits = 4 compute warps per SM measured slower).
+int jit_rb(int dflt) {
     const char *e = std::getenv("QSB_FUSED_JIT_RB");
     if (e && *e == '3') return 3;
-    return kJitDefaultRB;
+    if (e && *e == '4') return 4;
+    return dflt == 3 ? 3 : 4;
 }
 
 // The compiled program for one planned launch group (compiling it on first

@@ -58,7 +58,17 @@ def default_tile_qubits(num_qubits: int) -> int:
 
 
 def plan(num_qubits: int, ops, tile_qubits: int | None = None) -> list[Pass]:
-    """Greedy in-order grouping into passes of at most K tile qubits."""
+    """Greedy in-order grouping into passes of at most K tile qubits.  Without
+    an explicit K: 12-qubit tiles when they need no more passes than 13-qubit
+    ones (two persistent CTAs per SM fit with K = 12; see fused.cu)."""
+    if tile_qubits is None and num_qubits >= 13:
+        p12 = _plan(num_qubits, ops, 12)
+        p13 = _plan(num_qubits, ops, 13)
+        return p12 if len(p12) <= len(p13) else p13
+    return _plan(num_qubits, ops, tile_qubits)
+
+
+def _plan(num_qubits: int, ops, tile_qubits: int | None) -> list[Pass]:
     n = num_qubits
     K = tile_qubits or default_tile_qubits(n)
     if n < 10 or K < 10:
