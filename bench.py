@@ -451,6 +451,8 @@ def run_sharded(args):
                "d2h_bytes_per_step": (8 << L) * world, "steps": k2,
                "timing": "host wall clock, every rank uploads/downloads its shard around the layer, max over ranks"}
     extras = {}
+    if not args.no_extras:
+        extras["global_gates"] = run_global_gate_probe(n, local, world)
     if world >= 4 and not args.no_extras:
         extras["config5_hlayer_qft36"] = run_config5(st, eng, local, world)
     if rank == 0:
@@ -470,6 +472,47 @@ def run_sharded(args):
             "cpu_baseline": None,
         }))
     dist.destroy_process_group()
+
+
+def run_global_gate_probe(n, local, world, reps=3):
+    """H on each of the log2(N) global qubits from the identity qubit map:
+    NCCL qubit swaps + local sweeps (default path) vs one peer-memory kernel
+    per partner pair over NVLink (csrc/peer.cu).  Host wall clock between
+    device-synchronised barriers, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_00988_b200.gates import H
+    from paper_1805_00988_b200.sharded import ShardedState
+
+    g = int(round(math.log2(world)))
+    out = {"n_qubits": n, "global_qubits": g}
+    for name, peer in (("swap_nccl", False), ("peer_nvlink", True)):
+        try:
+            st = ShardedState.distributed(n, device=local, peer_gates=peer)
+            best = float("inf")
+            for _ in range(reps + 1):
+                st.reset(0)
+                st.synchronize()
+                torch.cuda.synchronize(local)
+                dist.barrier()
+                t0 = time.perf_counter()
+                for q in range(n - g, n):
+                    st.apply_gate(H, q)
+                st.synchronize()
+                torch.cuda.synchronize(local)
+                dist.barrier()
+                best = min(best, time.perf_counter() - t0)
+            t = torch.tensor([best], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out[name] = {"ms_per_global_gate": float(t.item()) * 1e3 / g,
+                         "swaps_per_rep": st.swaps // (reps + 1),
+                         "peer_gates_per_rep": st.peer_gate_count // (reps + 1),
+                         "peer_mode_active": st.peer_gates}
+            del st
+        except Exception as exc:  # noqa: BLE001
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 def run_config5(st_main, eng_main, local, world):

@@ -180,6 +180,23 @@ int qs_cdf_extend(qs_state *s, double start, double *end);
 int qs_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
                     uint64_t index_base, uint64_t global_dim, int is_last, int64_t *out);
 
+/* ---- global-qubit gates over peer memory (sharded registers) --------------- */
+/* cudaIpc handle (64 bytes) of the register's device buffer, and mapping a
+ * partner process's handle into this process on `device` (NVLink P2P). */
+int qs_ipc_handle(qs_state *s, void *out64);
+int qs_ipc_open(int device, const void *handle64, void **out);
+int qs_ipc_close(int device, void *ptr);
+/* The pair update of apply_gate / apply_controlled_gate (kernel.py:108-165)
+ * for a target on a GLOBAL qubit of a sharded register, in one kernel: this
+ * shard and `peer_amps` (the partner shard, same local index space) hold the
+ * two amplitudes of every pair; own_is_a = 1 on the shard whose rank bit is 0.
+ * Both partners call it concurrently; each updates half of the pairs (split
+ * on the highest local non-control bit), reading and writing the partner's
+ * amplitudes through peer memory.  ctrl_mask = local control bits (controls
+ * on other global qubits are rank predicates of the caller).  The caller
+ * orders the two shards' streams before and after. */
+int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const float m[8]);
+
 #ifdef __cplusplus
 }
 #endif

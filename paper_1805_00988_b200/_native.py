@@ -34,6 +34,7 @@ EXPORTS = (
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
+    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer",
 )
 
 
@@ -102,6 +103,10 @@ def _declare(L):
         "qs_cdf_extend": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sample_shard": ([vp, ctypes.POINTER(qs_pcg64), i64, ctypes.c_double, ctypes.c_double,
                              u64, u64, i32, vp], i32),
+        "qs_ipc_handle": ([vp, vp], i32),
+        "qs_ipc_open": ([i32, vp, ctypes.POINTER(vp)], i32),
+        "qs_ipc_close": ([i32, vp], i32),
+        "qs_apply_gate_peer": ([vp, vp, i32, u64, f32p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

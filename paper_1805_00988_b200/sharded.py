@@ -146,34 +146,6 @@ class CudaEngine:
     def probabilities(self) -> np.ndarray:
         return self.state.probabilities()
 
-    def sample_outcomes(self, samples: int, seed=None) -> np.ndarray:
-        """Per-draw outcomes (logical basis indices), bit-exact with pairsim's
-        sample on the full register (measure.py:76-85): the exact sequential
-        CDF is chained across shards in index order."""
-        from .errors import DegenerateStateError
-
-        if samples < 1:
-            raise ValueError("n_samples must be >= 1")
-        self.canonicalize()
-        rng = self.transport.common_seed_words(seed)
-        starts, total = self.transport.cdf_chain(self.engines, self.ranks)
-        if not total > 0.0:
-            raise DegenerateStateError("all outcome probabilities are zero")
-        L, dim = self.L, 1 << self.num_qubits
-        outs = [eng.sample_shard(samples, rng, starts[r], total, r << L, dim, r == self.world - 1)
-                for eng, r in zip(self.engines, self.ranks)]
-        return self.transport.combine_max(outs)
-
-    def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
-        keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
-        return {int(k): int(c) for k, c in zip(keys, counts)}
-
-    def measure_collapse(self, seed=None) -> int:
-        """One draw, then the register becomes |outcome> (measure.py:88-99)."""
-        m = int(self.sample_outcomes(1, seed)[0])
-        self.reset(m)
-        return m
-
     def norm_squared(self) -> float:
         return self.state.norm_squared()
 
@@ -185,6 +157,33 @@ class CudaEngine:
 
     def sample_shard(self, k, rng, start, total, base, gdim, is_last) -> np.ndarray:
         return self.state.sample_shard(k, rng, start, total, base, gdim, is_last)
+
+    # ---- peer-memory global gates (csrc/peer.cu) --------------------------------
+    def peer_ref(self):
+        """What a partner in this process passes to peer_gate: our device pointer."""
+        return self.state.device_pointer()
+
+    def ipc_handle(self) -> bytes:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(64)
+        N.check(N.lib().qs_ipc_handle(self.state.handle, buf))
+        return buf.raw
+
+    def open_peer(self, handle: bytes) -> int:
+        import ctypes
+
+        ptr = ctypes.c_void_p()
+        N.check(N.lib().qs_ipc_open(self.device, handle, ctypes.byref(ptr)))
+        return ptr.value
+
+    def close_peer(self, ptr: int) -> None:
+        N.lib().qs_ipc_close(self.device, ptr)
+
+    def peer_gate(self, peer, own_is_a: bool, ctrl_mask: int, m: np.ndarray) -> None:
+        mm = np.ascontiguousarray(m, dtype=np.float32)
+        N.check(N.lib().qs_apply_gate_peer(self.state.handle, peer, int(bool(own_is_a)), int(ctrl_mask),
+                                           N.f32ptr(mm)))
 
 
 # ----------------------------------------------------------------------------
@@ -214,6 +213,15 @@ class LocalTransport:
 
     def allreduce_sum(self, values):
         return [sum(values)] * len(values)
+
+    def peer_setup(self, engines, ranks, g):
+        """{(rank, partner): partner's peer reference} for every rank bit."""
+        by_rank = dict(zip(ranks, engines))
+        return {(r, r ^ (1 << b)): by_rank[r ^ (1 << b)].peer_ref() for r in ranks for b in range(g)}
+
+    def peer_barrier(self, engines):
+        for eng in engines:
+            eng.synchronize()
 
     def cdf_chain(self, engines, ranks):
         """Exact running-sum entry value of every shard, in rank order."""
@@ -260,6 +268,42 @@ class DistTransport:
                 w.wait()
             mine.copy_(stg)
         eng.comm_end()
+
+    def peer_setup(self, engines, ranks, g):
+        """Map the partner shards' buffers into this process (cudaIpc over
+        NVLink).  All ranks agree on success (a MIN all-reduce), so a rank that
+        cannot map its partners never leaves the others waiting: on failure
+        every rank returns None and the swap path is used."""
+        import torch
+
+        (eng,) = engines
+        handles = [None] * self.world
+        ok = 1
+        try:
+            mine = eng.ipc_handle()
+        except Exception:  # noqa: BLE001
+            mine, ok = b"", 0
+        self.dist.all_gather_object(handles, mine, group=self.group)
+        peers = {}
+        if ok:
+            try:
+                for b in range(g):
+                    partner = self.rank ^ (1 << b)
+                    peers[(self.rank, partner)] = eng.open_peer(handles[partner])
+            except Exception:  # noqa: BLE001
+                ok = 0
+        flag = self._tensor(torch.tensor([ok], dtype=torch.int32))
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(flag.cpu().item()) != 1:
+            for ptr in peers.values():
+                eng.close_peer(ptr)
+            return None
+        return peers
+
+    def peer_barrier(self, engines):
+        (eng,) = engines
+        eng.synchronize()
+        self.dist.barrier(group=self.group)
 
     def _tensor(self, arr):
         import torch
@@ -321,7 +365,7 @@ class ShardedState:
     """A 2^n register over 2^g shards (QCGPU-style gate API)."""
 
     def __init__(self, num_qubits: int, engines, transport, ranks, world: int,
-                 chunk_amps: int = 1 << 26):
+                 chunk_amps: int = 1 << 26, peer_gates: bool | None = None):
         g = int(round(math.log2(world)))
         if 1 << g != world:
             raise ValueError("the shard count must be a power of two")
@@ -333,10 +377,21 @@ class ShardedState:
         self.world = world
         self.chunk = chunk_amps
         self.swaps = 0
+        # Global-target pair gates as one peer-memory kernel per partner pair
+        # (csrc/peer.cu) instead of a qubit swap; QSB_SHARD_PEER=1 turns it on
+        # by default.  Falls back to swaps if the partners cannot be mapped.
+        if peer_gates is None:
+            import os
+
+            peer_gates = os.environ.get("QSB_SHARD_PEER", "0") == "1"
+        self.peer_gates = bool(peer_gates) and g > 0 and all(hasattr(e, "peer_gate") for e in self.engines)
+        self._peers = None
+        self.peer_gate_count = 0
 
     # ---- constructors ------------------------------------------------------
     @classmethod
-    def distributed(cls, num_qubits: int, group=None, device: int | None = None, engine_factory=None):
+    def distributed(cls, num_qubits: int, group=None, device: int | None = None, engine_factory=None,
+                    peer_gates: bool | None = None):
         import torch.distributed as dist
 
         tr = DistTransport(group)
@@ -349,17 +404,18 @@ class ShardedState:
             eng = CudaEngine(L, dev)
         else:
             eng = engine_factory(L)
-        st = cls(num_qubits, [eng], tr, [tr.rank], tr.world)
+        st = cls(num_qubits, [eng], tr, [tr.rank], tr.world, peer_gates=peer_gates)
         st.reset(0)
         return st
 
     @classmethod
-    def virtual(cls, num_qubits: int, shards: int, device: int = 0, engine_factory=None):
+    def virtual(cls, num_qubits: int, shards: int, device: int = 0, engine_factory=None,
+                peer_gates: bool | None = None):
         g = int(round(math.log2(shards)))
         L = num_qubits - g
         make = engine_factory or (lambda L_: CudaEngine(L_, device))
         engines = [make(L) for _ in range(shards)]
-        st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards)
+        st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards, peer_gates=peer_gates)
         st.reset(0)
         return st
 
@@ -386,6 +442,39 @@ class ShardedState:
         lay.swap_physical(p, lay.L - 1)
         self.swaps += 1
 
+    def _control_masks(self, controls) -> tuple[int, int]:
+        """(local control mask, rank-bit predicate) under the current qubit map."""
+        lay = self.layout
+        cmask, need = 0, 0
+        for c in controls:
+            pc = lay.pos[c]
+            if pc < lay.L:
+                cmask |= 1 << pc
+            else:
+                need |= 1 << (pc - lay.L)
+        return cmask, need
+
+    def _peer_ready(self) -> bool:
+        if not self.peer_gates:
+            return False
+        if self._peers is None:
+            self._peers = self.transport.peer_setup(self.engines, self.ranks, self.layout.g) or False
+            if self._peers is False:
+                self.peer_gates = False
+        return bool(self._peers)
+
+    def _peer_gate(self, rank_bit: int, cmask: int, need: int, m: np.ndarray) -> None:
+        """Pair update with the target on global rank bit `rank_bit`, applied by
+        both partners in one peer-memory kernel each (csrc/peer.cu)."""
+        self.transport.peer_barrier(self.engines)
+        for eng, r in zip(self.engines, self.ranks):
+            if (r & need) != need:
+                continue
+            partner = r ^ (1 << rank_bit)
+            eng.peer_gate(self._peers[(r, partner)], not (r >> rank_bit) & 1, cmask, m)
+        self.transport.peer_barrier(self.engines)
+        self.peer_gate_count += 1
+
     def apply_op(self, gate, target: int, controls=()) -> "ShardedState":
         n = self.num_qubits
         qs = [int(target), *map(int, controls)]
@@ -406,6 +495,10 @@ class ShardedState:
             if local:
                 target = local[0]
                 controls = [q for q in qs if q != target]
+        if kind == N.QS_OP_PAIR and not lay.is_local(target) and self._peer_ready():
+            cmask, need = self._control_masks(controls)
+            self._peer_gate(lay.pos[target] - lay.L, cmask, need, m)
+            return self
         if kind == N.QS_OP_PAIR or not any(lay.is_local(q) for q in [target, *controls]):
             self._ensure_local(target)
         t_phys = lay.pos[target]
@@ -485,14 +578,12 @@ class ShardedState:
                     controls = tuple(q for q in qs if q != target)
             if not lay.is_local(target):
                 flush()
-                self._ensure_local(target)
-            cmask, need = 0, 0
-            for c in controls:
-                pc = lay.pos[c]
-                if pc < lay.L:
-                    cmask |= 1 << pc
-                else:
-                    need |= 1 << (pc - lay.L)
+                if kind == N.QS_OP_PAIR and self._peer_ready():
+                    cmask, need = self._control_masks(controls)
+                    self._peer_gate(lay.pos[target] - lay.L, cmask, need, m)
+                    continue
+                self._ensure_local(target)  # moves qubits: masks after it
+            cmask, need = self._control_masks(controls)
             pending.append((kind, lay.pos[target], cmask, m, need))
         flush()
         return self

@@ -67,6 +67,30 @@ class OracleEngine:
     def cdf_extend(self, start):
         return float(np.cumsum(np.concatenate([[start], oc.probabilities(self.amps)]))[-1])
 
+    # peer-memory global gates: in one process the "peer reference" is the
+    # partner engine itself; the same half split as csrc/peer.cu
+    def peer_ref(self):
+        return self
+
+    def peer_gate(self, peer, own_is_a, ctrl_mask, m):
+        L = self.num_qubits
+        free = [q for q in range(L) if not (ctrl_mask >> q) & 1]
+        idx = np.arange(1 << L)
+        sel = (idx & ctrl_mask) == ctrl_mask
+        if free:
+            s = free[-1]
+            sel &= ((idx >> s) & 1) == (0 if own_is_a else 1)
+        elif not own_is_a:
+            return
+        i = idx[sel]
+        va = (self.amps if own_is_a else peer.amps)[i]
+        vb = (peer.amps if own_is_a else self.amps)[i]
+        tmp = np.empty(2 * i.size, np.complex64)
+        tmp[0::2], tmp[1::2] = va, vb
+        oc.apply_gate(tmp, 0, M8Gate(m))
+        (self.amps if own_is_a else peer.amps)[i] = tmp[0::2]
+        (peer.amps if own_is_a else self.amps)[i] = tmp[1::2]
+
     def sample_shard(self, k, rng, start, total, base, gdim, is_last):
         cdf = np.cumsum(np.concatenate([[start], oc.probabilities(self.amps)]))[1:]
         ncdf = cdf / total

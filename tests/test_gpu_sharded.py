@@ -55,3 +55,17 @@ def test_sharded_sampling_equals_unsharded(n, shards):
     for seed in (1, 77):
         assert np.array_equal(st.sample_outcomes(5000, seed), ref.sample_outcomes(5000, seed))
     assert st.measure(1000, seed=4) == ref.measure(1000, seed=4)
+
+
+@pytest.mark.parametrize("n,shards", [(12, 2), (16, 4), (20, 8)])
+def test_peer_gates_equal_unsharded(n, shards):
+    """Global-target gates through csrc/peer.cu (partner shards on the same GPU
+    stand in for NVLink peers): no swaps, same bits as the unsharded register."""
+    circ = Circuit(n, build_hadamard_layer(n).instructions + mixed_circuit(n, 80, n + 1).instructions
+                   + build_qft(n).instructions)
+    ref = State(n)
+    execute(circ, ref, fuse=False)
+    st = ShardedState.virtual(n, shards, peer_gates=True)
+    st.run(circ)
+    assert st.peer_gate_count > 0
+    assert same_values(st.amplitudes(), ref.amplitudes())

@@ -154,19 +154,75 @@ class TestVirtualShards:
         assert a[0b110101] == 1 and np.count_nonzero(a) == 1
 
 
+class TestPeerGates:
+    """Global-target gates as one peer-memory update per partner pair
+    (csrc/peer.cu semantics, oracle engines): no qubit swaps, same bits."""
+
+    @pytest.mark.parametrize("n,shards", [(6, 2), (7, 4), (8, 8), (9, 4)])
+    def test_random_circuits_bitwise(self, n, shards):
+        for seed in range(3):
+            circ = mixed_circuit(n, 60, seed + 10 * n)
+            ref = oracle_run(circ)
+            st = ShardedState.virtual(n, shards, engine_factory=OracleEngine, peer_gates=True)
+            st.run(circ)
+            assert st.peer_gate_count > 0
+            assert same_values(st.amplitudes(), ref)
+
+    def test_gate_api_and_controls_on_every_bit_class(self):
+        """Controls on local bits (including the split bit's neighbours), on other
+        global bits (rank predicates), and all-local-controlled targets."""
+        n, shards = 6, 4
+        rng = np.random.default_rng(3)
+        ins = [Apply(FIXED_GATES["h"], q) for q in range(n)]
+        for _ in range(40):
+            t = int(rng.integers(n - 2, n))  # global targets
+            others = [q for q in range(n) if q != t]
+            g = [FIXED_GATES["h"], FIXED_GATES["x"], FIXED_GATES["y"], u1(0.7)][int(rng.integers(4))]
+            k = rng.random()
+            if k < 0.3:
+                ins.append(Apply(g, t))
+            elif k < 0.7:
+                ins.append(ControlledApply(g, int(rng.choice(others)), t))
+            else:
+                c1, c2 = (int(x) for x in rng.choice(others, 2, replace=False))
+                ins.append(ControlledControlledApply(g, c1, c2, t))
+        circ = Circuit(n, tuple(ins))
+        st = ShardedState.virtual(n, shards, engine_factory=OracleEngine, peer_gates=True)
+        for i in circ.instructions:
+            if isinstance(i, Apply):
+                st.apply_gate(i.gate, i.target)
+            elif isinstance(i, ControlledApply):
+                st.apply_controlled_gate(i.gate, i.control, i.target)
+            else:
+                st.apply_controlled_controlled_gate(i.gate, i.control1, i.control2, i.target)
+        assert st.peer_gate_count > 0
+        assert same_values(st.amplitudes(), oracle_run(circ))
+
+    def test_hlayer_and_qft_without_swaps(self):
+        n, shards = 8, 4
+        circ = Circuit(n, build_hadamard_layer(n).instructions + build_qft(n).instructions)
+        st = ShardedState.virtual(n, shards, engine_factory=OracleEngine, peer_gates=True)
+        st.run(circ)
+        # only the all-global controlled phase cu1(7, 6) still swaps a qubit in
+        assert st.swaps <= 1 and st.peer_gate_count >= 2
+        assert same_values(st.amplitudes(), oracle_run(circ))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, seed, q):
+def _worker(rank, world, port, n, seed, q, peer=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         circ = mixed_circuit(n, 50, seed)
-        st = ShardedState.distributed(n, engine_factory=OracleEngine)
+        # peer=True: oracle engines cannot map a partner process's buffer, so
+        # every rank must agree to fall back to qubit swaps (no rank waits)
+        st = ShardedState.distributed(n, engine_factory=OracleEngine, peer_gates=peer)
         st.run(circ)
         amps = st.amplitudes()
         probs = st.probabilities()
@@ -181,12 +237,12 @@ def _worker(rank, world, port, n, seed, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 7), (4, 8)])
-def test_gloo_distributed_matches_oracle(world, n):
+@pytest.mark.parametrize("world,n,peer", [(2, 7, False), (4, 8, False), (2, 7, True)])
+def test_gloo_distributed_matches_oracle(world, n, peer):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, 1234 + n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, 1234 + n, q, peer)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
