@@ -141,6 +141,15 @@ int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile,
  * is qs_apply_fused). */
 int qs_apply_fused_f64(qs_state *s, const int32_t *tile_qubits, int ntile,
                        const qs_op64 *ops, int nops);
+/* Fused passes are compiled at run time into straight-line kernels (NVRTC,
+ * host worker threads); until a pass's program is ready it runs on the
+ * interpreter kernel, with the same bits.  Wait for every queued compile and
+ * load the programs of `device` (< 0: all).  Not needed for correctness. */
+int qs_jit_sync(int device);
+/* Drop queued compiles, let an in-flight one finish and stop the compile
+ * threads (call before process teardown; the Python layer registers it with
+ * atexit).  Later fused passes run on the interpreter kernel. */
+int qs_jit_shutdown(void);
 /* Swap qubits q1 and q2 (a basis permutation; used by the sharded layer). */
 int qs_swap_qubits(qs_state *s, int q1, int q2);
 

@@ -34,7 +34,8 @@ EXPORTS = (
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
-    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer",
+    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_jit_sync",
+    "qs_jit_shutdown",
 )
 
 
@@ -107,6 +108,8 @@ def _declare(L):
         "qs_ipc_open": ([i32, vp, ctypes.POINTER(vp)], i32),
         "qs_ipc_close": ([i32, vp], i32),
         "qs_apply_gate_peer": ([vp, vp, i32, u64, f32p], i32),
+        "qs_jit_sync": ([i32], i32),
+        "qs_jit_shutdown": ([], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -124,6 +127,10 @@ def lib():
             _build.build()
         _lib = ctypes.CDLL(str(LIB_PATH))
         _declare(_lib)
+        # stop the pass-compile threads before interpreter / library teardown
+        import atexit
+
+        atexit.register(_lib.qs_jit_shutdown)
     return _lib
 
 

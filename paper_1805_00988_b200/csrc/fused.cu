@@ -55,9 +55,9 @@
 namespace qsb {
 
 // run-time compiled pass programs (jit.cu)
-bool jit_wanted(int device, uint64_t sig);
+bool jit_enabled();
 int jit_rb(int dflt);
-void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max);
+void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait);
 int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned grid, unsigned block);
 
 namespace {
@@ -523,17 +523,15 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         return QS_OK;
     }
 
-    // Compiled straight-line programs (jit.cu) when the policy asks for them
-    // and every launch group compiles; otherwise the interpreter kernel.
-    uint64_t sig = 1469598103934665603ull ^ tile_mask ^ ((uint64_t)n << 56);
-    {
-        const unsigned char *b = (const unsigned char *)ops;
-        for (size_t i = 0; i < (size_t)nops * sizeof(qs_op); ++i) sig = (sig ^ b[i]) * 1099511628211ull;
-    }
+    // Compiled straight-line programs (jit.cu) once every launch group's
+    // program is ready; until then (compiles queued in the background) and
+    // without NVRTC, the interpreter kernel.
     const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
     uint64_t grid = (uint64_t)s->num_sms * (uint64_t)ctas_per_sm(K);
     if (grid > (1ull << (n - K))) grid = 1ull << (n - K);
-    if (jit_wanted(s->device, sig)) {
+    if (jit_enabled()) {
+        const char *jm = std::getenv("QSB_FUSED_JIT");
+        const bool wait = jm && std::atoi(jm) >= 2;
         // register bits per thread: 3 (twice the warps, shorter per-op bodies)
         // for phase-dominated passes, 4 otherwise (QSB_FUSED_JIT_RB overrides)
         int nphase = 0;
@@ -543,11 +541,13 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         if (plan_pass(s, tile_mask, ops, nops, jrb, groups) == QS_OK) {
             std::vector<void *> fns;
             for (const FParams &g : groups) {
-                void *fn = jit_get(s->device, g, K, jrb, bufs + kMaxOps * sizeof(FOp));
-                if (!fn) break;
+                void *fn = jit_get(s->device, g, K, jrb, bufs + kMaxOps * sizeof(FOp), wait);
+                if (!fn && wait) break;
                 fns.push_back(fn);
             }
-            if (fns.size() == groups.size()) {
+            bool all = fns.size() == groups.size();
+            for (void *f : fns) all = all && f;
+            if (all) {
                 for (size_t i = 0; i < groups.size(); ++i) {
                     const int rc = jit_launch(s, fns[i], groups[i], bufs + (size_t)groups[i].nops * sizeof(FOp),
                                               (unsigned)grid, (1u << (K - 1 - jrb)) + 32u);

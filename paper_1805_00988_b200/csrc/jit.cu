@@ -14,20 +14,29 @@
 // arithmetic, same `one` opaque to ptxas: the results are the interpreter's
 // bit for bit (tests run every fused case both ways).
 //
-// Policy (QSB_FUSED_JIT): 0 = off; 1 (default) = compile a pass program the
-// second time it is launched (repeated circuits, benchmarks), interpret it
-// the first time; 2 = always.  Compiled programs are cached per device for
-// the life of the process.  NVRTC is loaded with dlopen; without it the
-// interpreter kernel runs (same device code path, no CPU fallback).
+// Policy (QSB_FUSED_JIT): 0 = off; 1 (default) = queue the compile on the
+// first launch of a pass and keep interpreting it until the program is ready
+// (NVRTC runs on host worker threads, nothing blocks); 2 = compile
+// synchronously and always launch the program.  qs_jit_sync waits for the
+// queued compiles (benchmarks call it after warm-up).  Compiled programs are
+// cached per device for the life of the process.  NVRTC is loaded with
+// dlopen; without it the interpreter kernel runs (same device code path, no
+// CPU fallback).
 
 #include <dlfcn.h>
+#include <pthread.h>
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda.h>
@@ -203,10 +212,29 @@ std::string generate(const FParams &p, int K, int RB) {
     return src;
 }
 
+// ---- compile service ------------------------------------------------------------
+// NVRTC runs on a small pool of host worker threads; a finished cubin is
+// loaded into the device context by the next launching thread that asks for
+// it (or by qs_jit_sync), so no host thread blocks on a compile unless the
+// caller asks for it (QSB_FUSED_JIT=2, qs_jit_sync).
+struct Job {
+    int device = 0;
+    std::string src;
+    size_t smem_max = 0;
+    int state = 0;  // 0 queued / compiling, 1 cubin ready, 2 failed
+    std::vector<char> cubin;
+    std::string err;
+};
+using Key = std::pair<int, std::string>;
+
 std::mutex g_mu;
-std::map<std::pair<int, std::string>, CUfunction> g_fns;  // compiled programs
-std::map<std::pair<int, std::string>, bool> g_failed;
-std::map<std::pair<int, uint64_t>, int> g_seen;            // launches per op-list signature
+std::condition_variable g_cv;       // job state changes and new work
+std::map<Key, CUfunction> g_fns;   // loaded programs
+std::map<Key, bool> g_failed;
+std::map<Key, std::shared_ptr<Job>> g_jobs;  // queued, compiling or awaiting load
+std::deque<std::shared_ptr<Job>> g_queue;
+std::vector<pthread_t> g_workers;
+bool g_stop = false;
 
 int jit_mode() {
     const char *e = std::getenv("QSB_FUSED_JIT");
@@ -214,60 +242,109 @@ int jit_mode() {
     return std::atoi(e);
 }
 
-CUfunction compile(const std::string &src, std::string &err) {
+bool compile_cubin(Job &job) {
     const Nvrtc &nv = nvrtc();
-    if (!nv.ok) {
-        err = "libnvrtc not available";
-        return nullptr;
-    }
-    const Driver &dr = driver();
-    if (!dr.ok) {
-        err = "driver entry points not available";
-        return nullptr;
-    }
     const char *hdrs[2] = {kJitCommon, kJitFusedDev};
     const char *names[2] = {"common.cuh", "fused_dev.cuh"};
     nvrtcProgram_t prog = nullptr;
-    if (nv.create(&prog, src.c_str(), "qsb_pass.cu", 2, hdrs, names) != 0) {
-        err = "nvrtcCreateProgram failed";
-        return nullptr;
+    if (nv.create(&prog, job.src.c_str(), "qsb_pass.cu", 2, hdrs, names) != 0) {
+        job.err = "nvrtcCreateProgram failed";
+        return false;
     }
     const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DQSB_JIT=1"};
-    const int rc = nv.compile(prog, 4, opts);
-    if (rc != 0) {
+    if (nv.compile(prog, 4, opts) != 0) {
         size_t n = 0;
         nv.log_size(prog, &n);
         std::string log(n, '\0');
         nv.log(prog, &log[0]);
-        err = "NVRTC compile failed: " + log.substr(0, 2000);
+        job.err = "NVRTC compile failed: " + log.substr(0, 2000);
         nv.destroy(&prog);
-        return nullptr;
+        return false;
     }
     size_t n = 0;
     nv.cubin_size(prog, &n);
-    std::vector<char> cubin(n);
-    nv.cubin(prog, cubin.data());
+    job.cubin.resize(n);
+    nv.cubin(prog, job.cubin.data());
     nv.destroy(&prog);
+    return true;
+}
+
+void *worker(void *) {
+    std::unique_lock<std::mutex> lock(g_mu);
+    for (;;) {
+        g_cv.wait(lock, [] { return g_stop || !g_queue.empty(); });
+        if (g_stop) return nullptr;
+        std::shared_ptr<Job> job = g_queue.front();
+        g_queue.pop_front();
+        lock.unlock();
+        const bool ok = compile_cubin(*job);
+        lock.lock();
+        job->state = ok ? 1 : 2;
+        g_cv.notify_all();
+    }
+}
+
+// Stop the workers: queued compiles are dropped, an in-flight one finishes,
+// then the threads are joined.  Called by the Python layer's atexit hook
+// (qs_jit_shutdown) before interpreter and library teardown: a compile
+// running while libraries are torn down crashes, and joining from inside the
+// dynamic loader's exit processing can deadlock with NVRTC's own dlopen.
+void shutdown_workers() {
+    std::vector<pthread_t> ws;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        g_stop = true;
+        for (auto &j : g_queue) j->state = 2;  // dropped
+        g_queue.clear();
+        ws.swap(g_workers);
+    }
+    g_cv.notify_all();
+    for (pthread_t t : ws) pthread_join(t, nullptr);
+}
+
+void ensure_workers() {  // g_mu held; libnvrtc is loaded (jit_enabled)
+    if (!g_workers.empty() || g_stop) return;
+    unsigned n = std::thread::hardware_concurrency();
+    n = n < 2 ? 1 : (n > 16 ? 8 : n / 2);
+    if (const char *w = std::getenv("QSB_JIT_WORKERS")) n = (unsigned)std::max(1, std::atoi(w));
+    // NVRTC recurses deeply on long straight-line programs: give the workers
+    // the stack a main thread would have and then some (virtual reservation)
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, (size_t)512 << 20);
+    for (unsigned i = 0; i < n; ++i) {
+        pthread_t t;
+        if (pthread_create(&t, &attr, worker, nullptr) == 0) g_workers.push_back(t);
+    }
+    pthread_attr_destroy(&attr);
+}
+
+// Load a compiled job into the current device context (g_mu held).
+CUfunction load(const Key &key, Job &job) {
+    const Driver &dr = driver();
     CUmodule mod = nullptr;
     CUfunction fn = nullptr;
-    if (dr.load(&mod, cubin.data()) != CUDA_SUCCESS || dr.get(&fn, mod, "qsb_pass") != CUDA_SUCCESS) {
-        err = "cuModuleLoadData / cuModuleGetFunction failed";
-        return nullptr;
+    if (dr.load(&mod, job.cubin.data()) != CUDA_SUCCESS || dr.get(&fn, mod, "qsb_pass") != CUDA_SUCCESS) {
+        job.err = "cuModuleLoadData / cuModuleGetFunction failed";
+        fn = nullptr;
+    } else if (dr.set_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)job.smem_max) !=
+               CUDA_SUCCESS) {
+        job.err = "cuFuncSetAttribute(max dynamic smem) failed";
+        fn = nullptr;
+    }
+    if (fn) {
+        g_fns[key] = fn;
+    } else {
+        g_failed[key] = true;
+        if (std::getenv("QSB_FUSED_JIT_VERBOSE")) std::fprintf(stderr, "qsb jit: %s\n", job.err.c_str());
     }
     return fn;
 }
 
 }  // namespace
 
-// Should a pass with op-list signature `sig` run as a compiled program?
-// Counts launches per signature (policy 1 compiles from the second).
-bool jit_wanted(int device, uint64_t sig) {
-    const int mode = jit_mode();
-    if (mode <= 0 || !nvrtc().ok || !driver().ok) return false;
-    std::lock_guard<std::mutex> lock(g_mu);
-    const int seen = ++g_seen[{device, sig}];
-    return mode >= 2 || seen >= 2;
-}
+// Should fused passes use compiled programs at all (policy, NVRTC present)?
+bool jit_enabled() { return jit_mode() > 0 && nvrtc().ok && driver().ok; }
 
 // Register bits per thread of compiled programs: QSB_FUSED_JIT_RB (3 or 4)
 // or the caller's choice (5 bits = 4 compute warps per SM measured slower).
@@ -278,29 +355,63 @@ int jit_rb(int dflt) {
     return dflt == 3 ? 3 : 4;
 }
 
-// The compiled program for one planned launch group (compiling it on first
-// use), or nullptr when it cannot be built.
-void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max) {
-    std::string src = generate(p, K, RB);
-    std::lock_guard<std::mutex> lock(g_mu);
-    const auto key = std::make_pair(device, src);
+// The compiled program for one planned launch group, or nullptr while it is
+// still compiling (the compile is queued on first request) or if it cannot be
+// built.  wait = true blocks until the compile has finished (policy 2).
+void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait) {
+    Key key(device, generate(p, K, RB));
+    std::unique_lock<std::mutex> lock(g_mu);
     auto it = g_fns.find(key);
     if (it != g_fns.end()) return (void *)it->second;
     if (g_failed.count(key)) return nullptr;
-    std::string err;
-    CUfunction fn = compile(src, err);
-    if (fn && driver().set_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem_max) !=
-                  CUDA_SUCCESS) {
-        err = "cuFuncSetAttribute(max dynamic smem) failed";
-        fn = nullptr;
+    if (g_stop) return nullptr;  // shutting down: interpreter only
+    std::shared_ptr<Job> &job = g_jobs[key];
+    if (!job) {
+        job = std::make_shared<Job>();
+        job->device = device;
+        job->src = key.second;
+        job->smem_max = smem_max;
+        ensure_workers();
+        g_queue.push_back(job);
+        g_cv.notify_all();
     }
-    if (!fn) {
+    std::shared_ptr<Job> j = job;
+    if (wait) g_cv.wait(lock, [&] { return j->state != 0; });
+    if (j->state == 0) return nullptr;
+    g_jobs.erase(key);
+    if (j->state == 2) {
         g_failed[key] = true;
-        if (std::getenv("QSB_FUSED_JIT_VERBOSE")) std::fprintf(stderr, "qsb jit: %s\n", err.c_str());
+        if (std::getenv("QSB_FUSED_JIT_VERBOSE")) std::fprintf(stderr, "qsb jit: %s\n", j->err.c_str());
         return nullptr;
     }
-    g_fns[key] = fn;
-    return (void *)fn;
+    return (void *)load(key, *j);
+}
+
+// Wait for every queued compile and load the programs of `device` (< 0: the
+// current device's).  Returns the number of programs that failed.
+int jit_sync(int device) {
+    std::unique_lock<std::mutex> lock(g_mu);
+    g_cv.wait(lock, [] {
+        for (auto &kv : g_jobs)
+            if (kv.second->state == 0) return false;
+        return true;
+    });
+    int failed = 0;
+    for (auto it = g_jobs.begin(); it != g_jobs.end();) {
+        if (device >= 0 && it->first.first != device) {
+            ++it;
+            continue;
+        }
+        if (it->second->state == 1) {
+            DeviceGuard guard(it->first.first);
+            if (!load(it->first, *it->second)) ++failed;
+        } else {
+            g_failed[it->first] = true;
+            ++failed;
+        }
+        it = g_jobs.erase(it);
+    }
+    return failed;
 }
 
 int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned grid, unsigned block) {
@@ -316,3 +427,14 @@ int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned gr
 std::string jit_source(const FParams &p, int K, int RB) { return generate(p, K, RB); }
 
 }  // namespace qsb
+
+extern "C" int qs_jit_sync(int device) {
+    const int failed = qsb::jit_sync(device);
+    return failed ? qsb::set_error(QS_ERR_CUDA, std::to_string(failed) + " pass program(s) failed to compile")
+                  : QS_OK;
+}
+
+extern "C" int qs_jit_shutdown(void) {
+    qsb::shutdown_workers();
+    return QS_OK;
+}

@@ -93,6 +93,12 @@ def _plan(num_qubits: int, ops, tile_qubits: int | None) -> list[Pass]:
     return passes
 
 
+def jit_sync(device: int = -1) -> None:
+    """Wait until every queued pass program has compiled and is loaded (the
+    passes run on the interpreter kernel until then, with the same bits)."""
+    N.check(N.lib().qs_jit_sync(int(device)))
+
+
 def run(state, passes: list[Pass]) -> None:
     """Launch the planned passes on a State (asynchronous on its stream)."""
     for p in passes:

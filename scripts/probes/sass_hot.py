@@ -5,7 +5,12 @@ rep = sys.argv[1]; nl = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr = rows[1]; data = rows[2:]
+hdr = rows[1]; data = []
+for r in rows[2:]:  # first kernel only
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 iS = hdr.index("Warp Stall Sampling (All Samples)"); iE = hdr.index("Instructions Executed")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith('stall_') and 'Not Issued' not in h]
 num = lambda x: int(x) if x.isdigit() else 0

@@ -1,9 +1,10 @@
 """Run-time compiled fused-pass programs (csrc/jit.cu) against the interpreter
 kernel and the oracle.
 
-QSB_FUSED_JIT=2 compiles every pass with NVRTC, 0 runs the ahead-of-time
-interpreter; 1 (the default) interprets a pass the first time and compiles it
-when it is launched again.  All three must give the same bits.
+QSB_FUSED_JIT=2 compiles every pass with NVRTC before launching it, 0 runs the
+ahead-of-time interpreter; 1 (the default) queues the compile on a host worker
+and interprets the pass until its program is ready.  All must give the same
+bits.
 """
 
 from __future__ import annotations
@@ -117,9 +118,12 @@ def test_compiled_vs_oracle_all_tile_shapes(K, rb):
     assert same_values(run(circ, a0, 2, K=K, rb=rb), ref)
 
 
-def test_second_launch_policy():
-    """Mode 1: the first launch of a pass is interpreted, the repeat compiled;
-    the register evolves identically either way."""
+def test_background_compile_policy():
+    """Mode 1 (default): a pass's first launches are interpreted while its
+    program compiles on a host worker; after qs_jit_sync the compiled program
+    runs.  The register evolves identically either way."""
+    from paper_1805_00988_b200 import fusion
+
     n = 19
     rng = np.random.default_rng(5)
     a0 = rand_amps(n, rng)
@@ -127,7 +131,9 @@ def test_second_launch_policy():
     with jit(1):
         st = State(n)
         st.set_amplitudes(a0)
-        for _ in range(3):
+        execute(circ, st, fuse=True)
+        fusion.jit_sync()
+        for _ in range(2):
             execute(circ, st, fuse=True)
         got = st.amplitudes()
     with jit(0):
