@@ -228,6 +228,8 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     {
         const char *d = std::getenv("QSB_FUSED_DRY");
         p.dry = d && *d == '1';
+        const char *h = std::getenv("QSB_FUSED_L2HINT");
+        p.l2hint = h && *h == '1';
     }
     int local_of[64];
     for (int q = 0, i = 0; q < n; ++q) {

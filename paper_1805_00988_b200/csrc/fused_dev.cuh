@@ -63,6 +63,7 @@ struct FParams {
     int n, K, nwbits, nstages, nruns, nops;
     int dry;    // QSB_FUSED_DRY=1: move the tiles, skip the math (ring probe)
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
+    int l2hint;  // TMA copies with an L2 evict_first policy
     uint64_t ntiles;
     int qpos[kMaxK];  // global qubit of local bit i
     Run runs[kMaxRuns];
@@ -134,6 +135,30 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, int row, co
     asm volatile(
         "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %1, %1, %1, %2}], [%3];" ::"l"(map),
         "r"(0), "r"(row), "r"(smem_u32(smem_src))
+        : "memory");
+}
+// The same copies with an L2 eviction-priority hint (each amplitude is read
+// and written exactly once per pass: evict_first keeps the stream from
+// displacing anything else in L2).
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_5d_hint(void *smem_dst, const CUtensorMap *map, int row,
+                                                 uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %2, %2, %2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(0), "r"(row), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d_hint(const CUtensorMap *map, int row, const void *smem_src,
+                                                  uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group.L2::cache_hint"
+        " [%0, {%1, %1, %1, %1, %2}], [%3], %4;" ::"l"(map),
+        "r"(0), "r"(row), "r"(smem_u32(smem_src)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
@@ -391,6 +416,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
     if (warp == kCompute / 32) {
         // ---------------- producer warp: TMA loads and stores ----------------
         const CUtensorMap *map = &p.tmap;
+        const uint64_t pol = l2_evict_first();
         constexpr int kCopyF4 = 8 * 33;  // one 5-D box: 8 padded segments
         constexpr uint32_t kBoxBytes = 8u * 66u * 8u;
         uint64_t pending[kNB];
@@ -404,7 +430,10 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                 for (int c = lane; c < p.ncopies; c += 32) {
                     uint32_t row = row0;
                     for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
-                    tma_store_5d(map, (int)row, buf + c * kCopyF4);
+                    if (p.l2hint)
+                        tma_store_5d_hint(map, (int)row, buf + c * kCopyF4, pol);
+                    else
+                        tma_store_5d(map, (int)row, buf + c * kCopyF4);
                 }
                 bulk_commit();
                 bulk_wait_read0();  // buffer b may be overwritten
@@ -418,7 +447,10 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             for (int c = lane; c < p.ncopies; c += 32) {
                 uint32_t row = row0;
                 for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
-                tma_load_5d(buf + c * kCopyF4, map, (int)row, &full[b]);
+                if (p.l2hint)
+                    tma_load_5d_hint(buf + c * kCopyF4, map, (int)row, &full[b], pol);
+                else
+                    tma_load_5d(buf + c * kCopyF4, map, (int)row, &full[b]);
             }
         }
         // drain the last (up to) kNB tiles
@@ -429,7 +461,10 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             for (int c = lane; c < p.ncopies; c += 32) {
                 uint32_t row = row0;
                 for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
-                tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4);
+                if (p.l2hint)
+                    tma_store_5d_hint(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4, pol);
+                else
+                    tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4);
             }
             bulk_commit();
         }
