@@ -464,12 +464,27 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
             double s = start[lo];
             // s below `thr` cannot satisfy fl(s / t) > u; skip the division there
             const double thr = __dmul_rn(__dmul_rn(u, t), 1.0 - 0x1p-50);
-            uint64_t j = 0;
-            for (; j < C; ++j) {
-                s = __dadd_rn(s, prob(p[j]));
-                if (s >= thr && __ddiv_rn(s, t) > u) break;
+            // the same sequential sum, 8 probabilities loaded ahead of the
+            // chain (the loads do not depend on s; a one-at-a-time loop
+            // waits a memory latency per amplitude)
+            uint64_t j = 0, hit = C;
+            for (; j + 8 <= C && hit == C; j += 8) {
+                double pr[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pr[q] = prob(p[j + q]);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (hit == C) {
+                        s = __dadd_rn(s, pr[q]);
+                        if (s >= thr && __ddiv_rn(s, t) > u) hit = j + q;
+                    }
+                }
             }
-            idx = (lo << clog) + j;
+            for (; j < C && hit == C; ++j) {
+                s = __dadd_rn(s, prob(p[j]));
+                if (s >= thr && __ddiv_rn(s, t) > u) hit = j;
+            }
+            idx = (lo << clog) + hit;
         }
         idx += base;
         out[i] = (int64_t)(idx < gdim - 1 ? idx : gdim - 1);
