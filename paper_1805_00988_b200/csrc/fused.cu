@@ -366,10 +366,16 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         std::memset(&st, 0, sizeof st);
         for (int r = 0; r < RB; ++r) st.rf[r] = pl.rb[r];
         {
+            // lanes 0..2 must vary f0..f2 or f5..f7 (bank-conflict-free on the
+            // padded layout); a HIGH stage takes whichever triple its ops test
+            // less (when it does not hold register bits)
             const int low3[3] = {5, 6, 7}, high3[3] = {0, 1, 2};
             const int *first3 = pl.kind == 1 ? low3 : high3;
             bool used[32] = {false};
             for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
+            if (pl.kind == 2 && !used[5] && !used[6] && !used[7] && K - 1 > 7 &&
+                uses[5] + uses[6] + uses[7] < uses[0] + uses[1] + uses[2])
+                first3 = low3;
             for (int l = 0; l < 3; ++l) {
                 st.lf[l] = first3[l];
                 used[first3[l]] = true;

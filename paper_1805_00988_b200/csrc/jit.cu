@@ -360,6 +360,14 @@ int jit_rb(int dflt) {
 // built.  wait = true blocks until the compile has finished (policy 2).
 void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait) {
     Key key(device, generate(p, K, RB));
+    if (const char *dir = std::getenv("QSB_FUSED_JIT_DUMP")) {  // tooling: keep the generated sources
+        static int count = 0;
+        const std::string path = std::string(dir) + "/qsb_pass_" + std::to_string(count++) + ".cu";
+        if (FILE *f = std::fopen(path.c_str(), "w")) {
+            std::fputs(key.second.c_str(), f);
+            std::fclose(f);
+        }
+    }
     std::unique_lock<std::mutex> lock(g_mu);
     auto it = g_fns.find(key);
     if (it != g_fns.end()) return (void *)it->second;
