@@ -636,6 +636,34 @@ def run_extras(st, stream, n, cpu=True):
         res["config1_hlayer20_probs"]["probabilities_bit_identical"] = bool(p.tobytes() == probs.tobytes())
     s20.close()
 
+    # launch-bound small registers: QFT(16) as 136 separate sweeps, launched
+    # from Python one by one vs recorded once into a CUDA graph and replayed
+    from paper_1805_00988_b200 import execute
+
+    s16 = State(16)
+    s16_stream = torch.cuda.ExternalStream(s16.stream())
+    q16 = build_qft(16)
+    execute(q16, s16, fuse=False)
+    s16.flush()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        execute(q16, s16, fuse=False)
+    s16.flush()
+    direct_ms = (time.perf_counter() - t0) * 1e3 / 10
+    with s16.record() as rec:
+        execute(q16, s16, fuse=False)
+    rec.graph.replay(1)
+    s16.flush()
+    t0 = time.perf_counter()
+    rec.graph.replay(10)
+    s16.flush()
+    graph_ms = (time.perf_counter() - t0) * 1e3 / 10
+    rec.graph.close()
+    s16.close()
+    res["graph_qft16_unfused"] = {"gates": q16.gate_count(), "direct_ms": direct_ms, "graph_replay_ms": graph_ms,
+                                  "note": "host wall clock per circuit, 10 reps; direct = one ctypes call + "
+                                          "launch per gate, graph = State.record() once, Graph.replay()"}
+
     # measure path on the 30-qubit register (after the fused layers above it
     # holds a generic state): exact sampling chain (M1-M6, device-only) and
     # probabilities streamed to a host array

@@ -189,6 +189,18 @@ int qs_cdf_extend(qs_state *s, double start, double *end);
 int qs_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
                     uint64_t index_base, uint64_t global_dim, int is_last, int64_t *out);
 
+/* ---- CUDA graphs: record a gate sequence once, replay it --------------------- */
+/* Between qs_begin_capture and qs_end_capture, the asynchronous calls on the
+ * handle (gates, fused passes, reset, uploads) are recorded instead of run;
+ * qs_graph_launch replays them as one graph launch on the same handle (the
+ * recording addresses the capturing handle's buffer).  Getters synchronise and fail while
+ * recording.  For launch-bound (small) registers and repeated circuits. */
+typedef struct qs_graph qs_graph;
+int qs_begin_capture(qs_state *s);
+int qs_end_capture(qs_state *s, qs_graph **out);
+int qs_graph_launch(qs_state *s, qs_graph *g);
+int qs_graph_destroy(qs_graph *g);
+
 /* ---- global-qubit gates over peer memory (sharded registers) --------------- */
 /* cudaIpc handle (64 bytes) of the register's device buffer, and mapping a
  * partner process's handle into this process on `device` (NVLink P2P). */

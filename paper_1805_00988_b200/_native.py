@@ -35,7 +35,7 @@ EXPORTS = (
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
     "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_jit_sync",
-    "qs_jit_shutdown",
+    "qs_jit_shutdown", "qs_begin_capture", "qs_end_capture", "qs_graph_launch", "qs_graph_destroy",
 )
 
 
@@ -110,6 +110,10 @@ def _declare(L):
         "qs_apply_gate_peer": ([vp, vp, i32, u64, f32p], i32),
         "qs_jit_sync": ([i32], i32),
         "qs_jit_shutdown": ([], i32),
+        "qs_begin_capture": ([vp], i32),
+        "qs_end_capture": ([vp, ctypes.POINTER(vp)], i32),
+        "qs_graph_launch": ([vp, vp], i32),
+        "qs_graph_destroy": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -58,6 +58,7 @@ namespace qsb {
 bool jit_enabled();
 int jit_rb(int dflt);
 void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait);
+void *jit_lookup(int device, const FParams &p, int K, int RB);
 int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned grid, unsigned block);
 
 namespace {
@@ -537,9 +538,12 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
     uint64_t grid = (uint64_t)s->num_sms * (uint64_t)ctas_per_sm(K);
     if (grid > (1ull << (n - K))) grid = 1ull << (n - K);
+    cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s->stream, &capturing);
+    const bool recording = capturing != cudaStreamCaptureStatusNone;  // CUDA graph: no compiles / loads
     if (jit_enabled()) {
         const char *jm = std::getenv("QSB_FUSED_JIT");
-        const bool wait = jm && std::atoi(jm) >= 2;
+        const bool wait = jm && std::atoi(jm) >= 2 && !recording;
         // register bits per thread: 3 (twice the warps, shorter per-op bodies)
         // for phase-dominated passes, 4 otherwise (QSB_FUSED_JIT_RB overrides)
         int nphase = 0;
@@ -549,7 +553,8 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         if (plan_pass(s, tile_mask, ops, nops, jrb, groups) == QS_OK) {
             std::vector<void *> fns;
             for (const FParams &g : groups) {
-                void *fn = jit_get(s->device, g, K, jrb, bufs + kMaxOps * sizeof(FOp), wait);
+                void *fn = recording ? jit_lookup(s->device, g, K, jrb)
+                                     : jit_get(s->device, g, K, jrb, bufs + kMaxOps * sizeof(FOp), wait);
                 if (!fn && wait) break;
                 fns.push_back(fn);
             }

@@ -395,6 +395,15 @@ void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool
     return (void *)load(key, *j);
 }
 
+// An already loaded program, without queueing or loading anything (used while
+// the stream is being recorded into a CUDA graph).
+void *jit_lookup(int device, const FParams &p, int K, int RB) {
+    Key key(device, generate(p, K, RB));
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_fns.find(key);
+    return it == g_fns.end() ? nullptr : (void *)it->second;
+}
+
 // Wait for every queued compile and load the programs of `device` (< 0: the
 // current device's).  Returns the number of programs that failed.
 int jit_sync(int device) {

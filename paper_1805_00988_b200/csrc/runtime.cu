@@ -485,3 +485,65 @@ int qs_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, d
 }
 
 }  // extern "C"
+
+// ---- CUDA graphs: record a run of gate launches once, replay it -------------
+// For launch-bound registers (small n, many gates) a recorded gate sequence
+// replays as one graph launch.  Only asynchronous calls may be recorded: gate,
+// fused-pass, reset and amplitude-upload calls; getters (which synchronise)
+// fail while recording.
+struct qs_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int device = 0;
+};
+
+extern "C" {
+
+int qs_begin_capture(qs_state *s) {
+    CHECK_HANDLE(s);
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    return QS_OK;
+}
+
+int qs_end_capture(qs_state *s, qs_graph **out) {
+    CHECK_HANDLE(s);
+    if (!out) return set_error(QS_ERR_NULL, "null output pointer");
+    *out = nullptr;
+    DeviceGuard guard(s->device);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(s->stream, &g);
+    cudaGetLastError();  // a call that broke the recording must not poison later checks
+    if (ec != cudaSuccess) return cuda_fail(ec, "cudaStreamEndCapture");
+    qs_graph *h = new qs_graph();
+    h->graph = g;
+    h->device = s->device;
+    cudaError_t e = cudaGraphInstantiate(&h->exec, g, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        delete h;
+        return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    *out = h;
+    return QS_OK;
+}
+
+int qs_graph_launch(qs_state *s, qs_graph *g) {
+    CHECK_HANDLE(s);
+    if (!g) return set_error(QS_ERR_NULL, "null graph");
+    if (g->device != s->device) return set_error(QS_ERR_VALUE, "graph was recorded on another device");
+    DeviceGuard guard(s->device);
+    QS_CUDA(cudaGraphLaunch(g->exec, s->stream));
+    return QS_OK;
+}
+
+int qs_graph_destroy(qs_graph *g) {
+    if (!g) return QS_OK;
+    DeviceGuard guard(g->device);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return QS_OK;
+}
+
+}  // extern "C"

@@ -36,6 +36,51 @@ class _Queue:
         self._state.flush()
 
 
+class Graph:
+    """A recorded gate sequence (CUDA graph) of one State; replay() runs it
+    again as a single graph launch (qs_graph_launch)."""
+
+    def __init__(self, state: "State", handle: ctypes.c_void_p):
+        self._state = state
+        self._h = handle
+
+    def replay(self, times: int = 1) -> "State":
+        for _ in range(int(times)):
+            N.check(N.lib().qs_graph_launch(self._state.handle, self._h))
+        return self._state
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            N.lib().qs_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Recording:
+    def __init__(self, state: "State"):
+        self._state = state
+        self.graph: Graph | None = None
+
+    def __enter__(self):
+        N.check(N.lib().qs_begin_capture(self._state.handle))
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        h = ctypes.c_void_p()
+        rc = N.lib().qs_end_capture(self._state.handle, ctypes.byref(h))
+        if exc_type is None:
+            N.check(rc)
+            self.graph = Graph(self._state, h)
+        elif h.value:
+            N.lib().qs_graph_destroy(h)
+        return False
+
+
 class _Backend:
     """``state.backend.queue.finish()`` compatibility (PAPER.md:677)."""
 
@@ -163,6 +208,18 @@ class State:
         N.check(fn(self.handle, tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                    int(tq.size), ops.ctypes.data, int(ops.size)))
         return self
+
+    def record(self) -> "_Recording":
+        """Record the gate launches of a block into a CUDA graph instead of running them:
+
+            with st.record() as rec:
+                execute(circuit, st)
+            rec.graph.replay(100)
+
+        Only asynchronous calls (gates, fused passes, reset, uploads) may be
+        recorded; fused passes whose compiled program is not loaded yet are
+        recorded on the interpreter kernel (same bits)."""
+        return _Recording(self)
 
     def swap_qubits(self, q1: int, q2: int) -> "State":
         N.check(N.lib().qs_swap_qubits(self.handle, int(q1), int(q2)))

@@ -538,3 +538,35 @@ class TestLargeRegisters:
         got = np.array([st.amplitude(int(k)) for k in ks[:200]])
         want = np.exp(2j * np.pi * ((ks[:200] * rev) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
         assert np.max(np.abs(got - want)) < 1e-4 * abs(want[0])
+
+
+class TestGraphs:
+    """Recorded gate sequences (CUDA graphs, qs_begin_capture / qs_graph_launch)
+    replay with the same bits as running the gates again."""
+
+    @pytest.mark.parametrize("n,fuse", [(8, True), (12, False), (16, True), (16, False)])
+    def test_replay_equals_rerun(self, n, fuse):
+        rng = np.random.default_rng(4000 + n)
+        a0 = rand_amps(n, rng)
+        circ = Circuit(n, build_hadamard_layer(n).instructions + random_circuit(n, 40, rng).instructions
+                       + build_qft(n).instructions)
+        ref = load(n, a0)
+        for _ in range(3):
+            execute(circ, ref, fuse=fuse)
+        st = load(n, a0)
+        execute(circ, st, fuse=fuse)  # first run (queues pass programs)
+        with st.record() as rec:
+            execute(circ, st, fuse=fuse)
+        rec.graph.replay(1)  # the recorded block has not run yet: this is run 2
+        rec.graph.replay(1)
+        assert same_values(st.amplitudes(), ref.amplitudes())
+        rec.graph.close()
+
+    def test_getters_fail_while_recording(self):
+        st = State(6)
+        with pytest.raises(Exception):
+            with st.record():
+                st.h(0)
+                st.amplitudes()
+        st.h(1)  # the handle is usable again
+        assert st.amplitudes().shape == (64,)
