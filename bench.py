@@ -538,7 +538,19 @@ def run_config5(st_main, eng_main, local, world):
         eng_main.state.close()
         N.lib().qs_release_cached(-1)
         torch.cuda.synchronize(local)
-        st = ShardedState.distributed(n, device=local)
+        # a 36-qubit register on 4 GPUs is a 128 GiB shard: above the default
+        # 75%-of-free budget, so budget all but 6 GiB of the free memory
+        free_b, _ = torch.cuda.mem_get_info(local)
+        st, why = None, ""
+        try:
+            st = ShardedState.distributed(n, device=local, memory_budget=max(1, free_b - (6 << 30)))
+        except Exception as exc:  # noqa: BLE001
+            why = f"{type(exc).__name__}: {exc}"
+        ok = torch.tensor([1 if st is not None else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank allocated, or none proceeds
+        if int(ok.item()) != 1:
+            out["error"] = "allocation failed on a rank" + (f": {why}" if why else "")
+            return out
         eng = st.engines[0]
         stream = torch.cuda.ExternalStream(eng.state.stream(), device=torch.device("cuda", local))
         torch.cuda.synchronize(local)

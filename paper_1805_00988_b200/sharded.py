@@ -391,7 +391,7 @@ class ShardedState:
     # ---- constructors ------------------------------------------------------
     @classmethod
     def distributed(cls, num_qubits: int, group=None, device: int | None = None, engine_factory=None,
-                    peer_gates: bool | None = None):
+                    peer_gates: bool | None = None, memory_budget: int | None = None):
         import torch.distributed as dist
 
         tr = DistTransport(group)
@@ -401,7 +401,7 @@ class ShardedState:
             import torch
 
             dev = torch.cuda.current_device() if device is None else device
-            eng = CudaEngine(L, dev)
+            eng = CudaEngine(L, dev, memory_budget=memory_budget)
         else:
             eng = engine_factory(L)
         st = cls(num_qubits, [eng], tr, [tr.rank], tr.world, peer_gates=peer_gates)
