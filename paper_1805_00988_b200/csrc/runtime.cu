@@ -502,7 +502,9 @@ extern "C" {
 int qs_begin_capture(qs_state *s) {
     CHECK_HANDLE(s);
     DeviceGuard guard(s->device);
-    QS_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    // relaxed: a handle destroyed elsewhere in the recording thread (cudaFree
+    // of its buffer) must not invalidate the recording
+    QS_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed));
     return QS_OK;
 }
 

@@ -67,12 +67,21 @@ class _Recording:
         self.graph: Graph | None = None
 
     def __enter__(self):
+        import gc
+
+        # no garbage-collected State may free its buffer mid-recording
+        self._gc = gc.isenabled()
+        gc.disable()
         N.check(N.lib().qs_begin_capture(self._state.handle))
         return self
 
     def __exit__(self, exc_type, exc, tb):
+        import gc
+
         h = ctypes.c_void_p()
         rc = N.lib().qs_end_capture(self._state.handle, ctypes.byref(h))
+        if self._gc:
+            gc.enable()
         if exc_type is None:
             N.check(rc)
             self.graph = Graph(self._state, h)
