@@ -59,12 +59,18 @@ def default_tile_qubits(num_qubits: int) -> int:
 
 def plan(num_qubits: int, ops, tile_qubits: int | None = None) -> list[Pass]:
     """Greedy in-order grouping into passes of at most K tile qubits.  Without
-    an explicit K: 12-qubit tiles when they need no more passes than 13-qubit
-    ones (two persistent CTAs per SM fit with K = 12; see fused.cu)."""
+    an explicit K (measured on B200, scripts/probes/k13rb.sh):
+    phase-dominated op lists (QFT) keep 13-qubit tiles, whose compiled
+    programs then use 3 register bits per thread (16 compute warps); other
+    lists take 12-qubit tiles (two persistent CTAs per SM) unless those need
+    more than 25% more passes."""
     if tile_qubits is None and num_qubits >= 13:
-        p12 = _plan(num_qubits, ops, 12)
         p13 = _plan(num_qubits, ops, 13)
-        return p12 if len(p12) <= len(p13) else p13
+        nphase = sum(1 for op in ops if op[0] == N.QS_OP_PHASE)
+        if 2 * nphase > len(ops):
+            return p13
+        p12 = _plan(num_qubits, ops, 12)
+        return p12 if 4 * len(p12) <= 5 * len(p13) else p13
     return _plan(num_qubits, ops, tile_qubits)
 
 
