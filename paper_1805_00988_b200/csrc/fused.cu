@@ -228,7 +228,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     p.one = 1.0f;
     {
         const char *d = std::getenv("QSB_FUSED_DRY");
-        p.dry = d && *d == '1';
+        p.dry = d && *d >= '1' && *d <= '3' ? *d - '0' : 0;
         const char *h = std::getenv("QSB_FUSED_L2HINT");
         p.l2hint = h && *h == '1';
     }

@@ -61,7 +61,7 @@ struct FParams {
     int ncopies;       // TMA copies per tile (2^(K-9))
     int crow[4];       // row-index bit of copy-index bit i
     int n, K, nwbits, nstages, nruns, nops;
-    int dry;    // QSB_FUSED_DRY=1: move the tiles, skip the math (ring probe)
+    int dry;    // probes (QSB_FUSED_DRY): 1 skip the ops, 2 also the register stages, 3 also the stores
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
     int l2hint;  // TMA copies with an L2 evict_first policy
     uint64_t ntiles;
@@ -427,7 +427,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
                 mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
                 const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
-                for (int c = lane; c < p.ncopies; c += 32) {
+                for (int c = lane; c < (p.dry == 3 ? 0 : p.ncopies); c += 32) {
                     uint32_t row = row0;
                     for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
                     if (p.l2hint)
@@ -479,7 +479,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         float4 *tile = buf0 + b * kBufF4;
         const uint64_t base = tile_base(t, p);
         mbar_wait(&full[b], (i / kNB) & 1);
-        for (int s = 0; s < p.nstages; ++s) {
+        for (int s = 0; s < (p.dry >= 2 ? 0 : p.nstages); ++s) {
             const FStage &st = p.stages[s];
             uint32_t fb = 0;
 #pragma unroll
