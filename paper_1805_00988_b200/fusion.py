@@ -74,22 +74,63 @@ def plan(num_qubits: int, ops, tile_qubits: int | None = None) -> list[Pass]:
     return _plan(num_qubits, ops, tile_qubits)
 
 
-def _plan(num_qubits: int, ops, tile_qubits: int | None) -> list[Pass]:
+def is_permutation(m: np.ndarray) -> bool:
+    """X (b == c == 1, a == d == 0 exactly): with any controls, a basis
+    permutation — it moves amplitudes without arithmetic."""
+    return bool(m[0] == 0 and m[1] == 0 and m[2] == 1 and m[3] == 0 and m[4] == 1 and m[5] == 0
+                and m[6] == 0 and m[7] == 0)
+
+
+def _qubits(op) -> int:
+    kind, t, cm, _ = op
+    return cm | (1 << t)
+
+
+def _plan(num_qubits: int, ops, tile_qubits: int | None, defer: bool = True) -> list[Pass]:
+    """Greedy grouping in circuit order.  One exact reordering is allowed: a
+    permutation op (X / CX / CCX) whose target does not fit the current tile
+    is deferred past later ops that touch none of its qubits — a permutation
+    only relocates amplitudes, so it commutes bit for bit with any gate on
+    disjoint qubits — and lands in the next pass.  Every other op keeps its
+    place relative to every op it shares a qubit with."""
     n = num_qubits
     K = tile_qubits or default_tile_qubits(n)
     if n < 10 or K < 10:
         return [Pass(list(range(n)), list(ops))] if ops else []
+    from collections import deque
+
     base = list(range(min(LOW, n)))
     passes: list[Pass] = []
     cur = Pass(list(base))
-    for op in ops:
+    queue = deque(ops)
+    deferred: list = []
+    dmask = 0  # qubits touched by the deferred ops
+
+    def close():
+        nonlocal cur, deferred, dmask
+        if cur.ops:
+            passes.append(cur)
+        cur = Pass(list(base))
+        queue.extendleft(reversed(deferred))
+        deferred, dmask = [], 0
+
+    while queue or deferred:
+        if not queue:  # only deferred ops left: they start the next pass
+            close()
+            continue
+        op = queue.popleft()
         kind, t = op[0], op[1]
-        if kind == N.QS_OP_PAIR and t not in cur.tile:
-            if len(cur.tile) >= K:
-                passes.append(cur)
-                cur = Pass(list(base))
-            cur.tile.append(t)
-        cur.ops.append(op)
+        fits = kind != N.QS_OP_PAIR or t in cur.tile or len(cur.tile) < K
+        if fits and not (_qubits(op) & dmask):
+            if kind == N.QS_OP_PAIR and t not in cur.tile:
+                cur.tile.append(t)
+            cur.ops.append(op)
+        elif defer and kind == N.QS_OP_PAIR and is_permutation(op[3]) and len(deferred) < 64 and cur.ops:
+            deferred.append(op)
+            dmask |= _qubits(op)
+        else:
+            queue.appendleft(op)
+            close()
     if cur.ops:
         passes.append(cur)
     for p in passes:  # pad the tile to K qubits (extra qubits are free)
