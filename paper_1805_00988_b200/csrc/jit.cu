@@ -440,8 +440,6 @@ int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned gr
     return QS_OK;
 }
 
-// Test / tooling hook: the generated source of the next pass (QSB_FUSED_JIT_DUMP).
-std::string jit_source(const FParams &p, int K, int RB) { return generate(p, K, RB); }
 
 }  // namespace qsb
 
