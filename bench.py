@@ -732,6 +732,34 @@ def run_extras(st, stream, n, cpu=True):
                             "note": "complex128 register (8 GiB), H on every target, 3 reps each, CUDA events"}
     sd.close()
 
+    # the sharded machinery at full size on one GPU: a 31-qubit register as 2
+    # virtual shards of 30 qubits (16 GiB), H on every qubit; the global qubit
+    # goes through a qubit swap (in-process D2D exchange) or the peer-memory
+    # kernel (partner shard in the same HBM standing in for an NVLink peer)
+    from paper_1805_00988_b200.sharded import ShardedState
+    from paper_1805_00988_b200.gates import H as _Hg
+
+    from paper_1805_00988_b200 import _native as _N
+
+    sv = {}
+    for mode, peer in (("swap", False), ("peer", True)):
+        vs = ShardedState.virtual(31, 2, peer_gates=peer)
+        for q in range(31):
+            vs.apply_gate(_Hg, q)
+        vs.synchronize()
+        vs.reset(0)
+        vs.synchronize()
+        t0 = time.perf_counter()
+        for q in range(31):
+            vs.apply_gate(_Hg, q)
+        vs.synchronize()
+        sv[mode] = {"layer_ms": (time.perf_counter() - t0) * 1e3, "swaps": vs.swaps,
+                    "peer_gates": vs.peer_gate_count}
+        del vs
+        _N.lib().qs_release_cached(-1)
+    res["sharded_virtual_31q_2shards"] = {**sv, "note": "H layer over 31 qubits as 2 virtual shards on one "
+                                          "B200 (host wall clock incl. per-gate syncs of the sharded layer)"}
+
     # config 4: 32-qubit layered random H/T/CX circuit, depth 20, fused
     try:
         s32 = State(32)
