@@ -175,8 +175,11 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
     of a trailing SampleMeasure (or None)."""
     if circuit.num_qubits != state.num_qubits:
         raise ValueError("circuit and state widths differ")
-    ops = lower_ops(circuit, double=getattr(state, "is_double", False))
+    double = getattr(state, "is_double", False)
+    ops = lower_ops(circuit, double=double)
     if fuse:
+        if double and tile_qubits is None:
+            tile_qubits = 12  # complex128 tiles: 2^12 amplitudes = 64 KiB
         fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits))
     else:
         for kind, t, cm, m in ops:

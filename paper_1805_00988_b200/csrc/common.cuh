@@ -80,6 +80,15 @@ __device__ __forceinline__ float2 cmul(float2 g, float2 v) {
 
 __device__ __forceinline__ float2 cadd(float2 x, float2 y) { return f2add(x, y); }
 
+// complex128 registers: numpy's complex128 multiply has the same form;
+// explicit __d*_rn keeps nvcc / ptxas from contracting anything else
+__device__ __forceinline__ double2 cmul_d(double2 g, double2 v) {
+    return make_double2(__fma_rn(g.x, v.x, -__dmul_rn(g.y, v.y)), __fma_rn(g.x, v.y, __dmul_rn(g.y, v.x)));
+}
+__device__ __forceinline__ double2 cadd_d(double2 x, double2 y) {
+    return make_double2(__dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
+}
+
 // v_a' = a v_a + b v_b ; v_b' = d v_b + c v_a  (kernel.py:128-129)
 __device__ __forceinline__ void pair_update(const Gate2 &g, float2 &va, float2 &vb) {
     float2 na = cadd(cmul(g.a, va), cmul(g.b, vb));

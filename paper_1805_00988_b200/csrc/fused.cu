@@ -57,8 +57,9 @@ namespace qsb {
 // run-time compiled pass programs (jit.cu)
 bool jit_enabled();
 int jit_rb(int dflt);
-void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait);
-void *jit_lookup(int device, const FParams &p, int K, int RB);
+void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait,
+              const qs_op64 *ops64 = nullptr);
+void *jit_lookup(int device, const FParams &p, int K, int RB, const qs_op64 *ops64 = nullptr);
 int jit_launch(qs_state *s, void *fn, const FParams &p, size_t smem, unsigned grid, unsigned block);
 
 namespace {
@@ -194,9 +195,12 @@ int encode_tile_map(qs_state *s, FParams &p) {
             return set_error(QS_ERR_CUDA, "cuTensorMapEncodeTiled entry point not available");
         encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
     }
-    const cuuint64_t dims[5] = {64, 2, 2, 2, 1ull << (p.n - kLow)};
-    const cuuint64_t strides[4] = {8ull << p.qpos[kLow], 8ull << p.qpos[kLow + 1],
-                                   8ull << p.qpos[kLow + 2], 512ull};
+    // complex64: 64 amplitudes (8 B) per 512-B row; complex128: 32 (16 B);
+    // either way 64 eight-byte elements per row
+    const int low = s->prec == QS_DOUBLE ? 5 : kLow;
+    const uint64_t ab = s->prec == QS_DOUBLE ? 16ull : 8ull;
+    const cuuint64_t dims[5] = {64, 2, 2, 2, 1ull << (p.n - low)};
+    const cuuint64_t strides[4] = {ab << p.qpos[low], ab << p.qpos[low + 1], ab << p.qpos[low + 2], 512ull};
     const cuuint32_t box[5] = {66, 2, 2, 2, 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)s->amps, dims, strides,
@@ -204,8 +208,8 @@ int encode_tile_map(qs_state *s, FParams &p) {
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return set_error(QS_ERR_CUDA, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
-    p.ncopies = 1 << (p.K - kLow - 3);
-    for (int k = 0; k < 4; ++k) p.crow[k] = (kLow + 3 + k < p.K) ? p.qpos[kLow + 3 + k] - kLow : 0;
+    p.ncopies = 1 << (p.K - low - 3);
+    for (int k = 0; k < 4; ++k) p.crow[k] = (low + 3 + k < p.K) ? p.qpos[low + 3 + k] - low : 0;
     return QS_OK;
 }
 
@@ -215,15 +219,21 @@ int encode_tile_map(qs_state *s, FParams &p) {
 // per thread: stage layouts and lowered ops, split into launch groups within
 // the op / stage limits of one kernel parameter block.
 static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops, int RB,
-                     std::vector<FParams> &groups) {
+                     std::vector<FParams> &groups, std::vector<int> *group_offsets = nullptr) {
     const int n = s->num_qubits;
     const int K = __builtin_popcountll(tile_mask);
+    // 16-B units: complex64 packs local qubit 0 inside the unit (f = local - 1,
+    // K - 1 unit bits); complex128 units hold one amplitude (f = local, K bits)
+    const bool dbl = s->prec == QS_DOUBLE;
+    const int FB = dbl ? K : K - 1;
+    auto f_of = [&](int lb) { return dbl ? lb : lb - 1; };
+    auto is_half = [&](int lb) { return !dbl && lb == 0; };
     std::unique_ptr<FParams> holder(new FParams);  // ~28 KB: off the stack
     FParams &p = *holder;
     std::memset(&p, 0, sizeof p);
     p.n = n;
     p.K = K;
-    p.nwbits = K - 6 - RB;
+    p.nwbits = FB - 5 - RB;
     p.ntiles = 1ull << (n - K);
     p.one = 1.0f;
     {
@@ -264,9 +274,9 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     auto need_of = [&](const qs_op &op, int *fbit) -> int {
         if (op.kind != QS_OP_PAIR) return 0;
         const int lb = local_of[op.target];
-        if (lb == 0) return 0;
-        if (lb <= RB) return 1;
-        *fbit = lb - 1;
+        if (is_half(lb)) return 0;
+        if (f_of(lb) < RB) return 1;
+        *fbit = f_of(lb);
         return 2;
     };
     // (1) stage layouts and op ranges: greedy over the PAIR ops in circuit
@@ -298,7 +308,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
                     if (nd == 1) break;
                     if (nd == 2 && std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
                 }
-                for (int f = RB; f < K - 1 && (int)pl.rb.size() < RB; ++f)
+                for (int f = RB; f < FB && (int)pl.rb.size() < RB; ++f)
                     if (std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
                 std::sort(pl.rb.begin(), pl.rb.end());
             } else {
@@ -319,7 +329,8 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         if (op.kind == QS_OP_PHASE) need |= 1ull << op.target;
         uint32_t fb = 0;
         for (int q = 0; q < n; ++q)
-            if (((need >> q) & 1ull) && local_of[q] > 0) fb |= 1u << (local_of[q] - 1);
+            if (((need >> q) & 1ull) && local_of[q] >= 0 && !is_half(local_of[q]))
+                fb |= 1u << f_of(local_of[q]);
         return fb;
     };
     auto in_regs = [&](const Plan &pl, uint32_t fb) -> int {
@@ -361,7 +372,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         int uses[32] = {0};
         for (int j = pl.begin; j < pl.end; ++j) {
             const uint32_t fb = test_fbits(ops[j]);
-            for (int f = 0; f < K - 1; ++f) uses[f] += (fb >> f) & 1u;
+            for (int f = 0; f < FB; ++f) uses[f] += (fb >> f) & 1u;
         }
         FStage st;
         std::memset(&st, 0, sizeof st);
@@ -374,7 +385,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
             const int *first3 = pl.kind == 1 ? low3 : high3;
             bool used[32] = {false};
             for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
-            if (pl.kind == 2 && !used[5] && !used[6] && !used[7] && K - 1 > 7 &&
+            if (pl.kind == 2 && !used[5] && !used[6] && !used[7] && FB > 7 &&
                 uses[5] + uses[6] + uses[7] < uses[0] + uses[1] + uses[2])
                 first3 = low3;
             for (int l = 0; l < 3; ++l) {
@@ -382,7 +393,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
                 used[first3[l]] = true;
             }
             std::vector<int> fr;
-            for (int f = 0; f < K - 1; ++f)
+            for (int f = 0; f < FB; ++f)
                 if (!used[f]) fr.push_back(f);
             std::stable_sort(fr.begin(), fr.end(), [&](int x, int y) { return uses[x] < uses[y]; });
             st.lf[3] = fr[0];
@@ -410,21 +421,21 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
                 const int lb = local_of[q];
                 if (lb < 0)
                     o.ext_need |= 1ull << q;
-                else if (lb == 0)
+                else if (is_half(lb))
                     o.half_need = 1;
-                else if (reg_of[lb - 1] >= 0)
-                    o.reg_need |= 1u << reg_of[lb - 1];
-                else if (lane_of[lb - 1] >= 0)
-                    o.tid_need |= 1u << lane_of[lb - 1];
+                else if (reg_of[f_of(lb)] >= 0)
+                    o.reg_need |= 1u << reg_of[f_of(lb)];
+                else if (lane_of[f_of(lb)] >= 0)
+                    o.tid_need |= 1u << lane_of[f_of(lb)];
                 else
-                    o.tid_need |= 1u << (5 + warp_of[lb - 1]);
+                    o.tid_need |= 1u << (5 + warp_of[f_of(lb)]);
             }
             const int has_need = o.reg_need != 0 || o.half_need != 0;
             if (op.kind == QS_OP_PHASE) {
                 o.variant = kPhaseVariant + (int)o.reg_need * 2 + (o.half_need ? 1 : 0);
             } else {
                 const int lb = local_of[op.target];
-                const int slot = lb == 0 ? -1 : reg_of[lb - 1];
+                const int slot = is_half(lb) ? -1 : reg_of[f_of(lb)];
                 o.variant = ((slot + 1) * 4 + gate_class(op.m)) * 2 + has_need;
             }
             fops.push_back(o);
@@ -460,6 +471,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
             p.stages[k - si].op_end -= off;
         }
         std::memcpy(p.ops, fops.data() + off, (size_t)nop * sizeof(FOp));
+        if (group_offsets) group_offsets->push_back(off);  // FOp k of a group = op off + k
         for (int k = 0; k < p.nstages; ++k) {  // runs of equal variants, within a stage
             const FStage &st = p.stages[k];
             for (int o = st.op_begin; o < st.op_end;) {
@@ -592,6 +604,61 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
             case 12: rc = RB == 4 ? launch_fused_k<12, 4>(s, g) : launch_fused_k<12, 3>(s, g); break;
             default: rc = RB == 4 ? launch_fused_k<13, 4>(s, g) : launch_fused_k<13, 3>(s, g); break;
         }
+        if (rc) return rc;
+    }
+    return QS_OK;
+}
+
+// complex128 registers: a planned pass as a compiled program over 16-B
+// units (one amplitude each, csrc/fused_dev.cuh with V = double2).  Returns
+// QS_OK once launched, 1 when the programs are not ready yet (the caller runs
+// the ops as sweeps, same bits; compiles are queued), or an error code.
+int run_fused_tiles_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops, int nops) {
+    const int n = s->num_qubits;
+    uint64_t tile_mask = 0;
+    for (int i = 0; i < ntile; ++i) {
+        if (tile_qubits[i] < 0 || tile_qubits[i] >= n) return 1;
+        tile_mask |= 1ull << tile_qubits[i];
+    }
+    const int K = __builtin_popcountll(tile_mask);
+    if (n < 13 || K < 10 || K > 12 || (tile_mask & 31ull) != 31ull || !jit_enabled()) return 1;
+    for (int i = 0; i < nops; ++i)
+        if (ops[i].kind == QS_OP_PAIR && !((tile_mask >> ops[i].target) & 1ull)) return 1;
+    std::vector<qs_op> ops32((size_t)nops);
+    int nphase = 0;
+    for (int i = 0; i < nops; ++i) {
+        ops32[i].kind = ops[i].kind;
+        ops32[i].target = ops[i].target;
+        ops32[i].ctrl_mask = ops[i].ctrl_mask;
+        for (int k = 0; k < 8; ++k) ops32[i].m[k] = (float)ops[i].m[k];
+        nphase += ops[i].kind == QS_OP_PHASE;
+    }
+    const int RB = jit_rb(2 * nphase > nops ? 3 : 4);
+    std::vector<FParams> groups;
+    std::vector<int> offs;
+    int rc = plan_pass(s, tile_mask, ops32.data(), nops, RB, groups, &offs);
+    if (rc) return rc;
+    cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s->stream, &capturing);
+    const bool recording = capturing != cudaStreamCaptureStatusNone;
+    const char *jm = std::getenv("QSB_FUSED_JIT");
+    const bool wait = jm && std::atoi(jm) >= 2 && !recording;
+    const size_t bufs = (size_t)kNB * (1u << (K - 5)) * 33u * 16u;
+    std::vector<void *> fns;
+    bool all = true;
+    for (size_t g = 0; g < groups.size(); ++g) {
+        void *f = recording ? jit_lookup(s->device, groups[g], K, RB, ops + offs[g])
+                            : jit_get(s->device, groups[g], K, RB, bufs + kMaxOps * sizeof(FOp), wait, ops + offs[g]);
+        all = all && f;
+        fns.push_back(f);
+    }
+    if (!all) return 1;
+    uint64_t grid = (uint64_t)s->num_sms;
+    if (grid > (1ull << (n - K))) grid = 1ull << (n - K);
+    for (size_t g = 0; g < groups.size(); ++g) {
+        FParams q = groups[g];
+        q.nops = 0;  // the program carries the entries: no op table to stage
+        rc = jit_launch(s, fns[g], q, bufs, (unsigned)grid, (1u << (K - RB)) + 32u);
         if (rc) return rc;
     }
     return QS_OK;

@@ -369,15 +369,56 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// A tile is a padded array of 16-B units: a complex64 register packs two
+// amplitudes per unit (local qubit 0 = the unit's halves, 64 amplitudes per
+// 512-B row), a complex128 register one (32 per row).
+template <class V>
+struct UnitTraits;
+template <>
+struct UnitTraits<float4> {
+    static constexpr int kLowQ = 6;   // local qubits inside one 512-B row
+    static constexpr int kHalf = 1;   // local qubit 0 lives inside the unit
+};
+template <>
+struct UnitTraits<double2> {
+    static constexpr int kLowQ = 5;
+    static constexpr int kHalf = 0;
+};
+
+// complex128 forms for generated programs (generic 2x2, no class shortcuts:
+// the sweep's exact arithmetic, pair_update_d in gates64.cu)
+template <int T, int RNEED, int RB>
+__device__ __forceinline__ void pair_ct_d(const double (&m)[8], double2 (&v)[1 << RB]) {
+    const double2 ga = make_double2(m[0], m[1]), gb = make_double2(m[2], m[3]);
+    const double2 gc = make_double2(m[4], m[5]), gd = make_double2(m[6], m[7]);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (j & (1 << T)) continue;
+        if ((j & RNEED) != RNEED) continue;
+        const int k = j | (1 << T);
+        const double2 a = v[j], b = v[k];
+        v[j] = cadd_d(cmul_d(ga, a), cmul_d(gb, b));
+        v[k] = cadd_d(cmul_d(gd, b), cmul_d(gc, a));
+    }
+}
+
+template <int RNEED, int RB>
+__device__ __forceinline__ void phase_ct_d(double2 d, double2 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j)
+        if ((j & RNEED) == RNEED) v[j] = cmul_d(d, v[j]);
+}
+
 // The kernel body, shared by the ahead-of-time interpreter kernel (Prog =
 // Interp: op table in shared memory, one dispatch per run of ops) and the
 // run-time compiled pass kernels (Prog = a generated straight-line program,
 // fused.cu: JIT).  Everything but the op application is identical, so both
 // give the same bits.
-template <int K, int RB, class Prog>
+template <int K, int RB, class Prog, class V = float4>
 __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FParams &p) {
-    constexpr int kCompute = 1 << (K - 1 - RB);   // compute threads
-    constexpr int kSegs = 1 << (K - kLow);        // 512-B segments per tile
+    constexpr int kLowQ = UnitTraits<V>::kLowQ;
+    constexpr int kCompute = 1 << (K - UnitTraits<V>::kHalf - RB);  // compute threads
+    constexpr int kSegs = 1 << (K - kLowQ);       // 512-B segments per tile
     constexpr int kBufF4 = kSegs * 33;            // padded float4 per buffer
     extern __shared__ __align__(128) float4 smem[];
     float4 *buf0 = smem;
@@ -413,7 +454,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             float4 *buf = buf0 + b * kBufF4;
             if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
                 mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
-                const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
+                const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
                 for (int c = lane; c < (p.dry == 3 ? 0 : p.ncopies); c += 32) {
                     uint32_t row = row0;
                     for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
@@ -430,7 +471,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             pending[b] = base;
             if (lane == 0) mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
             __syncwarp();
-            const uint32_t row0 = (uint32_t)(base >> kLow);
+            const uint32_t row0 = (uint32_t)(base >> kLowQ);
             for (int c = lane; c < p.ncopies; c += 32) {
                 uint32_t row = row0;
                 for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
@@ -444,7 +485,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         for (int k = (i >= kNB ? i - kNB : 0); k < i; ++k) {
             const int b = k % kNB;
             mbar_wait(&done[b], (k / kNB) & 1);
-            const uint32_t row0 = (uint32_t)(pending[b] >> kLow);
+            const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
             for (int c = lane; c < p.ncopies; c += 32) {
                 uint32_t row = row0;
                 for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
@@ -476,14 +517,14 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             uint32_t rs[RB];
 #pragma unroll
             for (int r = 0; r < RB; ++r) rs[r] = padded(1u << st.rf[r]);
-            float4 v[1 << RB];
+            V v[1 << RB];
 #pragma unroll
             for (int j = 0; j < (1 << RB); ++j) {
                 uint32_t a = pb;
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
-                v[j] = tile[a];
+                v[j] = *reinterpret_cast<const V *>(tile + a);
             }
             if (!p.dry) Prog::template run<RB>(s, st, sops, (uint32_t)tid, base, p.one, v);
 #pragma unroll
@@ -492,7 +533,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
-                tile[a] = v[j];
+                *reinterpret_cast<V *>(tile + a) = v[j];
             }
             if (s + 1 < p.nstages) named_sync(1, kCompute);
         }

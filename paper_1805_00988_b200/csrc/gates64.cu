@@ -40,12 +40,6 @@ Gate2d gate_from_d(const double m[8]) {
     return g;
 }
 
-__device__ __forceinline__ double2 cmul_d(double2 g, double2 v) {
-    return make_double2(__fma_rn(g.x, v.x, -__dmul_rn(g.y, v.y)), __fma_rn(g.x, v.y, __dmul_rn(g.y, v.x)));
-}
-__device__ __forceinline__ double2 cadd_d(double2 x, double2 y) {
-    return make_double2(__dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
-}
 __device__ __forceinline__ void pair_update_d(const Gate2d &g, double2 &va, double2 &vb) {
     const double2 na = cadd_d(cmul_d(g.a, va), cmul_d(g.b, vb));
     const double2 nb = cadd_d(cmul_d(g.d, vb), cmul_d(g.c, va));
@@ -342,10 +336,11 @@ int launch_swap_d(qs_state *s, int q1, int q2) {
 }
 
 // Fused pass of a complex128 register: one shared-memory launch per <= 320 ops
-// for n <= 12, otherwise the ops in order through the sweep kernels (the
-// TMA tile pass is complex64-only).  Every op has the sweep arithmetic, so the
+// for n <= 12; otherwise the TMA tile pass as a compiled program (fused.cu:
+// run_fused_tiles_d) when it is ready, else the ops in order through the
+// sweep kernels.  Every op has the sweep arithmetic, so the
 // result is the same as applying the ops one by one.
-int run_fused_d(qs_state *s, const qs_op64 *ops, int nops) {
+int run_fused_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops, int nops) {
     const int n = s->num_qubits;
     for (int i = 0; i < nops; ++i) {
         const qs_op64 &op = ops[i];
@@ -381,6 +376,11 @@ int run_fused_d(qs_state *s, const qs_op64 *ops, int nops) {
             QS_CUDA(cudaGetLastError());
         }
         return QS_OK;
+    }
+    {  // a compiled tile pass (jit.cu) once its program is ready
+        const int rc = run_fused_tiles_d(s, tile_qubits, ntile, ops, nops);
+        if (rc == QS_OK) return QS_OK;
+        if (rc != 1) return rc;
     }
     for (int i = 0; i < nops; ++i) {
         const qs_op64 &op = ops[i];

@@ -70,7 +70,8 @@ int launch_sweep_d(qs_state *s, int target, uint64_t ctrl_mask, const double m[8
 int launch_phase_d(qs_state *s, uint64_t mask, double2 d);
 int launch_swap_d(qs_state *s, int q1, int q2);
 int launch_reset_d(qs_state *s, uint64_t basis);
-int run_fused_d(qs_state *s, const qs_op64 *ops, int nops);
+int run_fused_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops, int nops);
+int run_fused_tiles_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops, int nops);
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
 int run_norm(qs_state *s, double *out);
 int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);

@@ -212,6 +212,71 @@ std::string generate(const FParams &p, int K, int RB) {
     return src;
 }
 
+// complex128 registers: every op straight-line (pair_ct_d / phase_ct_d) with
+// its fp64 entries as literals from the caller's qs_op64 list (FOp k of the
+// group is op `first + k`).
+void hexd(std::string &out, double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, 8);
+    char buf[48];
+    std::snprintf(buf, sizeof buf, "__longlong_as_double(0x%016llxll)", (unsigned long long)b);
+    out += buf;
+}
+
+std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
+    std::string src;
+    src.reserve(8192 + (size_t)p.nops * 400);
+    src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
+           "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *, uint32_t tid,\n"
+           "      uint64_t base, float, double2 (&v)[1 << RB]) {\n    switch (s) {\n";
+    char buf[256];
+    for (int k = 0; k < p.nstages; ++k) {
+        const FStage &st = p.stages[k];
+        std::snprintf(buf, sizeof buf, "    case %d: {\n", k);
+        src += buf;
+        for (int o = st.op_begin; o < st.op_end; ++o) {
+            const FOp &op = p.ops[o];
+            const qs_op64 &g = ops64[o];
+            std::string test;
+            if (op.tid_need) {
+                std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need, op.tid_need);
+                test += buf;
+            }
+            if (op.ext_need) {
+                std::snprintf(buf, sizeof buf, "%s(base & 0x%llxull) == 0x%llxull", test.empty() ? "" : " && ",
+                              (unsigned long long)op.ext_need, (unsigned long long)op.ext_need);
+                test += buf;
+            }
+            src += test.empty() ? "      {" : "      if (" + test + ") {";
+            if (op.variant >= kPhaseVariant) {
+                std::snprintf(buf, sizeof buf, " phase_ct_d<%u, RB>(make_double2(", op.reg_need);
+                src += buf;
+                hexd(src, g.m[6]);
+                src += ", ";
+                hexd(src, g.m[7]);
+                src += "), v); }\n";
+            } else {
+                const int slot = (op.variant / 2) / 4 - 1;
+                src += " const double m[8] = {";
+                for (int i = 0; i < 8; ++i) {
+                    if (i) src += ", ";
+                    hexd(src, g.m[i]);
+                }
+                std::snprintf(buf, sizeof buf, "}; pair_ct_d<%d, %u, RB>(m, v); }\n", slot, op.reg_need);
+                src += buf;
+            }
+        }
+        src += "    } break;\n";
+    }
+    std::snprintf(buf, sizeof buf,
+                  "    default: break;\n    }\n  }\n};\n"
+                  "extern \"C\" __global__ void __maxnreg__(%d) qsb_pass(float4 *__restrict__ amps,\n"
+                  "    const __grid_constant__ FParams p) {\n  fused_body<%d, %d, GenProg, double2>(amps, p);\n}\n",
+                  RB == 4 ? 168 : 96, K, RB);
+    src += buf;
+    return src;
+}
+
 // ---- compile service ------------------------------------------------------------
 // NVRTC runs on a small pool of host worker threads; a finished cubin is
 // loaded into the device context by the next launching thread that asks for
@@ -358,8 +423,9 @@ int jit_rb(int dflt) {
 // The compiled program for one planned launch group, or nullptr while it is
 // still compiling (the compile is queued on first request) or if it cannot be
 // built.  wait = true blocks until the compile has finished (policy 2).
-void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait) {
-    Key key(device, generate(p, K, RB));
+void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait,
+              const qs_op64 *ops64) {
+    Key key(device, ops64 ? generate_d(p, K, RB, ops64) : generate(p, K, RB));
     if (const char *dir = std::getenv("QSB_FUSED_JIT_DUMP")) {  // tooling: keep the generated sources
         static int count = 0;
         const std::string path = std::string(dir) + "/qsb_pass_" + std::to_string(count++) + ".cu";
@@ -397,8 +463,8 @@ void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool
 
 // An already loaded program, without queueing or loading anything (used while
 // the stream is being recorded into a CUDA graph).
-void *jit_lookup(int device, const FParams &p, int K, int RB) {
-    Key key(device, generate(p, K, RB));
+void *jit_lookup(int device, const FParams &p, int K, int RB, const qs_op64 *ops64) {
+    Key key(device, ops64 ? generate_d(p, K, RB, ops64) : generate(p, K, RB));
     std::lock_guard<std::mutex> lock(g_mu);
     auto it = g_fns.find(key);
     return it == g_fns.end() ? nullptr : (void *)it->second;

@@ -331,7 +331,7 @@ int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_
             wide[i].ctrl_mask = ops[i].ctrl_mask;
             for (int k = 0; k < 8; ++k) wide[i].m[k] = (double)ops[i].m[k];
         }
-        return run_fused_d(s, wide.data(), nops);
+        return run_fused_d(s, tile_qubits, ntile, wide.data(), nops);
     }
     return run_fused(s, tile_qubits, ntile, ops, nops);
 }
@@ -342,7 +342,7 @@ int qs_apply_fused_f64(qs_state *s, const int32_t *tile_qubits, int ntile, const
     if (nops == 0) return QS_OK;
     if (!ops || !tile_qubits) return set_error(QS_ERR_NULL, "null op list or tile qubit list");
     DeviceGuard guard(s->device);
-    if (s->prec == QS_DOUBLE) return run_fused_d(s, ops, nops);
+    if (s->prec == QS_DOUBLE) return run_fused_d(s, tile_qubits, ntile, ops, nops);
     std::vector<qs_op> narrow((size_t)nops);
     for (int i = 0; i < nops; ++i) {
         narrow[i].kind = ops[i].kind;

@@ -237,3 +237,47 @@ class TestPairsimShimDouble:
         assert abs(ps.norm_squared(sv) - 1.0) < 1e-10
         p = ps.probabilities(sv)
         assert np.max(np.abs(p - np.abs(dense) ** 2)) < 1e-10
+
+
+class TestFusedTilesDouble:
+    """complex128 fused passes as compiled TMA tile programs (fused_dev.cuh
+    with 16-B one-amplitude units) against the sweeps, bit for bit."""
+
+    @pytest.mark.parametrize("n,kind", [(14, "mixed"), (17, "qft"), (20, "layered"), (22, "hlayer")])
+    def test_compiled_tiles_equal_sweeps(self, n, kind):
+        import os
+
+        from paper_1805_00988_b200 import build_hadamard_layer, layered_random_circuit
+
+        rng = np.random.default_rng(1300 + n)
+        a0 = rand_amps(n, rng)
+        if kind == "mixed":
+            ins = []
+            for _ in range(80):
+                t = int(rng.integers(n))
+                others = [q for q in range(n) if q != t]
+                r = rng.random()
+                if r < 0.5:
+                    ins.append(Apply(gate_mix(rng), t))
+                elif r < 0.85:
+                    ins.append(ControlledApply(gate_mix(rng), int(rng.choice(others)), t))
+                else:
+                    c1, c2 = (int(x) for x in rng.choice(others, 2, replace=False))
+                    ins.append(ControlledControlledApply(gate_mix(rng), c1, c2, t))
+            circ = Circuit(n, tuple(ins))
+        else:
+            circ = {"qft": build_qft(n), "layered": layered_random_circuit(n, 3, seed=n),
+                    "hlayer": build_hadamard_layer(n)}[kind]
+        ref = load(n, a0)
+        execute(circ, ref, fuse=False)
+        old = os.environ.get("QSB_FUSED_JIT")
+        os.environ["QSB_FUSED_JIT"] = "2"
+        try:
+            st = load(n, a0)
+            execute(circ, st, fuse=True)
+        finally:
+            if old is None:
+                os.environ.pop("QSB_FUSED_JIT", None)
+            else:
+                os.environ["QSB_FUSED_JIT"] = old
+        assert same_values(st.amplitudes(), ref.amplitudes())
