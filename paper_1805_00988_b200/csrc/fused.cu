@@ -236,6 +236,12 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     p.nwbits = FB - 5 - RB;
     p.ntiles = 1ull << (n - K);
     p.one = 1.0f;
+    if (!s->tile_ctr) {  // first fused pass of this handle: the scheduler's counter
+        DeviceGuard guard(s->device);
+        QS_CUDA(cudaMalloc(&s->tile_ctr, 256));
+        QS_CUDA(cudaMemsetAsync(s->tile_ctr, 0, 256, s->stream));
+    }
+    p.tile_ctr = s->tile_ctr;
     {
         const char *d = std::getenv("QSB_FUSED_DRY");
         p.dry = d && *d >= '1' && *d <= '3' ? *d - '0' : 0;
@@ -486,7 +492,13 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
                 std::fprintf(f, "pass K=%d RB=%d nstages=%d nops=%d\n", K, RB, p.nstages, p.nops);
                 for (int k = 0; k < p.nstages; ++k) {
                     const FStage &st = p.stages[k];
-                    std::fprintf(f, "stage %d %d %d\n", k, st.op_begin, st.op_end);
+                    std::fprintf(f, "stage %d %d %d rf", k, st.op_begin, st.op_end);
+                    for (int r = 0; r < RB; ++r) std::fprintf(f, " %d", st.rf[r]);
+                    std::fprintf(f, " lf");
+                    for (int l = 0; l < 5; ++l) std::fprintf(f, " %d", st.lf[l]);
+                    std::fprintf(f, " wf");
+                    for (int w = 0; w < p.nwbits; ++w) std::fprintf(f, " %d", st.wf[w]);
+                    std::fprintf(f, "\n");
                     for (int o = st.op_begin; o < st.op_end; ++o)
                         std::fprintf(f, "op %d %d %u %u %u %llu\n", o, p.ops[o].variant, p.ops[o].reg_need,
                                      p.ops[o].tid_need, p.ops[o].half_need,

@@ -65,6 +65,9 @@ struct FParams {
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
     int l2hint;  // TMA copies with an L2 evict_first policy
     uint64_t ntiles;
+    // Dynamic tile scheduler: the producers take tiles from this counter
+    // (zero at launch; the last CTA to find it exhausted zeroes it again).
+    unsigned long long *tile_ctr;
     int qpos[kMaxK];  // global qubit of local bit i
     Run runs[kMaxRuns];
     FStage stages[kMaxStages];
@@ -173,6 +176,17 @@ __device__ __forceinline__ float2 csub(float2 x, float2 y, float one) {
     return f2fma(y, make_float2(-one, -one), x);
 }
 
+// A diagonal op inside a conditional block (a lane, warp or tile test):
+// scalar FMUL / FFMA (the same four roundings per amplitude as cmul).
+// ptxas writes a packed FFMA2 result into its addend's register pair, so
+// after a branch every packed-updated pair needs two MOVs back into its home
+// registers; the scalar form updates the amplitude in place (no copies).
+__device__ __forceinline__ void cmul_s(float2 d, float &re, float &im) {
+    const float t0 = __fmul_rn(-d.y, im), t1 = __fmul_rn(d.y, re);
+    re = __fmaf_rn(d.x, re, t0);
+    im = __fmaf_rn(d.x, im, t1);
+}
+
 template <int CLS>
 __device__ __forceinline__ void pair_cls(const float *m, float one, float2 &va, float2 &vb) {
     if (CLS == kCplx) {
@@ -233,16 +247,15 @@ __device__ __forceinline__ void apply_pair(const FOp &op, float4 (&v)[1 << RB]) 
 
 // Diagonal op: multiply the registers whose index has every bit of RNEED set
 // (compile-time pattern) by d; ODD: only the odd half (phase bit on local 0).
+// (Always under a per-op test: the scalar in-place form, see phase_cs.)
 template <int RNEED, bool ODD, int RB>
 __device__ __forceinline__ void apply_phase(const FOp &op, float4 (&v)[1 << RB]) {
     const float2 d = make_float2(op.m[6], op.m[7]);
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
         if ((j & RNEED) != RNEED) continue;
-        float2 a = lo2(v[j]), b = hi2(v[j]);
-        if (!ODD) a = cmul(d, a);
-        b = cmul(d, b);
-        v[j] = mk4(a, b);
+        if (!ODD) cmul_s(d, v[j].x, v[j].y);
+        cmul_s(d, v[j].z, v[j].w);
     }
 }
 
@@ -353,6 +366,17 @@ __device__ __forceinline__ void phase_ct(float2 d, float4 (&v)[1 << RB]) {
     }
 }
 
+// The same diagonal op inside a conditional block (cmul_s, above).
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void phase_cs(float2 d, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if ((j & RNEED) != RNEED) continue;
+        if (!ODD) cmul_s(d, v[j].x, v[j].y);
+        cmul_s(d, v[j].z, v[j].w);
+    }
+}
+
 __device__ __forceinline__ uint64_t tile_base(uint64_t t, const FParams &p) {
     uint64_t r = 0;
     for (int i = 0; i < p.nruns; ++i)
@@ -424,6 +448,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
     float4 *buf0 = smem;
     FOp *sops = (FOp *)(smem + kNB * kBufF4);
     __shared__ uint64_t full[kNB], done[kNB];
+    __shared__ unsigned long long tile_id[kNB];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -443,13 +468,20 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
 
     if (warp == kCompute / 32) {
         // ---------------- producer warp: TMA loads and stores ----------------
+        // Tiles are handed out dynamically (one atomic per tile): the ops'
+        // tile-uniform tests (controls / phase bits outside the tile) make
+        // tiles unequal in work, and a static stride gives some CTAs only
+        // heavy tiles (e.g. tile-index bits 0-1 are constant per CTA under a
+        // stride of 148).  The tile index travels to the compute warps with
+        // the buffer (tile_id[b], published by the full-barrier arrival);
+        // ~0 ends the loop.
         const CUtensorMap *map = &p.tmap;
         const uint64_t pol = l2_evict_first();
         constexpr int kCopyF4 = 8 * 33;  // one 5-D box: 8 padded segments
         constexpr uint32_t kBoxBytes = 8u * 66u * 8u;
         uint64_t pending[kNB];
         int i = 0;
-        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+        for (;; ++i) {
             const int b = i % kNB;
             float4 *buf = buf0 + b * kBufF4;
             if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
@@ -467,9 +499,25 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                 bulk_wait_read0();  // buffer b may be overwritten
                 __syncwarp();
             }
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(p.tile_ctr, 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= p.ntiles) {
+                if (lane == 0) {
+                    // every CTA draws exactly one index >= ntiles; the largest
+                    // is the counter's last use in this launch
+                    if (t == p.ntiles + gridDim.x - 1) *p.tile_ctr = 0ull;
+                    tile_id[b] = ~0ull;
+                    mbar_arrive(&full[b]);
+                }
+                break;
+            }
             const uint64_t base = tile_base(t, p);
             pending[b] = base;
-            if (lane == 0) mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
+            if (lane == 0) {
+                tile_id[b] = t;
+                mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
+            }
             __syncwarp();
             const uint32_t row0 = (uint32_t)(base >> kLowQ);
             for (int c = lane; c < p.ncopies; c += 32) {
@@ -481,12 +529,12 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                     tma_load_5d(buf + c * kCopyF4, map, (int)row, &full[b]);
             }
         }
-        // drain the last (up to) kNB tiles
-        for (int k = (i >= kNB ? i - kNB : 0); k < i; ++k) {
+        // drain the last (up to) kNB - 1 tiles (tile i - kNB was stored above)
+        for (int k = (i >= kNB ? i - kNB + 1 : 0); k < i; ++k) {
             const int b = k % kNB;
             mbar_wait(&done[b], (k / kNB) & 1);
             const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
-            for (int c = lane; c < p.ncopies; c += 32) {
+            for (int c = lane; c < (p.dry == 3 ? 0 : p.ncopies); c += 32) {
                 uint32_t row = row0;
                 for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
                 if (p.l2hint)
@@ -501,12 +549,13 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
     }
 
     // -------------------- compute warps: register stages --------------------
-    int i = 0;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+    for (int i = 0;; ++i) {
         const int b = i % kNB;
         float4 *tile = buf0 + b * kBufF4;
-        const uint64_t base = tile_base(t, p);
         mbar_wait(&full[b], (i / kNB) & 1);
+        const uint64_t t = tile_id[b];
+        if (t == ~0ull) break;
+        const uint64_t base = tile_base(t, p);
         for (int s = 0; s < (p.dry >= 2 ? 0 : p.nstages); ++s) {
             const FStage &st = p.stages[s];
             uint32_t fb = 0;

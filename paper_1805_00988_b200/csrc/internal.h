@@ -23,6 +23,8 @@ struct qs_state {
     // fused-pass op buffer (device copy of qs_op arrays)
     void *ops_dev;
     size_t ops_bytes;
+    // fused-pass tile scheduler counter (lazily allocated, zero between launches)
+    unsigned long long *tile_ctr;
 };
 
 namespace qsb {

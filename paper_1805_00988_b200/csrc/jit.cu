@@ -130,6 +130,12 @@ void hexf(std::string &out, float x) {
 }
 
 std::string generate(const FParams &p, int K, int RB) {
+    // diagonal ops inside a test: 1 (default) scalar phase_cs, 0 packed
+    // phase_ct, 2 scalar everywhere (QSB_JIT_PHASE, for measurements)
+    int phase_mode = 1;
+    if (const char *e = std::getenv("QSB_JIT_PHASE")) phase_mode = std::atoi(e);
+    int loop_run = kJitLoopRun;
+    if (const char *e = std::getenv("QSB_JIT_LOOP_RUN")) loop_run = std::atoi(e);
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 200);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
@@ -152,7 +158,7 @@ std::string generate(const FParams &p, int K, int RB) {
                 ++e;
             // registers an op of this run touches (of 2^RB float4 per thread)
             const int touched = (1 << RB) >> __builtin_popcount(op.reg_need);
-            if (e - o >= kJitLoopRun && touched >= kJitLoopMinRegs) {
+            if (e - o >= loop_run && touched >= kJitLoopMinRegs) {
                 if (op.variant >= kPhaseVariant) {
                     const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
                     std::snprintf(buf, sizeof buf, "      run_phase<%d, %s, RB>(ops + %d, %d, tid, base, v);\n", R,
@@ -182,7 +188,9 @@ std::string generate(const FParams &p, int K, int RB) {
                 src += test.empty() ? "      {" : "      if (" + test + ") {";
                 if (op.variant >= kPhaseVariant) {
                     const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
-                    std::snprintf(buf, sizeof buf, " phase_ct<%d, %s, RB>(make_float2(", R, odd ? "true" : "false");
+                    const bool scalar = phase_mode == 2 || (phase_mode == 1 && !test.empty());
+                    std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(make_float2(", scalar ? "phase_cs" : "phase_ct", R,
+                                  odd ? "true" : "false");
                     src += buf;
                     hexf(src, op.m[6]);
                     src += ", ";

@@ -59,16 +59,12 @@ def default_tile_qubits(num_qubits: int) -> int:
 
 def plan(num_qubits: int, ops, tile_qubits: int | None = None) -> list[Pass]:
     """Greedy in-order grouping into passes of at most K tile qubits.  Without
-    an explicit K (measured on B200, scripts/probes/k13rb.sh):
-    phase-dominated op lists (QFT) keep 13-qubit tiles, whose compiled
-    programs then use 3 register bits per thread (16 compute warps); other
-    lists take 12-qubit tiles (two persistent CTAs per SM) unless those need
-    more than 25% more passes."""
+    an explicit K: 12-qubit tiles (two persistent CTAs per SM) unless those
+    need more than 25% more passes than 13-qubit ones.  (Measured on B200
+    with the dynamic tile scheduler, scripts/qft_passes.py: QFT(28) 8.5 ms
+    on 12-qubit tiles vs 9.3 ms on 13, QFT(30) 36.3 vs 37.5 ms.)"""
     if tile_qubits is None and num_qubits >= 13:
         p13 = _plan(num_qubits, ops, 13)
-        nphase = sum(1 for op in ops if op[0] == N.QS_OP_PHASE)
-        if 2 * nphase > len(ops):
-            return p13
         p12 = _plan(num_qubits, ops, 12)
         return p12 if 4 * len(p12) <= 5 * len(p13) else p13
     return _plan(num_qubits, ops, tile_qubits)
