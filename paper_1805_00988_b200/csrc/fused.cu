@@ -275,55 +275,57 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     }
 
     // ---- stage planning -----------------------------------------------------
-    // need: 0 = any stage (phase op / target on local qubit 0), 1 = LOW
-    // (target on local 1..RB), 2 = HIGH holding the target's f-bit
+    // need: 0 = any stage (phase op / target on local qubit 0), 2 = a stage
+    // holding the target's f-bit in registers
     auto need_of = [&](const qs_op &op, int *fbit) -> int {
         if (op.kind != QS_OP_PAIR) return 0;
         const int lb = local_of[op.target];
         if (is_half(lb)) return 0;
-        if (f_of(lb) < RB) return 1;
         *fbit = f_of(lb);
         return 2;
     };
     // (1) stage layouts and op ranges: greedy over the PAIR ops in circuit
-    // order; the layout follows the first op that constrains it.
+    // order.  A stage's register bits must hold the f-bit of every pair
+    // target in it (half-bit targets are free) and leave one of the triples
+    // {f0,f1,f2} / {f5,f6,f7} to lanes 0-2 (bank-conflict-free LDS/STS on
+    // the padded layout); a stage ends when the next target does not fit.
+    // (Low and high targets share a stage whenever they fit: a layered
+    // circuit alternating them used to open a new stage per op, and every
+    // stage is a shared-memory round trip of the whole tile.)
     struct Plan {
-        int kind;               // 1 = LOW, 2 = HIGH
-        std::vector<int> rb;    // HIGH: register f-bits
-        int begin, end, first;  // op range; first constraining op
+        int kind;               // 2 (kept for the dump format)
+        std::vector<int> rb;    // register f-bits
+        int begin, end, first;  // op range; first pair op with a register target
+    };
+    auto triple_ok = [&](const std::vector<int> &rb) {
+        bool low_free = true, high_free = FB > 7;
+        for (int f : rb) {
+            if (f <= 2) low_free = false;
+            if (f >= 5 && f <= 7) high_free = false;
+        }
+        return low_free || high_free;
+    };
+    auto fits = [&](const std::vector<int> &rb, int f) {
+        if (std::find(rb.begin(), rb.end(), f) != rb.end()) return true;
+        if ((int)rb.size() >= RB) return false;
+        std::vector<int> t = rb;
+        t.push_back(f);
+        return triple_ok(t);
     };
     std::vector<Plan> plans;
     {
         int i = 0;
         while (i < nops) {
             Plan pl;
-            pl.kind = 1;
+            pl.kind = 2;
             pl.begin = i;
             pl.first = nops;
-            for (int j = i; j < nops; ++j) {
-                int f = -1, nd = need_of(ops[j], &f);
-                if (nd) {
-                    pl.kind = nd;
-                    pl.first = j;
-                    break;
-                }
-            }
-            if (pl.kind == 2) {
-                for (int j = i; j < nops && (int)pl.rb.size() < RB; ++j) {
-                    int f = -1, nd = need_of(ops[j], &f);
-                    if (nd == 1) break;
-                    if (nd == 2 && std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
-                }
-                for (int f = RB; f < FB && (int)pl.rb.size() < RB; ++f)
-                    if (std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
-                std::sort(pl.rb.begin(), pl.rb.end());
-            } else {
-                for (int r = 0; r < RB; ++r) pl.rb.push_back(r);
-            }
             for (; i < nops; ++i) {
-                int f = -1, nd = need_of(ops[i], &f);
-                if (nd == 1 && pl.kind != 1) break;
-                if (nd == 2 && (pl.kind != 2 || std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end())) break;
+                int f = -1;
+                if (!need_of(ops[i], &f)) continue;
+                if (!fits(pl.rb, f)) break;
+                if (pl.first == nops) pl.first = i;
+                if (std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
             }
             pl.end = i;
             plans.push_back(pl);
@@ -344,6 +346,25 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         for (int f : pl.rb) c += (fb >> f) & 1u;
         return c;
     };
+    // (1b) free register slots take the f-bits the stage's ops test most (a
+    // register-bit test is a compile-time mask; a lane-bit test idles half
+    // the lanes), then the lowest free bits, always leaving a lane triple
+    for (Plan &pl : plans) {
+        int uses[32] = {0};
+        for (int j = pl.begin; j < pl.end; ++j) {
+            const uint32_t fb = test_fbits(ops[j]);
+            for (int f = 0; f < FB; ++f) uses[f] += (fb >> f) & 1u;
+        }
+        std::vector<int> cand;
+        for (int f = 0; f < FB; ++f) cand.push_back(f);
+        std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return uses[x] > uses[y]; });
+        for (int f : cand)
+            if ((int)pl.rb.size() < RB && fits(pl.rb, f) &&
+                std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end())
+                pl.rb.push_back(f);
+        if ((int)pl.rb.size() != RB) return set_error(QS_ERR_VALUE, "fused pass: no register layout for a stage");
+        std::sort(pl.rb.begin(), pl.rb.end());
+    }
     // (2) the unconstrained ops (phases, half-bit targets) between the last
     // pair op of stage s-1 and the first of stage s may run in either stage
     // (order is kept).  Move the trailing run to stage s when its bits are
@@ -385,15 +406,16 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         for (int r = 0; r < RB; ++r) st.rf[r] = pl.rb[r];
         {
             // lanes 0..2 must vary f0..f2 or f5..f7 (bank-conflict-free on the
-            // padded layout); a HIGH stage takes whichever triple its ops test
-            // less (when it does not hold register bits)
-            const int low3[3] = {5, 6, 7}, high3[3] = {0, 1, 2};
-            const int *first3 = pl.kind == 1 ? low3 : high3;
+            // padded layout): a triple free of register bits, the one the
+            // stage's ops test less when both are
+            const int tri_lo[3] = {0, 1, 2}, tri_hi[3] = {5, 6, 7};
             bool used[32] = {false};
             for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
-            if (pl.kind == 2 && !used[5] && !used[6] && !used[7] && FB > 7 &&
-                uses[5] + uses[6] + uses[7] < uses[0] + uses[1] + uses[2])
-                first3 = low3;
+            const bool lo_free = !used[0] && !used[1] && !used[2];
+            const bool hi_free = FB > 7 && !used[5] && !used[6] && !used[7];
+            const int *first3 = tri_lo;
+            if (!lo_free || (hi_free && uses[5] + uses[6] + uses[7] < uses[0] + uses[1] + uses[2]))
+                first3 = tri_hi;
             for (int l = 0; l < 3; ++l) {
                 st.lf[l] = first3[l];
                 used[first3[l]] = true;
