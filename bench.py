@@ -618,6 +618,33 @@ def run_extras(st, stream, n, cpu=True):
                      "pass_bytes": len(passes) * 16 * (1 << n),
                      "achieved_GBps": len(passes) * 16 * (1 << n) / (ms / 1e3) / 1e9}
 
+    # K2 / K3 / K4 single-op sweeps at full size (touched bytes
+    # and the full-sweep equivalent reported separately)
+    from paper_1805_00988_b200 import random_unitary_gate, u1 as _u1
+    import numpy as _np
+
+    g = random_unitary_gate(_np.random.default_rng(5))
+    kern = {}
+    for name, fn, touched in (
+            ("controlled_c29_t7", lambda: st.apply_controlled_gate(g, n - 1, 7), 8 << n),
+            ("controlled_c0_t7", lambda: st.apply_controlled_gate(g, 0, 7), 8 << n),
+            ("controlled_c3_t1", lambda: st.apply_controlled_gate(g, 3, 1), 8 << n),
+            ("ccontrolled_c29_c28_t7", lambda: st.apply_controlled_controlled_gate(g, n - 1, n - 2, 7), 4 << n),
+            ("cphase_c29_t7", lambda: st.apply_controlled_gate(_u1(0.3), n - 1, 7), 4 << n)):
+        fn()
+        st.flush()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(5):
+            fn()
+        b.record(stream)
+        st.flush()
+        ms = a.elapsed_time(b) / 5
+        kern[name] = {"ms": round(ms, 4), "touched_GBps": round(touched / ms / 1e6, 1),
+                      "full_sweep_equiv_GBps": round((16 << n) / ms / 1e6, 1)}
+    res["single_op_kernels30"] = kern
+
     # config 1: 20-qubit H on every qubit + probabilities (host wall clock, incl. the fp64 D2H)
     s20 = State(20)
     s20.h(0)

@@ -129,6 +129,32 @@ void hexf(std::string &out, float x) {
     out += buf;
 }
 
+// An op's thread / tile predicate as generated source: the uniform tests
+// (tile bits against the redux'd base `ub`, warp bits against `wid`) first,
+// the divergent lane test last; "" when the op applies everywhere.
+std::string op_test(const FOp &op) {
+    std::string test;
+    char buf[96];
+    auto add = [&](const char *t) {
+        if (!test.empty()) test += " && ";
+        test += t;
+    };
+    if (op.ext_need) {
+        std::snprintf(buf, sizeof buf, "(ub & 0x%llxull) == 0x%llxull", (unsigned long long)op.ext_need,
+                      (unsigned long long)op.ext_need);
+        add(buf);
+    }
+    if (op.tid_need & ~31u) {
+        std::snprintf(buf, sizeof buf, "(wid & 0x%xu) == 0x%xu", op.tid_need & ~31u, op.tid_need & ~31u);
+        add(buf);
+    }
+    if (op.tid_need & 31u) {
+        std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need & 31u, op.tid_need & 31u);
+        add(buf);
+    }
+    return test;
+}
+
 std::string generate(const FParams &p, int K, int RB) {
     // diagonal ops inside a test: 1 (default) scalar phase_cs, 0 packed
     // phase_ct, 2 scalar everywhere (QSB_JIT_PHASE, for measurements)
@@ -140,7 +166,14 @@ std::string generate(const FParams &p, int K, int RB) {
     src.reserve(8192 + (size_t)p.nops * 200);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
            "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *ops, uint32_t tid,\n"
-           "      uint64_t base, float one, float4 (&v)[1 << RB]) {\n    switch (s) {\n";
+           "      uint64_t base, float one, float4 (&v)[1 << RB]) {\n"
+           // warp index and tile base through redux.sync: values ptxas knows
+           // to be warp-uniform, so warp-bit and tile tests become uniform
+           // branches (no BSSY / BSYNC reconvergence per op)
+           "    const uint32_t wid = __reduce_or_sync(0xffffffffu, tid & ~31u);\n"
+           "    const uint64_t ub = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(base >> 32)) << 32) |\n"
+           "                        __reduce_or_sync(0xffffffffu, (unsigned)base);\n"
+           "    (void)wid;\n    (void)ub;\n    switch (s) {\n";
     char buf[256];
     for (int k = 0; k < p.nstages; ++k) {
         const FStage &st = p.stages[k];
@@ -175,16 +208,7 @@ std::string generate(const FParams &p, int K, int RB) {
             }
             for (; o < e; ++o) {
                 const FOp &op = p.ops[o];
-                std::string test;
-                if (op.tid_need) {
-                    std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need, op.tid_need);
-                    test += buf;
-                }
-                if (op.ext_need) {
-                    std::snprintf(buf, sizeof buf, "%s(base & 0x%llxull) == 0x%llxull", test.empty() ? "" : " && ",
-                                  (unsigned long long)op.ext_need, (unsigned long long)op.ext_need);
-                    test += buf;
-                }
+                const std::string test = op_test(op);
                 src += test.empty() ? "      {" : "      if (" + test + ") {";
                 if (op.variant >= kPhaseVariant) {
                     const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
@@ -236,7 +260,11 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
     src.reserve(8192 + (size_t)p.nops * 400);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
            "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *, uint32_t tid,\n"
-           "      uint64_t base, float, double2 (&v)[1 << RB]) {\n    switch (s) {\n";
+           "      uint64_t base, float, double2 (&v)[1 << RB]) {\n"
+           "    const uint32_t wid = __reduce_or_sync(0xffffffffu, tid & ~31u);\n"
+           "    const uint64_t ub = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(base >> 32)) << 32) |\n"
+           "                        __reduce_or_sync(0xffffffffu, (unsigned)base);\n"
+           "    (void)wid;\n    (void)ub;\n    switch (s) {\n";
     char buf[256];
     for (int k = 0; k < p.nstages; ++k) {
         const FStage &st = p.stages[k];
@@ -245,16 +273,7 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
         for (int o = st.op_begin; o < st.op_end; ++o) {
             const FOp &op = p.ops[o];
             const qs_op64 &g = ops64[o];
-            std::string test;
-            if (op.tid_need) {
-                std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need, op.tid_need);
-                test += buf;
-            }
-            if (op.ext_need) {
-                std::snprintf(buf, sizeof buf, "%s(base & 0x%llxull) == 0x%llxull", test.empty() ? "" : " && ",
-                              (unsigned long long)op.ext_need, (unsigned long long)op.ext_need);
-                test += buf;
-            }
+            std::string test = op_test(op);
             src += test.empty() ? "      {" : "      if (" + test + ") {";
             if (op.variant >= kPhaseVariant) {
                 std::snprintf(buf, sizeof buf, " phase_ct_d<%u, RB>(make_double2(", op.reg_need);
