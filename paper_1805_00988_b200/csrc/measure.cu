@@ -24,10 +24,12 @@
 //   M2 k_scan_guess   exclusive scan of the sums -> guessed chunk starts
 //   M3 k_trajectories both guessed trajectories per chunk (warp-transposed
 //                     through shared memory so HBM reads stay coalesced)
-//   M4 k_resolve_warp one thread walks the chunks (its warp stages the data): true start s, parity of
-//                     s's mantissa selects the trajectory, end = s + D exactly;
-//                     chunks that cross a binade (or whose guess fell in the
-//                     wrong binade) are re-summed sequentially from s
+//   M4 true chunk starts: the parity of s's mantissa selects the
+//                     trajectory, end = s + D exactly — composed as parity
+//                     maps over blocks of chunks (k_block_maps / k_block_walk
+//                     / k_block_fill); chunks that cross a binade (or whose
+//                     guess fell in the wrong binade) are re-summed
+//                     sequentially from s
 //   M5 k_chunk_last   normalised CDF value at each chunk end
 //   M6 k_draws        per draw: PCG64 jump-ahead, binary search over chunk
 //                     ends, then the sequential in-chunk walk from the exact
@@ -259,132 +261,179 @@ __device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, in
 }
 
 // ---- M4: resolve true chunk starts ------------------------------------------
-// M4 with the per-chunk data staged by a warp: the walk is a dependent chain
-// through s (the parity of s picks the trajectory), but the data it reads are
-// not, so 31 idle lanes are better spent fetching the next batch.  Each
-// iteration the warp issues the global loads of batch b+1 into registers,
-// lane 0 walks batch b out of shared memory (one DADD + a select on the
-// critical path per chunk), then the registers land in shared memory for
-// the next walk.  Same arithmetic and order as a single-thread walk.
-constexpr int kResolveBatch = 256;
+// Inside one binade a double's bit pattern is linear in its value (step u).
+// A chunk whose trajectory check passes moves the running value s to
+// s + d[parity(s)] exactly, i.e. its bit pattern by an integer inc[parity],
+// and the parity of the result follows from that.  Such parity maps
+// (inc0, inc1) compose associatively — (A then B)(p) = A_p + B[(p + A_p) & 1]
+// — so a block of chunks whose guesses share one binade reduces to one map
+// (M4a, a block scan that also keeps every chunk's exclusive prefix map);
+// one warp walks the blocks (M4b: a single step per regular block — its start
+// and end must lie in that binade — while a block holding a binade crossing,
+// a failed trajectory or the exact-zero prefix is walked chunk by chunk with
+// the exact sequential fallback); and every chunk start of a regular block is
+// its block start plus the prefix map (M4c).  The values are the ones the
+// chunk-by-chunk walk produces, bit for bit.
+constexpr int kMapBlock = 256;
+
+struct PMap {
+    long long a0, a1;  // bit-pattern increment from an even / odd start
+};
+__device__ __forceinline__ PMap pcompose(PMap x, PMap y) {  // x, then y
+    PMap r;
+    r.a0 = x.a0 + ((x.a0 & 1) ? y.a1 : y.a0);
+    r.a1 = x.a1 + (((1 + x.a1) & 1) ? y.a1 : y.a0);
+    return r;
+}
+
+__global__ void __launch_bounds__(kMapBlock)
+    k_block_maps(uint64_t nch, const double *__restrict__ g0, const double *__restrict__ d0,
+                 const double *__restrict__ d1, const int *__restrict__ flags, long long *__restrict__ pmap,
+                 long long *__restrict__ bmap) {
+    __shared__ PMap wsum[kMapBlock / 32];
+    __shared__ long long sE;
+    const uint64_t k = blockIdx.x * (uint64_t)kMapBlock + threadIdx.x;
+    const bool in = k < nch;
+    long long E = -1;
+    PMap m{0, 0};
+    bool ok = true;
+    if (in) {
+        const int f = flags[k];
+        const double g = g0[k];
+        const long long gb = __double_as_longlong(g);
+        E = (long long)((unsigned long long)gb >> 52);
+        ok = (f & kFlagOk) && !(f & kFlagExact0) && E >= 2;
+        if (ok) {  // t0 = g0 + d0 and t1 = g1 + d1 are exact (same grid, same binade)
+            m.a0 = __double_as_longlong(__dadd_rn(g, d0[k])) - gb;
+            m.a1 = __double_as_longlong(__dadd_rn(__longlong_as_double(gb + 1), d1[k])) - (gb + 1);
+        }
+    }
+    if (threadIdx.x == 0) sE = E;
+    __syncthreads();
+    ok = ok && (!in || E == sE);
+    if (!__syncthreads_and(ok)) {
+        if (threadIdx.x == 0) bmap[4 * blockIdx.x + 3] = 0;
+        return;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    PMap inc = m;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        PMap x;
+        x.a0 = __shfl_up_sync(0xffffffffu, inc.a0, o);
+        x.a1 = __shfl_up_sync(0xffffffffu, inc.a1, o);
+        if (lane >= o) inc = pcompose(x, inc);
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    PMap pre{0, 0};
+    for (int i = 0; i < w; ++i) pre = pcompose(pre, wsum[i]);
+    PMap ex;
+    ex.a0 = __shfl_up_sync(0xffffffffu, inc.a0, 1);
+    ex.a1 = __shfl_up_sync(0xffffffffu, inc.a1, 1);
+    if (lane == 0) ex = PMap{0, 0};
+    ex = pcompose(pre, ex);
+    if (in) {
+        pmap[2 * k] = ex.a0;
+        pmap[2 * k + 1] = ex.a1;
+    }
+    if (threadIdx.x == kMapBlock - 1) {
+        const PMap tot = pcompose(pre, inc);
+        bmap[4 * blockIdx.x + 0] = tot.a0;
+        bmap[4 * blockIdx.x + 1] = tot.a1;
+        bmap[4 * blockIdx.x + 2] = sE;
+        bmap[4 * blockIdx.x + 3] = 1;
+    }
+}
+
 template <class A>
 __global__ void __launch_bounds__(32)
-    k_resolve_warp(const A *__restrict__ amps, uint64_t nch, int clog, double s_start,
-                   const double *__restrict__ g0, const double *__restrict__ d0,
-                   const double *__restrict__ d1, const double *__restrict__ hi,
-                   const int *__restrict__ flags, double *__restrict__ start,
-                   double *__restrict__ total, unsigned long long *__restrict__ nslow) {
-    constexpr int kPer = kResolveBatch / 32;
-    __shared__ double sd0[kResolveBatch], sd1[kResolveBatch], shi[kResolveBatch], slo[kResolveBatch];
-    __shared__ int sfl[kResolveBatch];
-    __shared__ double sst[kResolveBatch];
+    k_block_walk(const A *__restrict__ amps, uint64_t nch, int clog, double s_start,
+                 const double *__restrict__ g0, const double *__restrict__ d0, const double *__restrict__ d1,
+                 const double *__restrict__ hi, const int *__restrict__ flags,
+                 const long long *__restrict__ bmap, uint64_t nblk, double *__restrict__ sblock,
+                 double *__restrict__ start, double *__restrict__ total, unsigned long long *__restrict__ nslow) {
+    __shared__ double sd0[kMapBlock], sd1[kMapBlock], shi[kMapBlock], slo[kMapBlock];
+    __shared__ int sfl[kMapBlock];
     const int lane = threadIdx.x;
-    double r0[kPer], r1[kPer], rh[kPer], rl[kPer];
-    int rf[kPer];
-    auto fetch = [&](uint64_t b0) {
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const uint64_t k = b0 + (uint64_t)(lane + 32 * i);
-            if (k < nch) {
-                r0[i] = d0[k];
-                r1[i] = d1[k];
-                rh[i] = hi[k];
-                rl[i] = binade_lo(g0[k]);
-                rf[i] = flags[k];
-            }
-        }
-    };
-    auto land = [&]() {
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const int j = lane + 32 * i;
-            sd0[j] = r0[i];
-            sd1[j] = r1[i];
-            shi[j] = rh[i];
-            slo[j] = rl[i];
-            sfl[j] = rf[i];
-        }
-    };
-    fetch(0);
-    land();
-    __syncwarp();
-    double s = s_start;
+    double s = s_start;  // identical in every lane
     unsigned long long slow = 0;
-    for (uint64_t b0 = 0; b0 < nch; b0 += kResolveBatch) {
-        const uint64_t nb = b0 + kResolveBatch;
-        if (nb < nch) fetch(nb);  // in flight during the walk below
-        const int cnt = (int)((nch - b0) < (uint64_t)kResolveBatch ? (nch - b0) : kResolveBatch);
-        if (lane == 0) {
-            // speculative walk: no data-dependent branch on the chain (the
-            // parity select and one DADD per chunk); validity is accumulated
-            // and the batch is re-walked with the exact slow path if any
-            // chunk failed (a binade crossing: a handful per register)
-            const double s0 = s;
-            bool all_ok = true;
-            for (int j0 = 0; j0 < cnt; j0 += 16) {
-                // 16 chunks' data into registers first: nothing on the chain
-                // waits for a shared-memory load
-                double a[16], b[16], h[16], lo[16], ss[16];
-                int fl[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    a[i] = sd0[j0 + i];
-                    b[i] = sd1[j0 + i];
-                    h[i] = shi[j0 + i];
-                    lo[i] = slo[j0 + i];
-                    fl[i] = sfl[j0 + i];
-                }
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    if (j0 + i >= cnt) break;  // only in the last, partial batch
-                    ss[i] = s;
-                    const bool odd = (__double_as_longlong(s) & 1ll) != 0;
-                    const double e_traj = __dadd_rn(s, odd ? b[i] : a[i]);
-                    const bool ex0 = (fl[i] & kFlagExact0) != 0;
-                    const bool ok_traj = ((fl[i] & kFlagOk) != 0) & (s >= lo[i]) & (s < h[i]) & (e_traj < h[i]);
-                    const bool ok_ex0 = s == s_start;
-                    all_ok &= ex0 ? ok_ex0 : ok_traj;
-                    s = ex0 ? a[i] : e_traj;
-                }
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (j0 + i < cnt) sst[j0 + i] = ss[i];
+    for (uint64_t b0 = 0; b0 < nblk; b0 += 32) {
+        long long F0 = 0, F1 = 0, E = -1, reg = 0;
+        if (b0 + lane < nblk) {
+            const long long *q = bmap + 4 * (b0 + lane);
+            reg = q[3];
+            if (reg) {
+                F0 = q[0];
+                F1 = q[1];
+                E = q[2];
             }
-            if (!all_ok) {
-                s = s0;
-                for (int j = 0; j < cnt; ++j) {
-                    const uint64_t k = b0 + j;
-                    sst[j] = s;
+        }
+        const int cnt = (int)((nblk - b0) < 32 ? (nblk - b0) : 32);
+        for (int i = 0; i < cnt; ++i) {
+            const long long f0 = __shfl_sync(0xffffffffu, F0, i), f1 = __shfl_sync(0xffffffffu, F1, i);
+            const long long e = __shfl_sync(0xffffffffu, E, i), r = __shfl_sync(0xffffffffu, reg, i);
+            const uint64_t b = b0 + i;
+            const long long sb = __double_as_longlong(s);
+            const long long eb = sb + ((sb & 1) ? f1 : f0);
+            if (r && (sb >> 52) == e && (eb >> 52) == e) {  // start and end inside the block's binade
+                if (lane == 0) sblock[b] = s;
+                s = __longlong_as_double(eb);
+                continue;
+            }
+            // irregular block: stage its chunk data, lane 0 walks it exactly
+            if (lane == 0) sblock[b] = -1.0;
+            const uint64_t k0 = b * kMapBlock;
+            const int m = (int)((nch - k0) < (uint64_t)kMapBlock ? (nch - k0) : kMapBlock);
+            for (int j = lane; j < m; j += 32) {
+                sd0[j] = d0[k0 + j];
+                sd1[j] = d1[k0 + j];
+                shi[j] = hi[k0 + j];
+                slo[j] = binade_lo(g0[k0 + j]);
+                sfl[j] = flags[k0 + j];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                for (int j = 0; j < m; ++j) {
+                    start[k0 + j] = s;
                     const int f = sfl[j];
-                    double e;
+                    double en;
                     bool valid;
                     if (f & kFlagExact0) {
                         valid = (s == s_start);
-                        e = sd0[j];
+                        en = sd0[j];
                     } else {
                         const bool odd = (__double_as_longlong(s) & 1ll) != 0;
-                        e = __dadd_rn(s, odd ? sd1[j] : sd0[j]);
+                        en = __dadd_rn(s, odd ? sd1[j] : sd0[j]);
                         const double h = shi[j];
-                        valid = (f & kFlagOk) && s >= slo[j] && s < h && e < h;
+                        valid = (f & kFlagOk) && s >= slo[j] && s < h && en < h;
                     }
                     if (!valid) {
-                        e = walk_chunk(amps, k, clog, s);
+                        en = walk_chunk(amps, k0 + j, clog, s);
                         ++slow;
                     }
-                    s = e;
+                    s = en;
                 }
             }
+            __syncwarp();
+            s = __shfl_sync(0xffffffffu, s, 0);
         }
-        __syncwarp();
-        for (int j = lane; j < cnt; j += 32) start[b0 + j] = sst[j];  // coalesced
-        __syncwarp();
-        if (nb < nch) land();
-        __syncwarp();
     }
     if (lane == 0) {
         *total = s;
         *nslow = slow;
     }
+}
+
+__global__ void __launch_bounds__(kMapBlock)
+    k_block_fill(uint64_t nch, const double *__restrict__ sblock, const long long *__restrict__ pmap,
+                 double *__restrict__ start) {
+    const double sb = sblock[blockIdx.x];
+    if (sb < 0.0) return;  // walked chunk by chunk in M4b
+    const uint64_t k = blockIdx.x * (uint64_t)kMapBlock + threadIdx.x;
+    if (k >= nch) return;
+    const long long bits = __double_as_longlong(sb);
+    start[k] = __longlong_as_double(bits + ((bits & 1) ? pmap[2 * k + 1] : pmap[2 * k]));
 }
 
 // ---- M5: normalised CDF value at each chunk end --------------------------------
@@ -580,8 +629,10 @@ int run_norm(qs_state *s, double *out) {
 struct CdfScratch {
     int clog;
     uint64_t nch;
-    double *csum, *g0, *d0, *d1, *hi, *start, *last, *end;
+    double *csum, *g0, *d0, *d1, *hi, *start, *last, *end, *sblock;
     unsigned long long *nslow;
+    long long *pmap, *bmap;
+    uint64_t nblk;
     int *flags;
     int64_t *dout;
 };
@@ -592,8 +643,10 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     c.clog = n < kChunkLog ? n : kChunkLog;
     c.nch = dim >> c.clog;
     const uint64_t nch = c.nch;
-    // csum, g0, d0, d1, hi, start, last (doubles) + end + nslow + flags + outcomes
-    const size_t nd = 7 * nch + 2;
+    c.nblk = (nch + kMapBlock - 1) / kMapBlock;
+    // csum, g0, d0, d1, hi, start, last (doubles) + end + nslow, prefix maps
+    // (2 per chunk), block maps (4 per block), block starts + flags + outcomes
+    const size_t nd = 7 * nch + 2 + 2 * nch + 5 * c.nblk;
     const size_t bytes = nd * sizeof(double) + nch * sizeof(int) + 64 + (size_t)k * sizeof(int64_t);
     int rc = ensure_scratch(s, bytes);
     if (rc) return rc;
@@ -607,6 +660,9 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     c.last = b + 6 * nch;
     c.end = b + 7 * nch;
     c.nslow = (unsigned long long *)(b + 7 * nch + 1);
+    c.pmap = (long long *)(b + 7 * nch + 2);
+    c.bmap = c.pmap + 2 * nch;
+    c.sblock = (double *)(c.bmap + 4 * c.nblk);
     c.flags = (int *)(b + nd);
     c.dout = (int64_t *)((char *)c.flags + ((nch * sizeof(int) + 63) & ~(size_t)63));
     return QS_OK;
@@ -624,8 +680,11 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
         k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
             amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags);
     }
-    k_resolve_warp<<<1, 32, 0, s->stream>>>(amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi,
-                                            c.flags, c.start, c.end, c.nslow);
+    k_block_maps<<<(unsigned)c.nblk, kMapBlock, 0, s->stream>>>(c.nch, c.g0, c.d0, c.d1, c.flags, c.pmap,
+                                                                 c.bmap);
+    k_block_walk<<<1, 32, 0, s->stream>>>(amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi, c.flags,
+                                          c.bmap, c.nblk, c.sblock, c.start, c.end, c.nslow);
+    k_block_fill<<<(unsigned)c.nblk, kMapBlock, 0, s->stream>>>(c.nch, c.sblock, c.pmap, c.start);
     QS_CUDA(cudaGetLastError());
     return QS_OK;
 }
