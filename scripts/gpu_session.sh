@@ -15,6 +15,6 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_r
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-extras > $OUT/ncu_launch_bench_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_sweep|k_phase|k_fused|qsb_pass|k_probs|k_chunk_sums|k_trajectories|k_resolve|k_draws" -c 12 \
+    -k regex:"k_sweep|k_phase|k_fused|qsb_pass|k_probs|k_chunk_sums|k_trajectories|k_block|k_draws" -c 14 \
     -o $OUT/prof_$TAG -f python scripts/profile_kernels.py --n 30 > $OUT/ncu_full_$TAG.log 2>&1
 echo done
