@@ -117,6 +117,20 @@ __global__ void k_chunk_sums(const A *__restrict__ amps, int clog, double *__res
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) csum[c] = acc;
 }
+// complex64 with 4096-amplitude chunks: 16-B loads, all eight of a thread's
+// loads in flight at once (the sums are guesses: any order will do)
+__global__ void __launch_bounds__(256) k_chunk_sums_f4(const float4 *__restrict__ amps, double *__restrict__ csum) {
+    __shared__ double sh[32];
+    const float4 *p = amps + (blockIdx.x << (kChunkLog - 1));
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldcs(p + threadIdx.x + 256 * i);
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += prob(make_float2(v[i].x, v[i].y)) + prob(make_float2(v[i].z, v[i].w));
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) csum[blockIdx.x] = acc;
+}
 
 // ---- M2: exclusive scan of chunk sums (single block) -------------------------
 __global__ void k_scan_guess(const double *__restrict__ csum, uint64_t nch, double *__restrict__ g) {
@@ -672,7 +686,10 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
 // `s_start`; leaves chunk starts in c.start and the final value in *c.end.
 template <class A>
 static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s_start) {
-    k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(amps, c.clog, c.csum);
+    if (sizeof(A) == sizeof(float2) && c.clog == kChunkLog)
+        k_chunk_sums_f4<<<(unsigned)c.nch, 256, 0, s->stream>>>((const float4 *)amps, c.csum);
+    else
+        k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(amps, c.clog, c.csum);
     k_scan_guess<<<1, 1024, 0, s->stream>>>(c.csum, c.nch, c.start);  // prefixes -> start[]
     {
         const uint64_t warps = (c.nch + 31) / 32;
