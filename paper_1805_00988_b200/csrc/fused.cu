@@ -238,7 +238,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     p.one = 1.0f;
     if (!s->tile_ctr) {  // first fused pass of this handle: the scheduler's counter
         DeviceGuard guard(s->device);
-        QS_CUDA(cudaMalloc(&s->tile_ctr, 256));
+        QS_CUDA(pool_alloc(s->device, 256, (void **)&s->tile_ctr));  // cached: no cudaFree (device sync) per handle
         QS_CUDA(cudaMemsetAsync(s->tile_ctr, 0, 256, s->stream));
     }
     p.tile_ctr = s->tile_ctr;

@@ -186,7 +186,7 @@ int qs_destroy(qs_state *s) {
     pool_free(s->device, s->amps, state_bytes(s));
     pool_free(s->device, s->scratch, s->scratch_bytes);
     if (s->ops_dev) cudaFree(s->ops_dev);
-    if (s->tile_ctr) cudaFree(s->tile_ctr);
+    if (s->tile_ctr) pool_free(s->device, s->tile_ctr, 256);  // zero again once its last pass finished
     if (s->pinned) cudaFreeHost(s->pinned);
     stream_release(s->device, s->stream);
     delete s;
