@@ -37,6 +37,10 @@
 // No N-sized CDF is materialised; every value compared against u equals the
 // reference's cdf[j] / total bit for bit.
 
+#include <sys/mman.h>
+
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -556,45 +560,35 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
 
 }  // namespace
 
-// Host-side copy of one staged piece, split over a few threads (a single
-// memcpy thread caps at ~10 GB/s, well below the PCIe D2H rate).
-static void parallel_memcpy(void *dst, const void *src, size_t bytes) {
-    const size_t kThreadsMax = 8, kMinPer = 4u << 20;
-    size_t nt = bytes / kMinPer;
-    if (nt > kThreadsMax) nt = kThreadsMax;
-    if (nt <= 1) {
-        std::memcpy(dst, src, bytes);
-        return;
-    }
-    std::vector<std::thread> th;
-    const size_t per = (bytes + nt - 1) / nt;
-    for (size_t t = 0; t < nt; ++t) {
-        const size_t lo = t * per, hi = lo + per < bytes ? lo + per : bytes;
-        if (lo >= hi) break;
-        th.emplace_back([=] { std::memcpy((char *)dst + lo, (const char *)src + lo, hi - lo); });
-    }
-    for (auto &x : th) x.join();
-}
-
 // probabilities into a (pageable) host array: |a|^2 pieces computed on the
 // device, copied D2H into two pinned staging buffers, and drained to `host`
-// by host threads while the next piece is in flight.
+// by a team of host threads (each copies its slice of every piece) while the
+// next piece is in flight.  The team lives for the whole call: spawning
+// threads per piece cost more than the copies.
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host) {
-    const uint64_t piece = 1ull << 22;  // 32 MiB of fp64 per staging round
+    uint64_t piece = 1ull << 23;  // 64 MiB of fp64 per staging round
+    if (const char *e = std::getenv("QSB_PROB_PIECE_LOG")) piece = 1ull << std::atoi(e);
     const uint64_t step = count < piece ? count : piece;
     int rc = ensure_scratch(s, 2 * step * sizeof(double));
     if (rc) return rc;
     rc = ensure_pinned(s, 2 * step * sizeof(double));
     if (rc) return rc;
+    // A fresh numpy result page-faults 4-KiB pages during the host copy: ask
+    // for transparent huge pages on its 2-MiB-aligned interior.
+    if (count * sizeof(double) >= (64u << 20)) {
+        const uintptr_t a = ((uintptr_t)host + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+        const uintptr_t z = ((uintptr_t)(host + count)) & ~(uintptr_t)((2u << 20) - 1);
+        if (z > a) madvise((void *)a, z - a, MADV_HUGEPAGE);
+    }
     double *dev[2] = {(double *)s->scratch, (double *)s->scratch + step};
     double *pin[2] = {(double *)s->pinned, (double *)s->pinned + step};
     cudaEvent_t ev[2];
     QS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     QS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-    uint64_t prev_off = 0, prev_len = 0;
-    int b = 0;
-    for (uint64_t done = 0; done < count; done += step, b ^= 1) {
-        const uint64_t m = (count - done) < step ? (count - done) : step;
+    const uint64_t npieces = (count + step - 1) / step;
+    auto enqueue = [&](uint64_t i) -> int {
+        const uint64_t done = i * step, m = (count - done) < step ? (count - done) : step;
+        const int b = (int)(i & 1);
         unsigned grid = (unsigned)((m + 255) / 256);
         if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
         if (s->prec == QS_DOUBLE)
@@ -602,21 +596,55 @@ int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host
         else
             k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, dev[b], m);
         QS_CUDA(cudaGetLastError());
-        QS_CUDA(cudaMemcpyAsync(pin[b], dev[b], m * sizeof(double), cudaMemcpyDeviceToHost,
-                                s->stream));
+        QS_CUDA(cudaMemcpyAsync(pin[b], dev[b], m * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
         QS_CUDA(cudaEventRecord(ev[b], s->stream));
-        if (prev_len) {  // drain the previous piece while this one is in flight
-            QS_CUDA(cudaEventSynchronize(ev[b ^ 1]));
-            parallel_memcpy(host + prev_off, pin[b ^ 1], prev_len * sizeof(double));
+        return QS_OK;
+    };
+    // copy team: worker t copies slice t of piece `ready`, then counts itself done
+    unsigned hw = std::thread::hardware_concurrency();
+    const int nt = count * sizeof(double) < (16u << 20) ? 0 : (int)(hw > 16 ? 16 : (hw < 2 ? 2 : hw));
+    std::atomic<long long> ready{-1};
+    std::atomic<int> finished{0};
+    std::atomic<bool> stop{false};
+    auto piece_len = [&](uint64_t i) { return (count - i * step) < step ? (count - i * step) : step; };
+    std::vector<std::thread> team;
+    for (int t = 0; t < nt; ++t)
+        team.emplace_back([&, t] {
+            long long seen = -1;
+            for (;;) {
+                long long r;
+                while ((r = ready.load(std::memory_order_acquire)) == seen && !stop.load(std::memory_order_acquire))
+                    std::this_thread::yield();
+                if (r == seen) return;  // stop
+                seen = r;
+                const uint64_t len = piece_len((uint64_t)r) * sizeof(double);
+                const uint64_t per = (len / nt + 63) & ~(uint64_t)63;
+                const uint64_t lo = (uint64_t)t * per, hi = lo + per < len ? lo + per : len;
+                if (lo < hi)
+                    std::memcpy((char *)(host + (uint64_t)r * step) + lo, (const char *)pin[r & 1] + lo, hi - lo);
+                finished.fetch_add(1, std::memory_order_acq_rel);
+            }
+        });
+    int err = QS_OK;
+    for (uint64_t i = 0; i < npieces && i < 2 && !err; ++i) err = enqueue(i);
+    for (uint64_t i = 0; i < npieces && !err; ++i) {
+        if (cudaEventSynchronize(ev[i & 1]) != cudaSuccess) {
+            err = cuda_fail(cudaGetLastError(), "cudaEventSynchronize");
+            break;
         }
-        prev_off = done;
-        prev_len = m;
+        if (nt) {
+            ready.store((long long)i, std::memory_order_release);
+            while (finished.load(std::memory_order_acquire) < (int)((i + 1) * nt)) std::this_thread::yield();
+        } else {
+            std::memcpy(host + i * step, pin[i & 1], piece_len(i) * sizeof(double));
+        }
+        if (i + 2 < npieces) err = enqueue(i + 2);  // buffer i & 1 is free again
     }
-    QS_CUDA(cudaEventSynchronize(ev[b ^ 1]));
-    parallel_memcpy(host + prev_off, pin[b ^ 1], prev_len * sizeof(double));
+    stop.store(true, std::memory_order_release);
+    for (auto &x : team) x.join();
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
-    return QS_OK;
+    return err;
 }
 
 int run_norm(qs_state *s, double *out) {
