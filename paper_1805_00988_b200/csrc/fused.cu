@@ -293,7 +293,6 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     // circuit alternating them used to open a new stage per op, and every
     // stage is a shared-memory round trip of the whole tile.)
     struct Plan {
-        int kind;               // 2 (kept for the dump format)
         std::vector<int> rb;    // register f-bits
         int begin, end, first;  // op range; first pair op with a register target
     };
@@ -317,7 +316,6 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         int i = 0;
         while (i < nops) {
             Plan pl;
-            pl.kind = 2;
             pl.begin = i;
             pl.first = nops;
             for (; i < nops; ++i) {
