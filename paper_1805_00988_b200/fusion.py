@@ -17,12 +17,13 @@ phase kernel touches fewer bytes than a full tile pass).
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _native as N
-from .gates import is_phase, m8_for
+from .gates import cached_ptr, entries_ptr, is_phase
 
 LOW = 6
 
@@ -44,12 +45,20 @@ class Pass:
         return arr
 
 
+_KIND: dict = {}  # id(cached entries array) -> QS_OP_PHASE / QS_OP_PAIR
+
+
 def lower(gate, target: int, controls=(), double: bool = False) -> tuple[int, int, int, np.ndarray]:
-    m = m8_for(gate, double)
+    m = entries_ptr(gate, double)[0]  # read-only, shared by every op of the same gate
     cm = 0
     for c in controls:
         cm |= 1 << int(c)
-    kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
+    kind = _KIND.get(id(m))
+    if kind is None:
+        kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
+        if cached_ptr(m) is not None:  # cached array: remember its kind while it lives
+            _KIND[id(m)] = kind
+            weakref.finalize(m, _KIND.pop, id(m), None)
     return kind, int(target), cm, m
 
 
@@ -155,12 +164,20 @@ def run(state, passes: list[Pass]) -> None:
 def _single(state, kind, t, cm, m) -> None:
     """One op: the dedicated sweep kernels (the phase kernel for diagonal ops)."""
     L = N.lib()
-    ctrls = [q for q in range(64) if (cm >> q) & 1]
+    ctrls = []
+    while cm and len(ctrls) < 3:
+        low = cm & -cm
+        ctrls.append(low.bit_length() - 1)
+        cm ^= low
+    cm |= sum(1 << q for q in ctrls)
+    mp = cached_ptr(m)  # entries arrays from lower() carry a cached pointer
     if m.dtype == np.float64:  # fp64 entries (complex128 registers)
-        mp = N.f64ptr(np.ascontiguousarray(m))
+        if mp is None:
+            mp = N.f64ptr(np.ascontiguousarray(m))
         g1, g2, g3 = L.qs_apply_gate_f64, L.qs_apply_controlled_gate_f64, L.qs_apply_controlled_controlled_gate_f64
     else:
-        mp = N.f32ptr(np.ascontiguousarray(m, dtype=np.float32))
+        if mp is None:
+            mp = N.f32ptr(np.ascontiguousarray(m, dtype=np.float32))
         g1, g2, g3 = L.qs_apply_gate, L.qs_apply_controlled_gate, L.qs_apply_controlled_controlled_gate
     if not ctrls:
         N.check(g1(state.handle, t, mp))

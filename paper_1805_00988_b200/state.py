@@ -25,7 +25,7 @@ import math
 import numpy as np
 
 from . import _native as N
-from .gates import FIXED_GATES, Gate, m8_for, u1 as _u1
+from .gates import FIXED_GATES, Gate, entries_ptr, u1 as _u1
 
 
 class _Queue:
@@ -181,8 +181,8 @@ class State:
     # Gate entries are rounded to the register's precision first
     # (kernel.py:118-119): float32 entry points for complex64, fp64 for complex128.
     def _m(self, gate):
-        m = m8_for(gate, self.is_double)
-        return N.f64ptr(m) if self.is_double else N.f32ptr(m), m
+        m, ptr = entries_ptr(gate, self.is_double)
+        return ptr, m
 
     def apply_gate(self, gate, target: int) -> "State":
         mp, _keep = self._m(gate)
