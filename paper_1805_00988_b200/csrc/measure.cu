@@ -176,7 +176,12 @@ __device__ __forceinline__ double binade_lo(double g) {
     return __longlong_as_double((long long)(E << 52));
 }
 
-enum : int { kFlagOk = 1, kFlagExact0 = 2 };
+enum : int { kFlagOk = 1, kFlagExact0 = 2, kFlagWalked = 4 };
+// Fine starts: M3 also keeps both trajectories (minus their guesses) at every
+// 256th amplitude of a 4096-amplitude chunk, so a draw can start its exact
+// walk at the last of the chunk's 16 sub-blocks whose running value is still
+// <= u instead of at the chunk start (16x less walking per draw).
+constexpr int kFineLog = 8, kFinePer = 1 << (kChunkLog - kFineLog);
 
 // ---- M3: guessed trajectories -------------------------------------------------
 // One warp owns 32 consecutive chunks; every 32-element step the warp loads a
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
     k_trajectories(const A *__restrict__ amps, uint64_t nch, int clog, double start,
                    const double *__restrict__ g, double *__restrict__ g0out,
                    double *__restrict__ d0, double *__restrict__ d1, double *__restrict__ hiout,
-                   int *__restrict__ flags) {
+                   int *__restrict__ flags, double *__restrict__ fine0, double *__restrict__ fine1) {
     __shared__ double tile[kTrajWarps][32][33];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t first = ((uint64_t)blockIdx.x * kTrajWarps + w) * 32;
@@ -229,6 +234,11 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
                 const double p = tile[w][lane][j];
                 t0 = __dadd_rn(t0, p);
                 t1 = __dadd_rn(t1, p);
+            }
+            const uint64_t pos = j0 + 32;  // elements summed so far
+            if (fine0 && (pos & ((1u << kFineLog) - 1)) == 0 && pos < C) {
+                fine0[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t0, g0);  // exact while in the binade
+                fine1[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t1, g1);
             }
         }
         __syncwarp();
@@ -368,7 +378,7 @@ template <class A>
 __global__ void __launch_bounds__(32)
     k_block_walk(const A *__restrict__ amps, uint64_t nch, int clog, double s_start,
                  const double *__restrict__ g0, const double *__restrict__ d0, const double *__restrict__ d1,
-                 const double *__restrict__ hi, const int *__restrict__ flags,
+                 const double *__restrict__ hi, int *__restrict__ flags,
                  const long long *__restrict__ bmap, uint64_t nblk, double *__restrict__ sblock,
                  double *__restrict__ start, double *__restrict__ total, unsigned long long *__restrict__ nslow) {
     __shared__ double sd0[kMapBlock], sd1[kMapBlock], shi[kMapBlock], slo[kMapBlock];
@@ -429,6 +439,7 @@ __global__ void __launch_bounds__(32)
                     if (!valid) {
                         en = walk_chunk(amps, k0 + j, clog, s);
                         ++slow;
+                        flags[k0 + j] = f | kFlagWalked;  // no fine starts for this chunk
                     }
                     s = en;
                 }
@@ -502,7 +513,8 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
                         const double *__restrict__ start, const double *__restrict__ last,
                         const double *__restrict__ end, double gtotal, double s_start,
                         uint64_t base, uint64_t gdim, int is_last, qs_pcg64 rng, int64_t k,
-                        int64_t *__restrict__ out) {
+                        int64_t *__restrict__ out, const int *__restrict__ flags,
+                        const double *__restrict__ fine0, const double *__restrict__ fine1) {
     const double t = gtotal > 0.0 ? gtotal : *end;
     const double u_lo = __ddiv_rn(s_start, t);
     const u128 st0 = mk128(rng.state_hi, rng.state_lo);
@@ -535,6 +547,24 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
             // chain (the loads do not depend on s; a one-at-a-time loop
             // waits a memory latency per amplitude)
             uint64_t j = 0, hit = C;
+            if (fine0 && clog == kChunkLog) {
+                const int f = flags[lo];
+                if ((f & kFlagOk) && !(f & (kFlagExact0 | kFlagWalked))) {
+                    // exact running values after 256, 512, ... amplitudes: the
+                    // chunk start plus the trajectory of its parity (M3, M4)
+                    const double *fd = ((__double_as_longlong(s) & 1ll) ? fine1 : fine0) + lo * kFinePer;
+                    double fs = s;
+                    int sb = 0;
+                    for (int q = 1; q < kFinePer; ++q) {
+                        const double v = __dadd_rn(s, fd[q]);
+                        if (v >= thr && __ddiv_rn(v, t) > u) break;
+                        sb = q;
+                        fs = v;
+                    }
+                    j = (uint64_t)sb << kFineLog;
+                    s = fs;
+                }
+            }
             for (; j + 8 <= C && hit == C; j += 8) {
                 double pr[8];
 #pragma unroll
@@ -671,7 +701,7 @@ int run_norm(qs_state *s, double *out) {
 struct CdfScratch {
     int clog;
     uint64_t nch;
-    double *csum, *g0, *d0, *d1, *hi, *start, *last, *end, *sblock;
+    double *csum, *g0, *d0, *d1, *hi, *start, *last, *end, *sblock, *fine0, *fine1;
     unsigned long long *nslow;
     long long *pmap, *bmap;
     uint64_t nblk;
@@ -688,7 +718,9 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     c.nblk = (nch + kMapBlock - 1) / kMapBlock;
     // csum, g0, d0, d1, hi, start, last (doubles) + end + nslow, prefix maps
     // (2 per chunk), block maps (4 per block), block starts + flags + outcomes
-    const size_t nd = 7 * nch + 2 + 2 * nch + 5 * c.nblk;
+    // + fine starts (two trajectories x 16 per chunk) when there are draws
+    const bool fine = k > 0 && c.clog == kChunkLog;
+    const size_t nd = 7 * nch + 2 + 2 * nch + 5 * c.nblk + (fine ? 2 * kFinePer * nch : 0);
     const size_t bytes = nd * sizeof(double) + nch * sizeof(int) + 64 + (size_t)k * sizeof(int64_t);
     int rc = ensure_scratch(s, bytes);
     if (rc) return rc;
@@ -705,6 +737,8 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     c.pmap = (long long *)(b + 7 * nch + 2);
     c.bmap = c.pmap + 2 * nch;
     c.sblock = (double *)(c.bmap + 4 * c.nblk);
+    c.fine0 = fine ? c.sblock + c.nblk : nullptr;
+    c.fine1 = fine ? c.fine0 + kFinePer * nch : nullptr;
     c.flags = (int *)(b + nd);
     c.dout = (int64_t *)((char *)c.flags + ((nch * sizeof(int) + 63) & ~(size_t)63));
     return QS_OK;
@@ -723,7 +757,7 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
         const uint64_t warps = (c.nch + 31) / 32;
         const unsigned blocks = (unsigned)((warps + kTrajWarps - 1) / kTrajWarps);
         k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
-            amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags);
+            amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
     }
     k_block_maps<<<(unsigned)c.nblk, kMapBlock, 0, s->stream>>>(c.nch, c.g0, c.d0, c.d1, c.flags, c.pmap,
                                                                  c.bmap);
@@ -754,11 +788,11 @@ static int draw(qs_state *s, const CdfScratch &c, const qs_pcg64 *rng, int64_t k
         if (s->prec == QS_DOUBLE)
             k_draws<<<grid, 128, 0, s->stream>>>(amps_d(s), c.nch, c.clog, 1ull << s->num_qubits,
                                                  c.start, c.last, c.end, gtotal, s_start, base, gdim,
-                                                 is_last, *rng, k, c.dout);
+                                                 is_last, *rng, k, c.dout, c.flags, c.fine0, c.fine1);
         else
             k_draws<<<grid, 128, 0, s->stream>>>(s->amps, c.nch, c.clog, 1ull << s->num_qubits,
                                                  c.start, c.last, c.end, gtotal, s_start, base, gdim,
-                                                 is_last, *rng, k, c.dout);
+                                                 is_last, *rng, k, c.dout, c.flags, c.fine0, c.fine1);
     }
     QS_CUDA(cudaGetLastError());
     int rc = ensure_pinned(s, sizeof(double));
