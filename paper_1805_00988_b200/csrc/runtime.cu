@@ -29,6 +29,12 @@ int cuda_fail(cudaError_t e, const char *what) {
 
 int ensure_scratch(qs_state *s, size_t bytes) {
     if (s->scratch_bytes >= bytes) return QS_OK;
+    // grow geometrically in 2-MiB steps: requests that creep up (k-dependent
+    // sample outputs) would otherwise reallocate (and synchronise) each time,
+    // and round sizes let the device buffer cache reuse blocks across handles
+    if (s->scratch_bytes && bytes < s->scratch_bytes + s->scratch_bytes / 2)
+        bytes = s->scratch_bytes + s->scratch_bytes / 2;
+    bytes = (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
     if (s->scratch) {
         QS_CUDA(cudaStreamSynchronize(s->stream));
         pool_free(s->device, s->scratch, s->scratch_bytes);
@@ -42,6 +48,9 @@ int ensure_scratch(qs_state *s, size_t bytes) {
 
 int ensure_pinned(qs_state *s, size_t bytes) {
     if (s->pinned_bytes >= bytes) return QS_OK;
+    if (s->pinned_bytes && bytes < s->pinned_bytes + s->pinned_bytes / 2)
+        bytes = s->pinned_bytes + s->pinned_bytes / 2;
+    bytes = (bytes + (64u << 10) - 1) & ~(size_t)((64u << 10) - 1);
     if (s->pinned) {
         QS_CUDA(cudaStreamSynchronize(s->stream));
         QS_CUDA(cudaFreeHost(s->pinned));
