@@ -119,8 +119,15 @@ const Driver &driver() {
 }
 
 // ---- code generation -----------------------------------------------------------
-constexpr int kJitLoopRun = 3;      // runs at least this long stay loops ...
-constexpr int kJitLoopMinRegs = 8;  // ... when each op touches at least 8 float4 registers
+// Runs of one variant at least kJitLoopRun long (each op touching at least
+// kJitLoopMinRegs float4 registers) may stay loops over the shared-memory op
+// table instead of straight-line code (smaller programs).  Measured on B200
+// the straight-line form is faster even when the program overflows the
+// instruction cache (QFT(28) 8.26 -> 8.14 ms, QFT(30) 35.3 -> 34.8 ms,
+// config 4 1002 -> 977 ms; 150 tile-tested phases 4.6 -> 4.1 ms), so loops
+// are off by default; QSB_JIT_LOOP_RUN=<n> turns them back on.
+constexpr int kJitLoopRun = 1 << 30;
+constexpr int kJitLoopMinRegs = 8;
 void hexf(std::string &out, float x) {
     uint32_t b;
     std::memcpy(&b, &x, 4);
@@ -181,10 +188,8 @@ std::string generate(const FParams &p, int K, int RB) {
         src += buf;
         for (int o = st.op_begin; o < st.op_end;) {
             const FOp &op = p.ops[o];
-            // a long run of one variant (the QFT's controlled phases on
-            // non-register bits) stays a loop over the shared-memory op
-            // table: straight-line copies of a 32-amplitude body per op would
-            // overflow the instruction cache
+            // optionally (QSB_JIT_LOOP_RUN, see kJitLoopRun) a long run of
+            // one variant stays a loop over the shared-memory op table
             int e = o + 1;
             while (e < st.op_end && p.ops[e].variant == op.variant && p.ops[e].reg_need == op.reg_need &&
                    p.ops[e].half_need == op.half_need)
