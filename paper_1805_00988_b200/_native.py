@@ -164,11 +164,24 @@ def device_count() -> int:
 
 
 def pcg_from_seed(seed) -> qs_pcg64:
-    """numpy default_rng(seed)'s PCG64 state (the reference's draw source, measure.py:81)."""
-    st = np.random.default_rng(seed).bit_generator.state["state"]
+    """numpy default_rng(seed)'s PCG64 state (the reference's draw source, measure.py:81).
+    A Generator / BitGenerator seed is snapshotted, not advanced: the caller
+    advances it with consume_draws() once the draws have been taken."""
+    bg = np.random.default_rng(seed).bit_generator
+    if not isinstance(bg, np.random.PCG64):
+        raise TypeError(f"sampling draws from PCG64 (numpy's default_rng); got {type(bg).__name__}")
+    st = bg.state["state"]
     s, inc = int(st["state"]), int(st["inc"])
     m = (1 << 64) - 1
     return qs_pcg64((s >> 64) & m, s & m, (inc >> 64) & m, inc & m)
+
+
+def consume_draws(seed, k: int) -> None:
+    """pairsim draws rng.random(k) from default_rng(seed) (measure.py:81-82, 97):
+    for a caller-owned Generator / BitGenerator that advances the caller's
+    stream by k 64-bit outputs; ints and None leave nothing to advance."""
+    if isinstance(seed, (np.random.Generator, np.random.BitGenerator)):
+        np.random.default_rng(seed).bit_generator.advance(int(k))
 
 
 def f32ptr(a: np.ndarray):

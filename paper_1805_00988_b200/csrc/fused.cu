@@ -78,12 +78,7 @@ template <int K, int RB>
 int launch_fused_k(qs_state *s, const FParams &p) {
     const size_t bufs = (size_t)kNB * (1u << (K - kLow)) * 33u * 16u;
     const size_t smem = bufs + (size_t)p.nops * sizeof(FOp);
-    static int configured = -1;
-    if (configured < (int)smem) {
-        QS_CUDA(cudaFuncSetAttribute(k_fused<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(bufs + kMaxOps * sizeof(FOp))));
-        configured = (int)(bufs + kMaxOps * sizeof(FOp));
-    }
+    if (int rc = ensure_smem_attr((const void *)k_fused<K, RB>, (int)(bufs + kMaxOps * sizeof(FOp)))) return rc;
     uint64_t grid = (uint64_t)s->num_sms * (uint64_t)ctas_per_sm(K);
     if (grid > p.ntiles) grid = p.ntiles;
     k_fused<K, RB><<<(unsigned)grid, (1 << (K - 1 - RB)) + 32, smem, s->stream>>>((float4 *)s->amps, p);
@@ -141,12 +136,7 @@ __global__ void __launch_bounds__(1024) k_small(float2 *__restrict__ amps,
 }
 
 int run_small(qs_state *s, const qs_op *ops, int nops) {
-    static bool configured = false;
-    if (!configured) {
-        QS_CUDA(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(8u << kSmallMaxQubits)));
-        configured = true;
-    }
+    if (int rc = ensure_smem_attr((const void *)k_small, (int)(8u << kSmallMaxQubits))) return rc;
     SParams p;
     std::memset(&p, 0, sizeof p);
     p.n = s->num_qubits;

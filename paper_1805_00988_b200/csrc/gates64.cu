@@ -17,6 +17,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 
 #include "common.cuh"
 #include "internal.h"
@@ -353,14 +354,10 @@ int run_fused_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op6
             return set_error(QS_ERR_VALUE, "phase op needs a == 1 and b == c == 0");
     }
     if (n <= kSmallMaxQubitsD) {
-        static bool configured = false;
-        if (!configured) {
-            QS_CUDA(cudaFuncSetAttribute(k_small_d, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(16u << kSmallMaxQubitsD)));
-            configured = true;
-        }
-        static SParamsD p;  // ~27 KB: keep it off the host stack
-        std::memset(&p, 0, sizeof p);
+        if (int rc = ensure_smem_attr((const void *)k_small_d, (int)(16u << kSmallMaxQubitsD))) return rc;
+        // ~27 KB: on the heap, one per call (concurrent callers on other handles)
+        std::unique_ptr<SParamsD> holder(new SParamsD());
+        SParamsD &p = *holder;
         p.n = n;
         const int threads = (1 << n) >= 2048 ? 1024 : ((1 << n) / 2 < 32 ? 32 : (1 << n) / 2);
         for (int base = 0; base < nops; base += kSmallMaxOpsD) {

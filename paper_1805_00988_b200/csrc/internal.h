@@ -25,6 +25,9 @@ struct qs_state {
     size_t ops_bytes;
     // fused-pass tile scheduler counter (lazily allocated, zero between launches)
     unsigned long long *tile_ctr;
+    // the register buffer was exported with cudaIpcGetMemHandle: other
+    // processes may still map it, so it is freed, never recycled by the pool
+    int ipc_exported;
 };
 
 namespace qsb {
@@ -36,6 +39,8 @@ inline uint64_t amp_bytes(const qs_state *s) { return s->prec == QS_DOUBLE ? 16u
 inline uint64_t state_bytes(const qs_state *s) { return amp_bytes(s) << s->num_qubits; }
 inline double2 *amps_d(const qs_state *s) { return reinterpret_cast<double2 *>(s->amps); }
 int cuda_fail(cudaError_t e, const char *what);
+// raise a kernel's max dynamic shared memory on the current device (once per size)
+int ensure_smem_attr(const void *fn, int bytes);
 
 // RAII guard: switch to the handle's device for the duration of a call.
 struct DeviceGuard {

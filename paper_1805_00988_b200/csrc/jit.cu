@@ -67,11 +67,8 @@ struct Nvrtc {
     nvrtcResult_t (*destroy)(nvrtcProgram_t *);
 };
 
-const Nvrtc &nvrtc() {
-    static Nvrtc n;
-    static bool tried = false;
-    if (tried) return n;
-    tried = true;
+Nvrtc load_nvrtc() {
+    Nvrtc n;
     const char *names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
     void *h = nullptr;
     for (const char *nm : names)
@@ -88,6 +85,12 @@ const Nvrtc &nvrtc() {
     return n;
 }
 
+// loaded once, thread-safe (function-local static initialisation)
+const Nvrtc &nvrtc() {
+    static const Nvrtc n = load_nvrtc();
+    return n;
+}
+
 // ---- driver entry points ------------------------------------------------------
 struct Driver {
     bool ok = false;
@@ -97,11 +100,8 @@ struct Driver {
     PFN_cuLaunchKernel_v4000 launch;
 };
 
-const Driver &driver() {
-    static Driver d;
-    static bool tried = false;
-    if (tried) return d;
-    tried = true;
+Driver load_driver() {
+    Driver d;
     auto sym = [](const char *name) -> void * {
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -115,6 +115,11 @@ const Driver &driver() {
     d.set_attr = (PFN_cuFuncSetAttribute_v9000)sym("cuFuncSetAttribute");
     d.launch = (PFN_cuLaunchKernel_v4000)sym("cuLaunchKernel");
     d.ok = d.load && d.get && d.set_attr && d.launch;
+    return d;
+}
+
+const Driver &driver() {
+    static const Driver d = load_driver();
     return d;
 }
 

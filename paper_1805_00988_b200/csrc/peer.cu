@@ -73,6 +73,7 @@ int qs_ipc_handle(qs_state *s, void *out) {
     DeviceGuard guard(s->device);
     cudaIpcMemHandle_t h;
     QS_CUDA(cudaIpcGetMemHandle(&h, s->amps));
+    s->ipc_exported = 1;
     std::memcpy(out, &h, sizeof h);
     return QS_OK;
 }

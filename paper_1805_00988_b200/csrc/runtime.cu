@@ -7,6 +7,8 @@
 
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -19,6 +21,23 @@ static thread_local std::string g_last_error;
 int set_error(int code, const std::string &msg) {
     g_last_error = msg;
     return code;
+}
+
+// cudaFuncSetAttribute applies to the current device's context only: track
+// the dynamic shared-memory limit already set per (kernel, device) and raise
+// it when a launch needs more (thread-safe; one entry per device a kernel
+// has run on).
+int ensure_smem_attr(const void *fn, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> done;
+    int dev = 0;
+    QS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    int &have = done[{fn, dev}];
+    if (have >= bytes) return QS_OK;
+    QS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+    return QS_OK;
 }
 
 int cuda_fail(cudaError_t e, const char *what) {
@@ -192,7 +211,10 @@ int qs_destroy(qs_state *s) {
     if (!s) return QS_OK;
     DeviceGuard guard(s->device);
     cudaStreamSynchronize(s->stream);  // the buffers may be recycled right away
-    pool_free(s->device, s->amps, state_bytes(s));
+    if (s->ipc_exported)
+        cudaFree(s->amps);
+    else
+        pool_free(s->device, s->amps, state_bytes(s));
     pool_free(s->device, s->scratch, s->scratch_bytes);
     if (s->ops_dev) cudaFree(s->ops_dev);
     if (s->tile_ctr) pool_free(s->device, s->tile_ctr, 256);  // zero again once its last pass finished

@@ -146,6 +146,10 @@ class CudaEngine:
     def probabilities(self) -> np.ndarray:
         return self.state.probabilities()
 
+    def close(self) -> None:
+        self._view = None
+        self.state.close()
+
     def norm_squared(self) -> float:
         return self.state.norm_squared()
 
@@ -369,6 +373,10 @@ class ShardedState:
         g = int(round(math.log2(world)))
         if 1 << g != world:
             raise ValueError("the shard count must be a power of two")
+        if chunk_amps < 1 or chunk_amps & (chunk_amps - 1):
+            # exchange chunks must tile the 2^(L-1)-amplitude half exactly, or
+            # the partners' send / receive sizes would differ
+            raise ValueError("chunk_amps must be a power of two")
         self.num_qubits = num_qubits
         self.layout = QubitLayout(num_qubits, g)
         self.engines = list(engines)
@@ -679,6 +687,7 @@ class ShardedState:
         L, dim = self.L, 1 << self.num_qubits
         outs = [eng.sample_shard(samples, rng, starts[r], total, r << L, dim, r == self.world - 1)
                 for eng, r in zip(self.engines, self.ranks)]
+        N.consume_draws(seed, samples)
         return self.transport.combine_max(outs)
 
     def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
@@ -700,3 +709,25 @@ class ShardedState:
     def synchronize(self) -> None:
         for eng in self.engines:
             eng.synchronize()
+
+    def close(self) -> None:
+        """Unmap the partners' shards (behind a barrier: no rank may still be
+        running a peer kernel on them), then free the local shards."""
+        if self._peers:
+            self.transport.peer_barrier(self.engines)
+            by_rank = dict(zip(self.ranks, self.engines))
+            for (r, _), ptr in self._peers.items():
+                if hasattr(by_rank[r], "close_peer") and not isinstance(self.transport, LocalTransport):
+                    by_rank[r].close_peer(ptr)
+        self._peers = None
+        for eng in self.engines:
+            if hasattr(eng, "close"):
+                eng.close()
+        self.engines = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False

@@ -69,10 +69,13 @@ class _Recording:
     def __enter__(self):
         import gc
 
-        # no garbage-collected State may free its buffer mid-recording
+        # no garbage-collected State may free its buffer mid-recording; gc is
+        # turned off only once the capture has started (a failed begin leaves
+        # the collector as it was)
+        h = self._state.handle
         self._gc = gc.isenabled()
+        N.check(N.lib().qs_begin_capture(h))
         gc.disable()
-        N.check(N.lib().qs_begin_capture(self._state.handle))
         return self
 
     def __exit__(self, exc_type, exc, tb):
@@ -315,6 +318,7 @@ class State:
         out = np.empty(int(samples), dtype=np.int64)
         rng = N.pcg_from_seed(seed)
         N.check(N.lib().qs_sample(self.handle, ctypes.byref(rng), int(samples), out.ctypes.data))
+        N.consume_draws(seed, samples)
         return out
 
     def cdf_extend(self, start: float) -> float:
@@ -346,6 +350,7 @@ class State:
         out = ctypes.c_int64()
         rng = N.pcg_from_seed(seed)
         N.check(N.lib().qs_measure_collapse(self.handle, ctypes.byref(rng), ctypes.byref(out)))
+        N.consume_draws(seed, 1)
         return int(out.value)
 
     def __repr__(self) -> str:
