@@ -17,9 +17,11 @@ logical qubit; the log2(N) gates on global qubits each trigger a qubit swap
 (each 2^30 amplitudes) per second summed over GPUs, so N=1 and N>1 values
 are directly comparable.
 
---impl reference times the reference CPU path (oracle/port.py, the numpy
-restatement of pairsim's ThreadExecutor sweep; /root/reference is absent on
-the GPU box) on the host cores, on a bounded sample of the same workload.
+--impl reference times the reference's own CPU path — pairsim, unmodified,
+pip-installed into baseline/_ref (git-ignored, travels to the GPU box;
+scripts/refbench.py), its apply_gate with a ThreadExecutor over every host
+core — on a bounded sample of the same workload (oracle/port.py, the numpy
+restatement, only if baseline/_ref is missing).
 """
 
 from __future__ import annotations
@@ -51,11 +53,15 @@ def _args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--qubits", type=int, default=N_QUBITS)
+    ap.add_argument("--qubits", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the fused-pass / config 1, 3, 4 measurements")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: a fixed 34-qubit register (--qubits overrides) over the N GPUs; "
+                         "reports seconds per H layer and per QFT")
+    ap.add_argument("--no-harness", action="store_true", help="skip the paper's Algorithm 2 harness in extras")
     return ap.parse_args()
 
 
@@ -143,71 +149,63 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------- CPU legs ----
-def cpu_sample(n: int, budget_s: float, threads: int):
-    """Time the numpy port of pairsim's sweep (oracle/port.py) on host cores.
-    Returns (gates, seconds, sample description)."""
-    from oracle import port
-    from paper_1805_00988_b200.gates import H
+# The reference's own CPU path: pairsim, unmodified, from baseline/_ref
+# (scripts/refbench.py); oracle/port.py when that is missing.
+CPU_TARGETS = [0, 29, 15, 3, 26, 7, 10, 11, 20, 1, 15, 28, 5, 19, 23, 27, 13, 9]
 
-    try:
-        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
-    except (ValueError, OSError):
-        avail = 0
-    # the reference sweep peaks near 4.5x the state bytes (SURVEY Appendix A.3)
-    while n > 20 and 4.6 * (8 << n) > 0.8 * avail:
+
+def cpu_sample(n: int, budget_s: float, threads: int):
+    """Time the reference sweep on host cores at the largest n <= the bench's
+    that fits host memory.  Returns (gates, seconds, n, ReferenceCPU description, kind)."""
+    from scripts.refbench import ReferenceCPU, fits
+
+    while n > 20 and not fits(n):
         n -= 1
-    amps = np.zeros(1 << n, dtype=np.complex64)
-    amps[0] = 1
-    ex = port.Executor(workers=threads)
-    targets = [0, n - 1, n // 2, 3, n - 4, 7, n // 3, 11, 2 * n // 3, 1, 15, n - 2, 5, 19, 23, 27, 13, 9]
-    port.apply_gate(amps, n // 2, H, ex)  # warm-up
+    r = ReferenceCPU(n, threads)
+    r.h(n // 2)  # warm-up
     t0 = time.perf_counter()
     gates = 0
-    while gates < 3 or (time.perf_counter() - t0 < budget_s and gates < len(targets)):
-        port.apply_gate(amps, targets[gates % len(targets)] % n, H, ex)
+    while gates < 3 or (time.perf_counter() - t0 < budget_s and gates < len(CPU_TARGETS)):
+        r.h(CPU_TARGETS[gates % len(CPU_TARGETS)] % n)
         gates += 1
     dt = time.perf_counter() - t0
-    ex.close()
-    return gates, dt, n
+    r.close()
+    return gates, dt, n, r.describe(), r.kind
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path
+    (pairsim.kernel.apply_gate with a ThreadExecutor over every host core),
+    one H sweep of the 30-qubit register per step, targets spread over 0..29
+    (stride 11, coprime with 30).  Rank 0 only under torchrun."""
     rank, world, _ = _dist_env()
     if rank != 0:
         return
-    threads = len(os.sched_getaffinity(0))
-    from oracle import port
-    from paper_1805_00988_b200.gates import H
+    from scripts.refbench import ReferenceCPU, cpu_model, fits, host_cores
 
-    n = args.qubits
-    try:
-        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
-    except (ValueError, OSError):
-        avail = 0
-    while n > 20 and 4.6 * (8 << n) > 0.8 * avail:
+    threads = host_cores()
+    n = args.qubits or N_QUBITS
+    while n > 20 and not fits(n):
         n -= 1
-    amps = np.zeros(1 << n, dtype=np.complex64)
-    amps[0] = 1
-    ex = port.Executor(workers=threads)
-    per_step = 1  # one H sweep per step: a bounded sample of the 30-gate layer
+    r = ReferenceCPU(n, threads)
     for w in range(args.warmup):
-        port.apply_gate(amps, w % n, H, ex)
+        r.h((w * 11) % n)
     t0 = time.perf_counter()
     for s in range(args.steps):
-        for g in range(per_step):
-            port.apply_gate(amps, (s * per_step + g) % n, H, ex)
+        r.h(((args.warmup + s) * 11) % n)
     dt = time.perf_counter() - t0
-    ex.close()
-    gates = args.steps * per_step
+    r.close()
+    gates = args.steps
     value = gates / dt
-    sample = (f"{gates} H sweeps on a {n}-qubit complex64 register (targets 0..{gates - 1} mod {n}), "
-              f"numpy port of pairsim ThreadExecutor with {threads} workers")
+    sample = (f"{gates} H sweeps on a {n}-qubit complex64 register (targets (11 k) mod {n}), "
+              f"{r.describe()}, host {cpu_model()} ({threads} cores)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64",
-        "data": "synthetic", "config": {"workload": "hlayer_sweep", "n_qubits": n, "gates_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "data": "synthetic", "config": {"workload": "hlayer_sweep", "n_qubits": n, "gates_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": r.kind, "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -226,7 +224,7 @@ def run_ours(args):
     from paper_1805_00988_b200.gates import H, m8
     from paper_1805_00988_b200 import _native as N
 
-    n = args.qubits
+    n = args.qubits or N_QUBITS
     st = State(n, device=local)
     stream = torch.cuda.ExternalStream(st.stream(), device=torch.device("cuda", local))
     L = N.lib()
@@ -282,7 +280,7 @@ def run_ours(args):
 
     extras = {}
     if not args.no_extras and rank == 0:
-        extras = run_extras(st, stream, n, cpu=not args.no_cpu)
+        extras = run_extras(st, stream, n, cpu=not args.no_cpu, harness=not args.no_harness)
 
     # ---- e2e through the C ABI with pinned host buffers -------------------
     e2e = None
@@ -342,12 +340,17 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = len(os.sched_getaffinity(0))
-        g, dt, ncpu = cpu_sample(n, 20.0, threads)
-        cpu = {"value": g / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{g} H sweeps on a {ncpu}-qubit register, oracle/port.py (numpy restatement of "
-                         f"pairsim's ThreadExecutor sweep, kernel.py:108-132) with {threads} workers, "
-                         f"{dt:.1f} s"}
+        from scripts.refbench import cpu_breadth, cpu_model, host_cores
+
+        threads = host_cores()
+        g, dt, ncpu, desc, kind = cpu_sample(n, 10.0, threads)
+        cpu = {"value": g / dt, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+               "sample": f"{g} H sweeps on a {ncpu}-qubit register (targets spread over 0..{ncpu - 1}), "
+                         f"{desc}, {dt:.1f} s"}
+        try:
+            cpu["breadth"] = cpu_breadth()
+        except Exception as exc:  # noqa: BLE001
+            cpu["breadth"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
         out = {
@@ -387,16 +390,11 @@ def run_sharded(args):
     from paper_1805_00988_b200.sharded import ShardedState
 
     rank, world, local = _dist_env()
-    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only in tests
-    torch.cuda.set_device(local)
-    import datetime
-
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local),
-                            timeout=datetime.timedelta(minutes=10))
+    local = init_dist()
     g = int(round(math.log2(world)))
     if 1 << g != world:
         raise SystemExit("--gpus must be a power of two")
-    L = args.qubits
+    L = args.qubits or N_QUBITS
     n = L + g
     st = ShardedState.distributed(n, device=local)
     eng = st.engines[0]
@@ -460,10 +458,16 @@ def run_sharded(args):
     extras = {}
     if not args.no_extras:
         extras["global_gates"] = run_global_gate_probe(n, local, world)
+        try:
+            eng.state.close()  # the weak-scaling register is done: room for the 34-qubit one
+            extras["strong34"] = measure_strong(34, world, local, 1, 1)
+        except Exception as exc:  # noqa: BLE001
+            extras["strong34"] = {"error": f"{type(exc).__name__}: {exc}"}
     if world >= 4 and not args.no_extras:
         extras["config5_hlayer_qft36"] = run_config5(st, eng, local, world)
+    line = None
     if rank == 0:
-        print(json.dumps({
+        line = json.dumps({
             "extras": extras,
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -477,8 +481,158 @@ def run_sharded(args):
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": None,
-        }))
+        })
+    finish_dist(line)
+
+
+def init_dist() -> int:
+    """One rank per GPU over NCCL.  The communicator is created eagerly
+    (device_id) with NCCL's INIT-subsystem INFO lines on (rank, nranks, cudaDev
+    per communicator) so the logs show every rank joined.  Returns the local
+    device."""
+    import datetime
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    _, _, local = _dist_env()
+    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only with QSB_BENCH_SHARE_GPU
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                            timeout=datetime.timedelta(minutes=10))
+    return local
+
+
+def finish_dist(line: str | None) -> None:
+    """Tear the communicators down on every rank, then let rank 0 print its
+    JSON line once no other rank can still write NCCL log lines to the shared
+    stdout (a handshake through the launcher's store, which outlives the
+    process group)."""
+    import torch.distributed as dist
+
+    from torch.distributed import distributed_c10d as c10d
+
+    rank, world, _ = _dist_env()
+    store = c10d._get_default_store()
+    dist.barrier()
     dist.destroy_process_group()
+    sys.stdout.flush()
+    store.add("qsb_bench_done", 1)
+    if rank == 0:
+        deadline = time.time() + 120
+        while store.add("qsb_bench_done", 0) < world and time.time() < deadline:
+            time.sleep(0.05)
+        print(line, flush=True)
+
+
+def measure_strong(n: int, world: int, local: int, steps: int, warmup: int) -> dict:
+    """ONE n-qubit register over the `world` GPUs (world = 1: one device
+    register): seconds per H layer (unfused: one sweep per qubit, global
+    qubits through qubit swaps), per fused H layer and per QFT(n) (fused
+    local passes + swaps, ShardedState.run).  CUDA events on each rank's
+    register stream, max over ranks.  Analytic check: QFT (no swaps) maps the
+    uniform state to |0>, so after H layer + QFT amplitude 0 must be ~1."""
+    import torch
+
+    from paper_1805_00988_b200 import _native as N
+    from paper_1805_00988_b200 import build_hadamard_layer, build_qft, fusion
+    from paper_1805_00988_b200.gates import H
+    from paper_1805_00988_b200.sharded import ShardedState
+
+    g = int(round(math.log2(world)))
+    N.lib().qs_release_cached(-1)
+    free_b, _ = torch.cuda.mem_get_info(local)
+    budget = max(1, free_b - (6 << 30))
+    if world > 1:
+        st = ShardedState.distributed(n, device=local, memory_budget=budget)
+    else:
+        st = ShardedState.virtual(n, 1, device=local, memory_budget=budget)
+    eng = st.engines[0]
+    stream = torch.cuda.ExternalStream(eng.state.stream(), device=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def timed(fn, reps):
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        barrier()
+        return a.elapsed_time(b) / 1e3 / reps
+
+    def layer():
+        for q in range(n):
+            st.apply_gate(H, q)
+
+    hl, qft = build_hadamard_layer(n), build_qft(n)
+    for _ in range(warmup):
+        layer()
+    swaps0 = st.swaps
+    t_layer = timed(layer, steps)
+    swaps = (st.swaps - swaps0) / steps
+    st.run(hl)
+    st.run(qft)  # queues the pass programs' compiles
+    fusion.jit_sync()
+    st.reset(0)
+    t_fused = timed(lambda: st.run(hl), 1)
+    t_qft = timed(lambda: st.run(qft), 1)
+    vals = [t_layer, t_fused, t_qft]
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor(vals, device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        vals = [float(x) for x in t.tolist()]
+    st.canonicalize()
+    a0 = complex(eng.state.amplitude(0)) if st.ranks[0] == 0 else None
+    out = {"n_qubits": n, "n_gpus": world, "shard_qubits": n - g, "hlayer_s": vals[0], "hlayer_fused_s": vals[1],
+           "qft_s": vals[2], "qft_gates": qft.gate_count(), "global_qubit_swaps_per_layer": swaps,
+           "timing": "CUDA events on each rank's register stream, max over ranks"}
+    if a0 is not None:
+        out["amp0_after_hlayer_qft"] = [a0.real, a0.imag]
+        out["analytic_check_ok"] = bool(abs(a0 - 1.0) < 1e-3)
+    st.close()
+    N.lib().qs_release_cached(-1)
+    return out
+
+
+def run_strong(args):
+    """--strong: the strong-scaling line (SURVEY 8(e) "Reporting"), value =
+    seconds per unfused H layer of ONE 34-qubit register (--qubits
+    overrides) over the N GPUs; the fused layer and QFT(n) ride along."""
+    import torch
+
+    rank, world, local = _dist_env()
+    n = args.qubits or 34
+    if world > 1:
+        local = init_dist()
+    else:
+        torch.cuda.set_device(local)
+    with ClockSampler(local) as clocks:
+        r = measure_strong(n, world, local, args.steps, args.warmup)
+    line = json.dumps({
+        "metric": f"seconds per H layer ({n} qubits, strong scaling)", "value": r["hlayer_s"], "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["hlayer_s"] * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": f"hlayer{n}_strong", "n_qubits": n, "shard_qubits": r["shard_qubits"],
+                   "parallelism": f"shard{world}" if world > 1 else "single",
+                   "global_qubit_swaps_per_layer": r["global_qubit_swaps_per_layer"]},
+        "strong": r, "gpu_launches": args.steps * n, "clocks": clocks.summary(),
+    })
+    if world > 1:
+        finish_dist(line if rank == 0 else None)
+    else:
+        print(line)
 
 
 def run_global_gate_probe(n, local, world, reps=3):
@@ -586,7 +740,7 @@ def run_config5(st_main, eng_main, local, world):
     return out
 
 
-def run_extras(st, stream, n, cpu=True):
+def run_extras(st, stream, n, cpu=True, harness=True):
     """Fused passes on the 30-qubit register, plus BASELINE configs 1, 3, 4."""
     import torch
 
@@ -660,22 +814,32 @@ def run_extras(st, stream, n, cpu=True):
     res["config1_hlayer20_probs"] = {"ms_wall": best * 1e3, "gates": 20,
                                      "note": "State(20).reset + 20 x h + probabilities() to host, best of 5"}
     if cpu:
-        from oracle import port
-        from paper_1805_00988_b200.gates import H
+        from scripts.refbench import ReferenceCPU, host_cores
 
-        ex = port.Executor(workers=len(os.sched_getaffinity(0)))
-        amps = np.zeros(1 << 20, np.complex64)
+        r = ReferenceCPU(20, host_cores())
         cbest = float("inf")
         for _ in range(3):
             t0 = time.perf_counter()
-            amps[:] = 0
-            amps[0] = 1
+            if r.kind == "reference":
+                r.state.amps[:] = 0
+                r.state.amps[0] = 1
+            else:
+                r.amps[:] = 0
+                r.amps[0] = 1
             for q in range(20):
-                port.apply_gate(amps, q, H, ex)
-            p = port.probabilities(amps)
+                r.h(q)
+            if r.kind == "reference":
+                from pairsim import measure as _pm
+
+                p = _pm.probabilities(r.state)
+            else:
+                from oracle import port
+
+                p = port.probabilities(r.amps)
             cbest = min(cbest, time.perf_counter() - t0)
-        ex.close()
-        res["config1_hlayer20_probs"]["cpu_port_ms"] = cbest * 1e3
+        r.close()
+        res["config1_hlayer20_probs"]["cpu_ms"] = cbest * 1e3
+        res["config1_hlayer20_probs"]["cpu_kind"] = r.kind
         res["config1_hlayer20_probs"]["probabilities_bit_identical"] = bool(p.tobytes() == probs.tobytes())
     s20.close()
 
@@ -809,6 +973,36 @@ def run_extras(st, stream, n, cpu=True):
     res["sharded_virtual_31q_2shards"] = {**sv, "note": "H layer over 31 qubits as 2 virtual shards on one "
                                           "B200 (host wall clock incl. per-gate syncs of the sharded layer)"}
 
+    # per-gate H sweeps at the CPU baseline's sizes (cpu_baseline.breadth)
+    per_n = {}
+    for nn in (20, 24, 26, 28):
+        sn = State(nn)
+        sn_stream = torch.cuda.ExternalStream(sn.stream())
+        for q in range(nn):
+            sn.h(q)
+        sn.flush()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(sn_stream)
+        for rep in range(5):
+            for q in range(nn):
+                sn.h(q)
+        b.record(sn_stream)
+        sn.flush()
+        ms = a.elapsed_time(b) / (5 * nn)
+        per_n[str(nn)] = {"h_ms": ms, "GBps": 16 * (1 << nn) / ms / 1e6}
+        sn.close()
+    per_n["30"] = {"h_ms": None, "note": "the headline (roofline.per_target_ms)"}
+    res["per_gate_by_n"] = {**per_n, "note": "H on every target, 5 layers, CUDA events; n <= 24 fits L2"}
+
+    if harness:
+        try:
+            from scripts.refbench import paper_harness
+
+            res["paper_algorithm2"] = paper_harness(max_qubits=20, samples=6)
+        except Exception as exc:  # noqa: BLE001
+            res["paper_algorithm2"] = {"error": f"{type(exc).__name__}: {exc}"}
+
     # config 4: 32-qubit layered random H/T/CX circuit, depth 20, fused
     try:
         s32 = State(32)
@@ -824,13 +1018,55 @@ def run_extras(st, stream, n, cpu=True):
                                      "pass_bytes": len(passes) * 16 * (1 << 32),
                                      "achieved_GBps": len(passes) * 16 * (1 << 32) / (ms / 1e3) / 1e9}
     s32.close()
+
+    # strong-scaling reference point: one 34-qubit register (128 GiB) on this GPU
+    try:
+        res["strong34"] = measure_strong(34, 1, torch.cuda.current_device(), 1, 1)
+    except Exception as exc:  # noqa: BLE001
+        res["strong34"] = {"error": f"{type(exc).__name__}: {exc}"}
     return res
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
+def _visible_gpus() -> int:
+    import torch
+
+    return torch.cuda.device_count()
 
 
 def main():
     args = _args()
     if args.impl == "reference":
         run_reference(args)
+        return
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: start N ranks (one
+        # process per GPU) under torch.distributed.run ourselves
+        have = _visible_gpus()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} GPU(s) are visible\n")
+            sys.exit(2)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    world = int(world_env or 1)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
+    if world > 1 and _visible_gpus() < world and os.environ.get("QSB_BENCH_SHARE_GPU") != "1":
+        sys.stderr.write(f"bench.py: {world} ranks but only {_visible_gpus()} GPU(s) are visible\n")
+        sys.exit(2)
+    if args.strong:
+        run_strong(args)
     else:
         run_ours(args)
 

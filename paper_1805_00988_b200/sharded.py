@@ -418,10 +418,10 @@ class ShardedState:
 
     @classmethod
     def virtual(cls, num_qubits: int, shards: int, device: int = 0, engine_factory=None,
-                peer_gates: bool | None = None):
+                peer_gates: bool | None = None, memory_budget: int | None = None):
         g = int(round(math.log2(shards)))
         L = num_qubits - g
-        make = engine_factory or (lambda L_: CudaEngine(L_, device))
+        make = engine_factory or (lambda L_: CudaEngine(L_, device, memory_budget=memory_budget))
         engines = [make(L) for _ in range(shards)]
         st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards, peer_gates=peer_gates)
         st.reset(0)
