@@ -377,6 +377,50 @@ __device__ __forceinline__ void phase_cs(float2 d, float4 (&v)[1 << RB]) {
     }
 }
 
+// Predicated forms for ops whose test involves LANE bits (generated
+// programs).  A divergent branch around each such op costs a BSSY/BSYNC
+// reconvergence and splits the basic blocks ptxas schedules; instead every
+// lane runs the body with an operand selected per lane:
+// * phase: multiply by d where the test holds and by exactly (1, 0)
+//   elsewhere: fma(1, re, -rn(0 * im)) == re and fma(1, im, rn(0 * re)) == im
+//   for every finite value (only the sign of a zero result can differ: the
+//   same freedom as the class shortcuts above), so the bits equal the
+//   branch form;
+// * swap (X / CX / CCX): select between the swapped and unswapped values.
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void phase_sel(bool on, float2 d, float4 (&v)[1 << RB]) {
+    const float2 e = make_float2(on ? d.x : 1.0f, on ? d.y : 0.0f);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if ((j & RNEED) != RNEED) continue;
+        if (!ODD) cmul_s(e, v[j].x, v[j].y);
+        cmul_s(e, v[j].z, v[j].w);
+    }
+}
+
+template <int T, int RNEED, bool ODD_ONLY, int RB>
+__device__ __forceinline__ void swap_sel(bool on, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (T >= 0 && (j & (1 << T))) continue;
+        if ((j & RNEED) != RNEED) continue;
+        if (T < 0) {  // the two halves of one unit
+            const float4 a = v[j];
+            v[j] = make_float4(on ? a.z : a.x, on ? a.w : a.y, on ? a.x : a.z, on ? a.y : a.w);
+        } else {
+            const int k = j | (1 << (T < 0 ? 0 : T));
+            const float4 a = v[j], b = v[k];
+            if (ODD_ONLY) {
+                v[j] = make_float4(a.x, a.y, on ? b.z : a.z, on ? b.w : a.w);
+                v[k] = make_float4(b.x, b.y, on ? a.z : b.z, on ? a.w : b.w);
+            } else {
+                v[j] = make_float4(on ? b.x : a.x, on ? b.y : a.y, on ? b.z : a.z, on ? b.w : a.w);
+                v[k] = make_float4(on ? a.x : b.x, on ? a.y : b.y, on ? a.z : b.z, on ? a.w : b.w);
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ uint64_t tile_base(uint64_t t, const FParams &p) {
     uint64_t r = 0;
     for (int i = 0; i < p.nruns; ++i)

@@ -142,29 +142,36 @@ void hexf(std::string &out, float x) {
 }
 
 // An op's thread / tile predicate as generated source: the uniform tests
-// (tile bits against the redux'd base `ub`, warp bits against `wid`) first,
-// the divergent lane test last; "" when the op applies everywhere.
-std::string op_test(const FOp &op) {
+// (tile bits against the redux'd base `ub`, warp bits against `wid`) and the
+// divergent lane test; "" when the op applies everywhere.
+std::string uniform_test(const FOp &op) {
     std::string test;
     char buf[96];
-    auto add = [&](const char *t) {
-        if (!test.empty()) test += " && ";
-        test += t;
-    };
     if (op.ext_need) {
         std::snprintf(buf, sizeof buf, "(ub & 0x%llxull) == 0x%llxull", (unsigned long long)op.ext_need,
                       (unsigned long long)op.ext_need);
-        add(buf);
+        test += buf;
     }
     if (op.tid_need & ~31u) {
         std::snprintf(buf, sizeof buf, "(wid & 0x%xu) == 0x%xu", op.tid_need & ~31u, op.tid_need & ~31u);
-        add(buf);
-    }
-    if (op.tid_need & 31u) {
-        std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need & 31u, op.tid_need & 31u);
-        add(buf);
+        if (!test.empty()) test += " && ";
+        test += buf;
     }
     return test;
+}
+
+std::string lane_test(const FOp &op) {
+    if (!(op.tid_need & 31u)) return "";
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "(tid & 0x%xu) == 0x%xu", op.tid_need & 31u, op.tid_need & 31u);
+    return buf;
+}
+
+std::string op_test(const FOp &op) {
+    std::string u = uniform_test(op), l = lane_test(op);
+    if (u.empty()) return l;
+    if (l.empty()) return u;
+    return u + " && " + l;
 }
 
 std::string generate(const FParams &p, int K, int RB) {
@@ -174,6 +181,10 @@ std::string generate(const FParams &p, int K, int RB) {
     if (const char *e = std::getenv("QSB_JIT_PHASE")) phase_mode = std::atoi(e);
     int loop_run = kJitLoopRun;
     if (const char *e = std::getenv("QSB_JIT_LOOP_RUN")) loop_run = std::atoi(e);
+    // ops under a LANE test: 1 (default) predicated selection (phase_sel /
+    // swap_sel: no divergent branch), 0 a branch around the body
+    int sel_mode = 1;
+    if (const char *e = std::getenv("QSB_JIT_SEL")) sel_mode = std::atoi(e);
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 200);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
@@ -218,9 +229,32 @@ std::string generate(const FParams &p, int K, int RB) {
             }
             for (; o < e; ++o) {
                 const FOp &op = p.ops[o];
-                const std::string test = op_test(op);
+                const std::string test = op_test(op), utest = uniform_test(op), ltest = lane_test(op);
+                const bool is_phase = op.variant >= kPhaseVariant;
+                const int cls = is_phase ? -1 : (op.variant / 2) % 4;
+                if (sel_mode && !ltest.empty() && (is_phase || cls == kSwap)) {
+                    // predicated selection under the lane test, branch only on
+                    // the (warp-uniform) rest
+                    src += utest.empty() ? "      {" : "      if (" + utest + ") {";
+                    if (is_phase) {
+                        const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
+                        std::snprintf(buf, sizeof buf, " phase_sel<%d, %s, RB>(%s, make_float2(", R,
+                                      odd ? "true" : "false", ltest.c_str());
+                        src += buf;
+                        hexf(src, op.m[6]);
+                        src += ", ";
+                        hexf(src, op.m[7]);
+                        src += "), v); }\n";
+                    } else {
+                        const int slot = (op.variant / 2) / 4 - 1;
+                        std::snprintf(buf, sizeof buf, " swap_sel<%d, %u, %s, RB>(%s, v); }\n", slot, op.reg_need,
+                                      op.half_need ? "true" : "false", ltest.c_str());
+                        src += buf;
+                    }
+                    continue;
+                }
                 src += test.empty() ? "      {" : "      if (" + test + ") {";
-                if (op.variant >= kPhaseVariant) {
+                if (is_phase) {
                     const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
                     const bool scalar = phase_mode == 2 || (phase_mode == 1 && !test.empty());
                     std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(make_float2(", scalar ? "phase_cs" : "phase_ct", R,
@@ -231,7 +265,7 @@ std::string generate(const FParams &p, int K, int RB) {
                     hexf(src, op.m[7]);
                     src += "), v); }\n";
                 } else {
-                    const int cls = (op.variant / 2) % 4, slot = (op.variant / 2) / 4 - 1;
+                    const int slot = (op.variant / 2) / 4 - 1;
                     src += " const float m[8] = {";
                     for (int i = 0; i < 8; ++i) {
                         if (i) src += ", ";
