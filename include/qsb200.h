@@ -217,6 +217,14 @@ int qs_ipc_close(int device, void *ptr);
  * on other global qubits are rank predicates of the caller).  The caller
  * orders the two shards' streams before and after. */
 int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const float m[8]);
+/* Qubit-swap exchange over peer memory (the data movement of a global-target
+ * swap, sharded.py's exchange_plan): amplitudes [own_offset, own_offset +
+ * count) of this shard trade places with [peer_offset, peer_offset + count)
+ * of the partner's, in one kernel on this handle's stream (16-B accesses, no
+ * staging buffer).  Partners split the exchanged range between them and call
+ * it concurrently on disjoint parts; the caller orders both streams before
+ * and after. */
+int qs_swap_peer(qs_state *s, void *peer_amps, uint64_t own_offset, uint64_t peer_offset, uint64_t count);
 
 #ifdef __cplusplus
 }

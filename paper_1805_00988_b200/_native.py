@@ -34,7 +34,7 @@ EXPORTS = (
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
-    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_jit_sync",
+    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_swap_peer", "qs_jit_sync",
     "qs_jit_shutdown", "qs_begin_capture", "qs_end_capture", "qs_graph_launch", "qs_graph_destroy",
 )
 
@@ -108,6 +108,7 @@ def _declare(L):
         "qs_ipc_open": ([i32, vp, ctypes.POINTER(vp)], i32),
         "qs_ipc_close": ([i32, vp], i32),
         "qs_apply_gate_peer": ([vp, vp, i32, u64, f32p], i32),
+        "qs_swap_peer": ([vp, vp, u64, u64, u64], i32),
         "qs_jit_sync": ([i32], i32),
         "qs_jit_shutdown": ([], i32),
         "qs_begin_capture": ([vp], i32),

@@ -319,6 +319,7 @@ __device__ __forceinline__ void apply_run(int variant, const FOp *ops, int len, 
 
 // Ahead-of-time program: walks the op table staged in shared memory.
 struct Interp {
+    static constexpr bool kPlanar = false;
     template <int RB>
     static __device__ __forceinline__ void run(int, const FStage &st, const FOp *sops, uint32_t tid,
                                                uint64_t base, float, float4 (&v)[1 << RB]) {
@@ -413,6 +414,125 @@ __device__ __forceinline__ void swap_sel(bool on, float4 (&v)[1 << RB]) {
             if (ODD_ONLY) {
                 v[j] = make_float4(a.x, a.y, on ? b.z : a.z, on ? b.w : a.w);
                 v[k] = make_float4(b.x, b.y, on ? a.z : b.z, on ? a.w : b.w);
+            } else {
+                v[j] = make_float4(on ? b.x : a.x, on ? b.y : a.y, on ? b.z : a.z, on ? b.w : a.w);
+                v[k] = make_float4(on ? a.x : b.x, on ? a.y : b.y, on ? a.z : b.z, on ? a.w : b.w);
+            }
+        }
+    }
+}
+
+// ---- planar register layout (generated programs, phase-heavy passes) --------
+// A 16-B unit holds two amplitudes (local qubit 0 = the half): interleaved
+// (re0, im0, re1, im1) in memory.  Planar programs keep each unit as
+// (re0, re1, im0, im1) in registers, so the real parts of both amplitudes
+// form one packed register pair and the imaginary parts another: a complex
+// product of both amplitudes is then four packed instructions (FMUL2 x 2,
+// FFMA2 x 2) instead of six or eight, with every lane the same IEEE
+// operation as the scalar form (bit-identical).  The units are transposed
+// once after the first stage's load and back before the last stage's store;
+// intermediate stages keep the planar order in shared memory (the unit
+// addresses do not change).
+__device__ __forceinline__ float4 to_planar(float4 u) { return make_float4(u.x, u.z, u.y, u.w); }
+__device__ __forceinline__ float4 from_planar(float4 u) { return make_float4(u.x, u.z, u.y, u.w); }
+
+// both halves multiplied by d: re' = fma(dx, re, -rn(dy im)), im' = fma(dx, im, rn(dy re))
+__device__ __forceinline__ float4 pcmul2(float2 d, float4 u) {
+    const float2 re = make_float2(u.x, u.y), im = make_float2(u.z, u.w);
+    const float2 tr = f2mul(make_float2(-d.y, -d.y), im), ti = f2mul(make_float2(d.y, d.y), re);
+    const float2 nr = f2fma(make_float2(d.x, d.x), re, tr), ni = f2fma(make_float2(d.x, d.x), im, ti);
+    return make_float4(nr.x, nr.y, ni.x, ni.y);
+}
+
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void pphase(float2 d, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if ((j & RNEED) != RNEED) continue;
+        if (ODD)
+            cmul_s(d, v[j].y, v[j].w);  // the odd half only: (re1, im1)
+        else
+            v[j] = pcmul2(d, v[j]);
+    }
+}
+
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void pphase_sel(bool on, float2 d, float4 (&v)[1 << RB]) {
+    pphase<RNEED, ODD, RB>(make_float2(on ? d.x : 1.0f, on ? d.y : 0.0f), v);
+}
+
+// Packed class bodies on a planar unit pair (a, b) = both halves of the
+// pair's two amplitudes: same per-lane arithmetic as pair_cls.
+template <int CLS>
+__device__ __forceinline__ void ppair_cls(const float *m, float one, float4 &a, float4 &b) {
+    const float2 ar = make_float2(a.x, a.y), ai = make_float2(a.z, a.w);
+    const float2 br = make_float2(b.x, b.y), bi = make_float2(b.z, b.w);
+    float2 nar, nai, nbr, nbi;
+    if (CLS == kCplx) {
+        const float4 p = pcmul2(make_float2(m[0], m[1]), a), q = pcmul2(make_float2(m[2], m[3]), b);
+        const float4 r = pcmul2(make_float2(m[6], m[7]), b), t = pcmul2(make_float2(m[4], m[5]), a);
+        nar = f2add(make_float2(p.x, p.y), make_float2(q.x, q.y));
+        nai = f2add(make_float2(p.z, p.w), make_float2(q.z, q.w));
+        nbr = f2add(make_float2(r.x, r.y), make_float2(t.x, t.y));
+        nbi = f2add(make_float2(r.z, r.w), make_float2(t.z, t.w));
+    } else if (CLS == kReal) {
+        nar = rsum(rmul(m[0], ar), rmul(m[2], br), one);
+        nai = rsum(rmul(m[0], ai), rmul(m[2], bi), one);
+        nbr = rsum(rmul(m[6], br), rmul(m[4], ar), one);
+        nbi = rsum(rmul(m[6], bi), rmul(m[4], ai), one);
+    } else if (CLS == kHlike) {
+        const float2 pr = rmul(m[0], ar), pi = rmul(m[0], ai), qr = rmul(m[2], br), qi = rmul(m[2], bi);
+        nar = rsum(pr, qr, one);
+        nai = rsum(pi, qi, one);
+        nbr = csub(pr, qr, one);
+        nbi = csub(pi, qi, one);
+    } else {
+        nar = br, nai = bi, nbr = ar, nbi = ai;
+    }
+    a = make_float4(nar.x, nar.y, nai.x, nai.y);
+    b = make_float4(nbr.x, nbr.y, nbi.x, nbi.y);
+}
+
+// pair op on planar registers: T = register slot of the target (-1: the
+// half), RNEED register-bit controls, ODD_ONLY a control on the half bit
+template <int T, int CLS, int RNEED, bool ODD_ONLY, int RB>
+__device__ __forceinline__ void ppair(const float (&m)[8], float one, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (T >= 0 && (j & (1 << T))) continue;
+        if ((j & RNEED) != RNEED) continue;
+        if (T < 0) {  // the two halves of one unit: (re0, im0) and (re1, im1)
+            float2 a = make_float2(v[j].x, v[j].z), b = make_float2(v[j].y, v[j].w);
+            pair_cls<CLS>(m, one, a, b);
+            v[j] = make_float4(a.x, b.x, a.y, b.y);
+        } else {
+            const int k = j | (1 << (T < 0 ? 0 : T));
+            if (ODD_ONLY) {
+                float2 a = make_float2(v[j].y, v[j].w), b = make_float2(v[k].y, v[k].w);
+                pair_cls<CLS>(m, one, a, b);
+                v[j].y = a.x, v[j].w = a.y, v[k].y = b.x, v[k].w = b.y;
+            } else {
+                ppair_cls<CLS>(m, one, v[j], v[k]);
+            }
+        }
+    }
+}
+
+template <int T, int RNEED, bool ODD_ONLY, int RB>
+__device__ __forceinline__ void pswap_sel(bool on, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if (T >= 0 && (j & (1 << T))) continue;
+        if ((j & RNEED) != RNEED) continue;
+        if (T < 0) {
+            const float4 a = v[j];  // (re0, re1, im0, im1) -> (re1, re0, im1, im0)
+            v[j] = make_float4(on ? a.y : a.x, on ? a.x : a.y, on ? a.w : a.z, on ? a.z : a.w);
+        } else {
+            const int k = j | (1 << (T < 0 ? 0 : T));
+            const float4 a = v[j], b = v[k];
+            if (ODD_ONLY) {
+                v[j] = make_float4(a.x, on ? b.y : a.y, a.z, on ? b.w : a.w);
+                v[k] = make_float4(b.x, on ? a.y : b.y, b.z, on ? a.w : b.w);
             } else {
                 v[j] = make_float4(on ? b.x : a.x, on ? b.y : a.y, on ? b.z : a.z, on ? b.w : a.w);
                 v[k] = make_float4(on ? a.x : b.x, on ? a.y : b.y, on ? a.z : b.z, on ? a.w : b.w);
@@ -619,7 +739,19 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                     if (j & (1 << r)) a += rs[r];
                 v[j] = *reinterpret_cast<const V *>(tile + a);
             }
+            if constexpr (Prog::kPlanar && UnitTraits<V>::kHalf) {
+                if (s == 0) {
+#pragma unroll
+                    for (int j = 0; j < (1 << RB); ++j) v[j] = to_planar(v[j]);
+                }
+            }
             if (!p.dry) Prog::template run<RB>(s, st, sops, (uint32_t)tid, base, p.one, v);
+            if constexpr (Prog::kPlanar && UnitTraits<V>::kHalf) {
+                if (s + 1 == p.nstages) {
+#pragma unroll
+                    for (int j = 0; j < (1 << RB); ++j) v[j] = from_planar(v[j]);
+                }
+            }
 #pragma unroll
             for (int j = 0; j < (1 << RB); ++j) {
                 uint32_t a = pb;

@@ -185,9 +185,19 @@ std::string generate(const FParams &p, int K, int RB) {
     // swap_sel: no divergent branch), 0 a branch around the body
     int sel_mode = 1;
     if (const char *e = std::getenv("QSB_JIT_SEL")) sel_mode = std::atoi(e);
+    // planar register layout (fused_dev.cuh: pphase / ppair): 2 (default)
+    // for phase-dominated passes, 1 always, 0 never
+    int planar_mode = 2;
+    if (const char *e = std::getenv("QSB_JIT_PLANAR")) planar_mode = std::atoi(e);
+    int nphase = 0;
+    for (int o = 0; o < p.nops; ++o) nphase += p.ops[o].variant >= kPhaseVariant;
+    const bool planar = planar_mode == 1 || (planar_mode == 2 && 2 * nphase > p.nops);
+    if (planar) loop_run = 1 << 30;  // the op-table loops (run_phase / run_pair) are interleaved-layout code
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 200);
-    src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
+    src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n";
+    src += planar ? "  static constexpr bool kPlanar = true;\n" : "  static constexpr bool kPlanar = false;\n";
+    src += "  template <int RB>\n"
            "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *ops, uint32_t tid,\n"
            "      uint64_t base, float one, float4 (&v)[1 << RB]) {\n"
            // warp index and tile base through redux.sync: values ptxas knows
@@ -238,8 +248,8 @@ std::string generate(const FParams &p, int K, int RB) {
                     src += utest.empty() ? "      {" : "      if (" + utest + ") {";
                     if (is_phase) {
                         const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
-                        std::snprintf(buf, sizeof buf, " phase_sel<%d, %s, RB>(%s, make_float2(", R,
-                                      odd ? "true" : "false", ltest.c_str());
+                        std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(%s, make_float2(",
+                                      planar ? "pphase_sel" : "phase_sel", R, odd ? "true" : "false", ltest.c_str());
                         src += buf;
                         hexf(src, op.m[6]);
                         src += ", ";
@@ -247,7 +257,8 @@ std::string generate(const FParams &p, int K, int RB) {
                         src += "), v); }\n";
                     } else {
                         const int slot = (op.variant / 2) / 4 - 1;
-                        std::snprintf(buf, sizeof buf, " swap_sel<%d, %u, %s, RB>(%s, v); }\n", slot, op.reg_need,
+                        std::snprintf(buf, sizeof buf, " %s<%d, %u, %s, RB>(%s, v); }\n",
+                                      planar ? "pswap_sel" : "swap_sel", slot, op.reg_need,
                                       op.half_need ? "true" : "false", ltest.c_str());
                         src += buf;
                     }
@@ -257,8 +268,8 @@ std::string generate(const FParams &p, int K, int RB) {
                 if (is_phase) {
                     const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
                     const bool scalar = phase_mode == 2 || (phase_mode == 1 && !test.empty());
-                    std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(make_float2(", scalar ? "phase_cs" : "phase_ct", R,
-                                  odd ? "true" : "false");
+                    std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(make_float2(",
+                                  planar ? "pphase" : (scalar ? "phase_cs" : "phase_ct"), R, odd ? "true" : "false");
                     src += buf;
                     hexf(src, op.m[6]);
                     src += ", ";
@@ -271,8 +282,8 @@ std::string generate(const FParams &p, int K, int RB) {
                         if (i) src += ", ";
                         hexf(src, op.m[i]);
                     }
-                    std::snprintf(buf, sizeof buf, "}; pair_ct<%d, %d, %u, %s, RB>(m, one, v); }\n", slot, cls,
-                                  op.reg_need, op.half_need ? "true" : "false");
+                    std::snprintf(buf, sizeof buf, "}; %s<%d, %d, %u, %s, RB>(m, one, v); }\n",
+                                  planar ? "ppair" : "pair_ct", slot, cls, op.reg_need, op.half_need ? "true" : "false");
                     src += buf;
                 }
             }
@@ -302,7 +313,8 @@ void hexd(std::string &out, double x) {
 std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 400);
-    src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n  template <int RB>\n"
+    src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n"
+           "  static constexpr bool kPlanar = false;\n  template <int RB>\n"
            "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *, uint32_t tid,\n"
            "      uint64_t base, float, double2 (&v)[1 << RB]) {\n"
            "    const uint32_t wid = __reduce_or_sync(0xffffffffu, tid & ~31u);\n"

@@ -59,6 +59,88 @@ __global__ void __launch_bounds__(256) k_peer_pair(float2 *__restrict__ own, flo
     }
 }
 
+// The same pair update on 16-B units (two amplitudes, local bit 0 free): one
+// 16-B access per amplitude pair and side instead of two 8-B ones, so each
+// NVLink request carries twice the payload.  Items enumerate units; the
+// fixed bits (controls, the split bit) are deposited into unit indices.
+template <int U>
+__global__ void __launch_bounds__(256) k_peer_pair16(float4 *__restrict__ own, float4 *__restrict__ peer,
+                                                     uint64_t nitems, FixedBits fb, uint64_t set_mask,
+                                                     int own_is_a, Gate2 g) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = tid; base < nitems; base += nthreads * U) {
+        float4 x[U], y[U];
+        uint64_t idx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t item = base + u * nthreads;
+            idx[u] = deposit(item, fb) | set_mask;
+            if (item < nitems) {
+                x[u] = __ldcs(own + idx[u]);
+                y[u] = __ldcg(peer + idx[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (base + u * nthreads >= nitems) continue;
+            const float4 a = own_is_a ? x[u] : y[u], b = own_is_a ? y[u] : x[u];
+            float2 a0 = make_float2(a.x, a.y), a1 = make_float2(a.z, a.w);
+            float2 b0 = make_float2(b.x, b.y), b1 = make_float2(b.z, b.w);
+            pair_update(g, a0, b0);
+            pair_update(g, a1, b1);
+            const float4 na = make_float4(a0.x, a0.y, a1.x, a1.y), nb = make_float4(b0.x, b0.y, b1.x, b1.y);
+            __stcs(own + idx[u], own_is_a ? na : nb);
+            __stcg(peer + idx[u], own_is_a ? nb : na);
+        }
+    }
+}
+
+// Qubit-swap exchange over peer memory: own[i] <-> peer[i] for i < n units
+// of 16 B (two complex64 amplitudes).  Both partners run it at once on
+// disjoint halves of the exchanged range, so the swap is one pass with no
+// staging buffer and no copy-back (the NCCL path stages the received half
+// and copies it into place: an extra half-shard of HBM traffic).
+template <int U>
+__global__ void __launch_bounds__(256) k_peer_swap(float4 *__restrict__ own, float4 *__restrict__ peer,
+                                                   uint64_t n) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = tid; base < n; base += nthreads * U) {
+        float4 x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * nthreads;
+            if (i < n) {
+                x[u] = __ldcs(own + i);
+                y[u] = __ldcg(peer + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * nthreads;
+            if (i < n) {
+                __stcs(own + i, y[u]);
+                __stcg(peer + i, x[u]);
+            }
+        }
+    }
+}
+
+__global__ void k_peer_swap8(float2 *__restrict__ own, float2 *__restrict__ peer, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float2 a = own[i], b = peer[i];
+        own[i] = b;
+        peer[i] = a;
+    }
+}
+
+unsigned grid_for(const qs_state *s, uint64_t items, int per_thread) {
+    uint64_t blocks = (items + 256ull * per_thread - 1) / (256ull * per_thread);
+    if (blocks > (uint64_t)s->num_sms * 8) blocks = (uint64_t)s->num_sms * 8;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
 }  // namespace
 
 }  // namespace qsb
@@ -126,17 +208,42 @@ int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl
             pos[j] = pos[j - 1];
             pos[j - 1] = t;
         }
-    FixedBits fb;
-    fb.n = np;
-    for (int i = 0; i < kMaxFixed; ++i) fb.pos[i] = i < np ? pos[i] : 0;
-    const uint64_t nitems = 1ull << (L - np);
     DeviceGuard guard(s->device);
     constexpr int U = 4;
-    uint64_t blocks = (nitems + 256ull * U - 1) / (256ull * U);
-    if (blocks > (uint64_t)s->num_sms * 8) blocks = (uint64_t)s->num_sms * 8;
-    if (blocks < 1) blocks = 1;
-    k_peer_pair<U><<<(unsigned)blocks, 256, 0, s->stream>>>(s->amps, (float2 *)peer_amps, nitems, fb, set_mask,
-                                                             own_is_a, gate_from(m));
+    const bool wide = np == 0 || pos[0] > 0;  // local bit 0 free: 16-B units
+    FixedBits fb;
+    fb.n = np;
+    for (int i = 0; i < kMaxFixed; ++i) fb.pos[i] = i < np ? pos[i] - (wide ? 1 : 0) : 0;
+    const Gate2 g = gate_from(m);
+    if (wide) {
+        const uint64_t nitems = 1ull << (L - 1 - np);
+        k_peer_pair16<U><<<grid_for(s, nitems, U), 256, 0, s->stream>>>(
+            (float4 *)s->amps, (float4 *)peer_amps, nitems, fb, set_mask >> 1, own_is_a, g);
+    } else {
+        const uint64_t nitems = 1ull << (L - np);
+        k_peer_pair<U><<<grid_for(s, nitems, U), 256, 0, s->stream>>>(s->amps, (float2 *)peer_amps, nitems, fb,
+                                                                       set_mask, own_is_a, g);
+    }
+    QS_CUDA(cudaGetLastError());
+    return QS_OK;
+}
+
+int qs_swap_peer(qs_state *s, void *peer_amps, uint64_t own_offset, uint64_t peer_offset, uint64_t count) {
+    if (!s) return set_error(QS_ERR_NULL, "null qs_state handle");
+    if (!peer_amps) return set_error(QS_ERR_NULL, "null peer buffer");
+    if (s->prec != QS_SINGLE) return set_error(QS_ERR_VALUE, "peer swaps need complex64 shards");
+    const uint64_t dim = 1ull << s->num_qubits;
+    if (own_offset > dim || count > dim - own_offset) return set_error(QS_ERR_INDEX, "swap range out of bounds");
+    if (count == 0) return QS_OK;
+    DeviceGuard guard(s->device);
+    float2 *own = s->amps + own_offset, *peer = (float2 *)peer_amps + peer_offset;
+    if (((own_offset | peer_offset | count) & 1ull) == 0) {
+        constexpr int U = 4;
+        const uint64_t n = count >> 1;
+        k_peer_swap<U><<<grid_for(s, n, U), 256, 0, s->stream>>>((float4 *)own, (float4 *)peer, n);
+    } else {
+        k_peer_swap8<<<grid_for(s, count, 1), 256, 0, s->stream>>>(own, peer, count);
+    }
     QS_CUDA(cudaGetLastError());
     return QS_OK;
 }

@@ -184,6 +184,9 @@ class CudaEngine:
     def close_peer(self, ptr: int) -> None:
         N.lib().qs_ipc_close(self.device, ptr)
 
+    def swap_peer(self, peer, own_off: int, peer_off: int, count: int) -> None:
+        N.check(N.lib().qs_swap_peer(self.state.handle, peer, int(own_off), int(peer_off), int(count)))
+
     def peer_gate(self, peer, own_is_a: bool, ctrl_mask: int, m: np.ndarray) -> None:
         mm = np.ascontiguousarray(m, dtype=np.float32)
         N.check(N.lib().qs_apply_gate_peer(self.state.handle, peer, int(bool(own_is_a)), int(ctrl_mask),
@@ -253,24 +256,44 @@ class DistTransport:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self._staging = None
+        # send/recv of device tensors needs NCCL; a gloo control plane with
+        # CUDA shards moves data through mapped peer memory instead
+        self.moves_device_buffers = dist.get_backend(group) == "nccl"
 
     def exchange(self, engines, rank_bit: int, L: int, chunk: int) -> None:
+        """NCCL send/recv of the half-shard in chunks through two staging
+        buffers: chunk k+1's transfer is in flight while chunk k is copied
+        into place (the send of a chunk and the receive into the same
+        addresses cannot alias, hence the staging)."""
         dist = self.dist
         (eng,) = engines
         partner, off, cnt = exchange_plan(self.rank, rank_bit, L)
         eng.comm_begin()
         v = eng.view()
         step = min(cnt, chunk)
-        if self._staging is None or self._staging.numel() < 2 * step or self._staging.device != v.device:
-            self._staging = v.new_empty(2 * step)
-        stg = self._staging[: 2 * step]
+        nbuf = 2 if cnt > step else 1
+        if self._staging is None or self._staging.numel() < 2 * step * nbuf or self._staging.device != v.device:
+            self._staging = v.new_empty(2 * step * nbuf)
         peer = dist.get_global_rank(self.group, partner) if self.group is not None else partner
-        for c in range(off, off + cnt, step):
+        starts = list(range(off, off + cnt, step))
+
+        def post(i):
+            c = starts[i]
             mine = v[2 * c: 2 * (c + step)]
+            stg = self._staging[2 * step * (i % nbuf): 2 * step * (i % nbuf + 1)]
             ops = [dist.P2POp(dist.isend, mine, peer, self.group), dist.P2POp(dist.irecv, stg, peer, self.group)]
-            for w in dist.batch_isend_irecv(ops):
+            return dist.batch_isend_irecv(ops), mine, stg
+
+        cur = post(0)
+        for i in range(len(starts)):
+            # posted after chunk i-1's copy-back (stream order protects its
+            # staging buffer), before chunk i's
+            nxt = post(i + 1) if i + 1 < len(starts) else None
+            works, mine, stg = cur
+            for w in works:
                 w.wait()
             mine.copy_(stg)
+            cur = nxt
         eng.comm_end()
 
     def peer_setup(self, engines, ranks, g):
@@ -369,7 +392,7 @@ class ShardedState:
     """A 2^n register over 2^g shards (QCGPU-style gate API)."""
 
     def __init__(self, num_qubits: int, engines, transport, ranks, world: int,
-                 chunk_amps: int = 1 << 26, peer_gates: bool | None = None):
+                 chunk_amps: int = 1 << 26, peer_gates: bool | None = None, exchange: str | None = None):
         g = int(round(math.log2(world)))
         if 1 << g != world:
             raise ValueError("the shard count must be a power of two")
@@ -392,14 +415,29 @@ class ShardedState:
             import os
 
             peer_gates = os.environ.get("QSB_SHARD_PEER", "0") == "1"
-        self.peer_gates = bool(peer_gates) and g > 0 and all(hasattr(e, "peer_gate") for e in self.engines)
+        can_peer = g > 0 and all(hasattr(e, "peer_gate") for e in self.engines)
+        self.peer_gates = bool(peer_gates) and can_peer
+        # Qubit-swap data movement: "nccl" (transport send/recv; in-process
+        # copies for virtual shards) or "peer" (qs_swap_peer: one kernel per
+        # partner over mapped peer memory, no staging).  Default: "peer" when
+        # the transport cannot move device buffers itself (gloo control
+        # plane with CUDA shards), else QSB_SHARD_EXCHANGE or "nccl".
+        if exchange is None:
+            import os
+
+            exchange = os.environ.get("QSB_SHARD_EXCHANGE") or ("peer" if can_peer and not getattr(
+                transport, "moves_device_buffers", True) else "nccl")
+        if exchange not in ("nccl", "peer"):
+            raise ValueError("exchange must be 'nccl' or 'peer'")
+        self.exchange = exchange if can_peer else "nccl"
         self._peers = None
         self.peer_gate_count = 0
+        self.peer_swaps = 0
 
     # ---- constructors ------------------------------------------------------
     @classmethod
     def distributed(cls, num_qubits: int, group=None, device: int | None = None, engine_factory=None,
-                    peer_gates: bool | None = None, memory_budget: int | None = None):
+                    peer_gates: bool | None = None, memory_budget: int | None = None, exchange: str | None = None):
         import torch.distributed as dist
 
         tr = DistTransport(group)
@@ -412,18 +450,19 @@ class ShardedState:
             eng = CudaEngine(L, dev, memory_budget=memory_budget)
         else:
             eng = engine_factory(L)
-        st = cls(num_qubits, [eng], tr, [tr.rank], tr.world, peer_gates=peer_gates)
+        st = cls(num_qubits, [eng], tr, [tr.rank], tr.world, peer_gates=peer_gates, exchange=exchange)
         st.reset(0)
         return st
 
     @classmethod
     def virtual(cls, num_qubits: int, shards: int, device: int = 0, engine_factory=None,
-                peer_gates: bool | None = None, memory_budget: int | None = None):
+                peer_gates: bool | None = None, memory_budget: int | None = None, exchange: str | None = None):
         g = int(round(math.log2(shards)))
         L = num_qubits - g
         make = engine_factory or (lambda L_: CudaEngine(L_, device, memory_budget=memory_budget))
         engines = [make(L) for _ in range(shards)]
-        st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards, peer_gates=peer_gates)
+        st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards, peer_gates=peer_gates,
+                 exchange=exchange)
         st.reset(0)
         return st
 
@@ -441,12 +480,36 @@ class ShardedState:
         return self
 
     # ---- gates ------------------------------------------------------------------
+    def _exchange(self, rank_bit: int) -> None:
+        """Swap physical positions L + rank_bit and L - 1 (data movement only;
+        the caller updates the qubit map)."""
+        if self.exchange == "peer" and self.L >= 2 and self._peer_ready():
+            self._peer_swap(rank_bit)
+        else:
+            self.transport.exchange(self.engines, rank_bit, self.L, self.chunk)
+
+    def _peer_swap(self, rank_bit: int) -> None:
+        """The exchange of exchange_plan over peer memory: partners trade the
+        halves whose bit L-1 differs from their rank bit, each moving half of
+        that range with one qs_swap_peer kernel (no staging, no copy-back)."""
+        L = self.L
+        half = 1 << (L - 1)
+        part = half // 2
+        self.transport.peer_barrier(self.engines)
+        for eng, r in zip(self.engines, self.ranks):
+            partner, off, _ = exchange_plan(r, rank_bit, L)
+            _, poff, _ = exchange_plan(partner, rank_bit, L)
+            sub = part if (r >> rank_bit) & 1 else 0
+            eng.swap_peer(self._peers[(r, partner)], off + sub, poff + sub, part)
+        self.transport.peer_barrier(self.engines)
+        self.peer_swaps += 1
+
     def _ensure_local(self, target: int) -> None:
         lay = self.layout
         if lay.is_local(target):
             return
         p = lay.pos[target]
-        self.transport.exchange(self.engines, p - lay.L, lay.L, self.chunk)
+        self._exchange(p - lay.L)
         lay.swap_physical(p, lay.L - 1)
         self.swaps += 1
 
@@ -463,12 +526,13 @@ class ShardedState:
         return cmask, need
 
     def _peer_ready(self) -> bool:
-        if not self.peer_gates:
+        if not (self.peer_gates or self.exchange == "peer"):
             return False
         if self._peers is None:
             self._peers = self.transport.peer_setup(self.engines, self.ranks, self.layout.g) or False
-            if self._peers is False:
+            if self._peers is False:  # every rank agreed: fall back to transport swaps
                 self.peer_gates = False
+                self.exchange = "nccl"
         return bool(self._peers)
 
     def _peer_gate(self, rank_bit: int, cmask: int, need: int, m: np.ndarray) -> None:
@@ -626,7 +690,7 @@ class ShardedState:
             for eng in self.engines:
                 eng.swap_qubits(loc, s)
             lay.swap_physical(loc, s)
-        self.transport.exchange(self.engines, glob - lay.L, lay.L, self.chunk)
+        self._exchange(glob - lay.L)
         lay.swap_physical(glob, s)
         self.swaps += 1
         if loc != s:

@@ -91,6 +91,11 @@ class OracleEngine:
         (self.amps if own_is_a else peer.amps)[i] = tmp[0::2]
         (peer.amps if own_is_a else self.amps)[i] = tmp[1::2]
 
+    def swap_peer(self, peer, own_off, peer_off, count):
+        a = self.amps[own_off: own_off + count].copy()
+        self.amps[own_off: own_off + count] = peer.amps[peer_off: peer_off + count]
+        peer.amps[peer_off: peer_off + count] = a
+
     def sample_shard(self, k, rng, start, total, base, gdim, is_last):
         cdf = np.cumsum(np.concatenate([[start], oc.probabilities(self.amps)]))[1:]
         ncdf = cdf / total

@@ -214,7 +214,34 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, seed, q, peer=False):
+class TestPeerExchange:
+    """Qubit swaps moved by qs_swap_peer semantics (partners split the
+    exchanged half between them; oracle engines) == the oracle, bitwise."""
+
+    @pytest.mark.parametrize("n,shards", [(6, 2), (7, 4), (8, 8)])
+    def test_random_circuits_bitwise(self, n, shards):
+        for seed in range(3):
+            circ = mixed_circuit(n, 60, seed + 7 * n)
+            ref = oracle_run(circ)
+            st = ShardedState.virtual(n, shards, engine_factory=OracleEngine, exchange="peer")
+            st.run(circ)
+            assert st.peer_swaps > 0 and st.peer_swaps == st.swaps
+            assert same_values(st.amplitudes(), ref)
+
+    def test_peer_gates_and_peer_swaps_together(self):
+        n, shards = 7, 4
+        circ = mixed_circuit(n, 80, 99)
+        st = ShardedState.virtual(n, shards, engine_factory=OracleEngine, peer_gates=True, exchange="peer")
+        st.run(circ)
+        st.canonicalize()  # readout swaps go through the peer exchange too
+        assert same_values(st.amplitudes(), oracle_run(circ))
+
+    def test_bad_mode(self):
+        with pytest.raises(ValueError):
+            ShardedState.virtual(5, 2, engine_factory=OracleEngine, exchange="carrier-pigeon")
+
+
+def _worker(rank, world, port, n, seed, q, peer=False, chunk=1 << 26):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -223,6 +250,7 @@ def _worker(rank, world, port, n, seed, q, peer=False):
         # peer=True: oracle engines cannot map a partner process's buffer, so
         # every rank must agree to fall back to qubit swaps (no rank waits)
         st = ShardedState.distributed(n, engine_factory=OracleEngine, peer_gates=peer)
+        st.chunk = chunk  # small chunks: the double-buffered send/recv loop
         st.run(circ)
         amps = st.amplitudes()
         probs = st.probabilities()
@@ -237,12 +265,13 @@ def _worker(rank, world, port, n, seed, q, peer=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,peer", [(2, 7, False), (4, 8, False), (2, 7, True)])
-def test_gloo_distributed_matches_oracle(world, n, peer):
+@pytest.mark.parametrize("world,n,peer,chunk", [(2, 7, False, 1 << 26), (4, 8, False, 1 << 26), (2, 7, True, 1 << 26),
+                                               (2, 8, False, 8), (4, 8, False, 4)])
+def test_gloo_distributed_matches_oracle(world, n, peer, chunk):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, 1234 + n, q, peer)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, 1234 + n, q, peer, chunk)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
