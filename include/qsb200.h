@@ -226,6 +226,39 @@ int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl
  * and after. */
 int qs_swap_peer(qs_state *s, void *peer_amps, uint64_t own_offset, uint64_t peer_offset, uint64_t count);
 
+/* ---- registers sharded over several GPUs by ONE process ----------------------
+ * SURVEY 8(b) qs_create_sharded / 8(e): n qubits over nshards = 2^g shards on
+ * the top g qubits, shard r (the slice [r 2^L, (r+1) 2^L), L = n - g) on
+ * device devs[r] (devices may repeat: several shards per GPU).  Same gate and
+ * readout semantics as the single-device calls (the pairsim functions they
+ * cite); a gate on a global qubit swaps it with local qubit L-1 through an
+ * exchange of half of each partner shard (NCCL send/recv over NVLink with one
+ * communicator per device from ncclCommInitAll, libnccl loaded at run time;
+ * or a peer-memory swap kernel), or with peer gates on runs one pair kernel
+ * over peer memory.  Readout un-permutes the lazy qubit map.  memory_budget
+ * applies per shard (0: 75% of each device's free memory).
+ * Reference anchor: paper_1805_00988_b200/sharded.py (the torch.distributed
+ * multi-process form of the same layout). */
+typedef struct qs_sharded qs_sharded;
+enum { QS_EXCHANGE_NCCL = 1, QS_EXCHANGE_P2P = 2 };
+int qs_create_sharded(int num_qubits, int nshards, const int *devs, uint64_t memory_budget, qs_sharded **out);
+int qs_sharded_destroy(qs_sharded *h);
+int qs_sharded_info(const qs_sharded *h, int *num_qubits, int *nshards, int *shard_qubits);
+int qs_sharded_shard(qs_sharded *h, int rank, qs_state **out);
+/* peer_gates: 1 on, 0 off, -1 unchanged; exchange: QS_EXCHANGE_NCCL / _P2P (0: unchanged) */
+int qs_sharded_set_mode(qs_sharded *h, int peer_gates, int exchange);
+int qs_sharded_stats(const qs_sharded *h, uint64_t *swaps, uint64_t *peer_gates, int *exchange);
+int qs_sharded_reset(qs_sharded *h, uint64_t basis);
+int qs_sharded_apply_gate(qs_sharded *h, int target, const float m[8]);
+int qs_sharded_apply_controlled_gate(qs_sharded *h, int control, int target, const float m[8]);
+int qs_sharded_apply_controlled_controlled_gate(qs_sharded *h, int c1, int c2, int target, const float m[8]);
+int qs_sharded_synchronize(qs_sharded *h);
+int qs_sharded_get_amplitudes(qs_sharded *h, uint64_t offset, uint64_t count, void *host);
+int qs_sharded_set_amplitudes(qs_sharded *h, uint64_t offset, uint64_t count, const void *host);
+int qs_sharded_probabilities(qs_sharded *h, uint64_t offset, uint64_t count, double *host);
+int qs_sharded_norm_squared(qs_sharded *h, double *out);
+int qs_sharded_sample(qs_sharded *h, const qs_pcg64 *rng, int64_t k, int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,12 @@ EXPORTS = (
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
     "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_swap_peer", "qs_jit_sync",
     "qs_jit_shutdown", "qs_begin_capture", "qs_end_capture", "qs_graph_launch", "qs_graph_destroy",
+    "qs_create_sharded", "qs_sharded_destroy", "qs_sharded_info", "qs_sharded_shard", "qs_sharded_set_mode",
+    "qs_sharded_stats", "qs_sharded_reset", "qs_sharded_apply_gate", "qs_sharded_apply_controlled_gate",
+    "qs_sharded_apply_controlled_controlled_gate", "qs_sharded_synchronize", "qs_sharded_get_amplitudes",
+    "qs_sharded_set_amplitudes", "qs_sharded_probabilities", "qs_sharded_norm_squared", "qs_sharded_sample",
 )
+QS_EXCHANGE_NCCL, QS_EXCHANGE_P2P = 1, 2
 
 
 class qs_pcg64(ctypes.Structure):
@@ -109,6 +114,22 @@ def _declare(L):
         "qs_ipc_close": ([i32, vp], i32),
         "qs_apply_gate_peer": ([vp, vp, i32, u64, f32p], i32),
         "qs_swap_peer": ([vp, vp, u64, u64, u64], i32),
+        "qs_create_sharded": ([i32, i32, ctypes.POINTER(i32), u64, ctypes.POINTER(vp)], i32),
+        "qs_sharded_destroy": ([vp], i32),
+        "qs_sharded_info": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
+        "qs_sharded_shard": ([vp, i32, ctypes.POINTER(vp)], i32),
+        "qs_sharded_set_mode": ([vp, i32, i32], i32),
+        "qs_sharded_stats": ([vp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(i32)], i32),
+        "qs_sharded_reset": ([vp, u64], i32),
+        "qs_sharded_apply_gate": ([vp, i32, f32p], i32),
+        "qs_sharded_apply_controlled_gate": ([vp, i32, i32, f32p], i32),
+        "qs_sharded_apply_controlled_controlled_gate": ([vp, i32, i32, i32, f32p], i32),
+        "qs_sharded_synchronize": ([vp], i32),
+        "qs_sharded_get_amplitudes": ([vp, u64, u64, vp], i32),
+        "qs_sharded_set_amplitudes": ([vp, u64, u64, vp], i32),
+        "qs_sharded_probabilities": ([vp, u64, u64, vp], i32),
+        "qs_sharded_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
+        "qs_sharded_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),
         "qs_jit_sync": ([i32], i32),
         "qs_jit_shutdown": ([], i32),
         "qs_begin_capture": ([vp], i32),

@@ -143,6 +143,20 @@ unsigned grid_for(const qs_state *s, uint64_t items, int per_thread) {
 
 }  // namespace
 
+// own[i] <-> peer[i], i < count amplitudes, on s's stream (caller: device guard)
+int launch_peer_swap(qs_state *s, float2 *own, float2 *peer, uint64_t count) {
+    if (count == 0) return QS_OK;
+    if ((((uintptr_t)own | (uintptr_t)peer) & 15u) == 0 && (count & 1ull) == 0) {
+        constexpr int U = 4;
+        const uint64_t n = count >> 1;
+        k_peer_swap<U><<<grid_for(s, n, U), 256, 0, s->stream>>>((float4 *)own, (float4 *)peer, n);
+    } else {
+        k_peer_swap8<<<grid_for(s, count, 1), 256, 0, s->stream>>>(own, peer, count);
+    }
+    QS_CUDA(cudaGetLastError());
+    return QS_OK;
+}
+
 }  // namespace qsb
 
 using namespace qsb;
@@ -236,16 +250,7 @@ int qs_swap_peer(qs_state *s, void *peer_amps, uint64_t own_offset, uint64_t pee
     if (own_offset > dim || count > dim - own_offset) return set_error(QS_ERR_INDEX, "swap range out of bounds");
     if (count == 0) return QS_OK;
     DeviceGuard guard(s->device);
-    float2 *own = s->amps + own_offset, *peer = (float2 *)peer_amps + peer_offset;
-    if (((own_offset | peer_offset | count) & 1ull) == 0) {
-        constexpr int U = 4;
-        const uint64_t n = count >> 1;
-        k_peer_swap<U><<<grid_for(s, n, U), 256, 0, s->stream>>>((float4 *)own, (float4 *)peer, n);
-    } else {
-        k_peer_swap8<<<grid_for(s, count, 1), 256, 0, s->stream>>>(own, peer, count);
-    }
-    QS_CUDA(cudaGetLastError());
-    return QS_OK;
+    return launch_peer_swap(s, s->amps + own_offset, (float2 *)peer_amps + peer_offset, count);
 }
 
 }  // extern "C"
