@@ -170,9 +170,13 @@ def lower_ops(circuit: Circuit, double: bool = False) -> list:
     return ops
 
 
-def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: int | None = None):
+def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: int | None = None,
+            reorder: bool | None = None):
     """Apply `circuit` to a device State in place; returns the per-draw outcomes
-    of a trailing SampleMeasure (or None)."""
+    of a trailing SampleMeasure (or None).  reorder (default: QSB_FUSE_REORDER
+    == "1") lets the fused planner exchange gates on disjoint qubits: fewer
+    passes, results equal to the reference to rounding (rtol 1e-5) instead of
+    bit for bit (fusion.plan)."""
     if circuit.num_qubits != state.num_qubits:
         raise ValueError("circuit and state widths differ")
     double = getattr(state, "is_double", False)
@@ -180,7 +184,11 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
     if fuse:
         if double and tile_qubits is None:
             tile_qubits = 12  # complex128 tiles: 2^12 amplitudes = 64 KiB
-        fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits))
+        if reorder is None:
+            import os
+
+            reorder = os.environ.get("QSB_FUSE_REORDER") == "1"
+        fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits, reorder=reorder))
     else:
         for kind, t, cm, m in ops:
             fusion._single(state, kind, t, cm, m)

@@ -461,6 +461,25 @@ __device__ __forceinline__ void pphase_sel(bool on, float2 d, float4 (&v)[1 << R
     pphase<RNEED, ODD, RB>(make_float2(on ? d.x : 1.0f, on ? d.y : 0.0f), v);
 }
 
+// The planar phase inside a (warp-uniform) branch: scalar in-place FMUL /
+// FFMA per component (cmul_s), so the branch leaves every value in its home
+// register (packed results land in fresh register pairs, which costs MOVs
+// back at the join).
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void pphase_cs(float2 d, float4 (&v)[1 << RB]) {
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+        if ((j & RNEED) != RNEED) continue;
+        if (!ODD) cmul_s(d, v[j].x, v[j].z);
+        cmul_s(d, v[j].y, v[j].w);
+    }
+}
+
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void pphase_sel_cs(bool on, float2 d, float4 (&v)[1 << RB]) {
+    pphase_cs<RNEED, ODD, RB>(make_float2(on ? d.x : 1.0f, on ? d.y : 0.0f), v);
+}
+
 // Packed class bodies on a planar unit pair (a, b) = both halves of the
 // pair's two amplitudes: same per-lane arithmetic as pair_cls.
 template <int CLS>

@@ -249,7 +249,8 @@ std::string generate(const FParams &p, int K, int RB) {
                     if (is_phase) {
                         const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
                         std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(%s, make_float2(",
-                                      planar ? "pphase_sel" : "phase_sel", R, odd ? "true" : "false", ltest.c_str());
+                                      planar ? (utest.empty() ? "pphase_sel" : "pphase_sel_cs") : "phase_sel", R,
+                                      odd ? "true" : "false", ltest.c_str());
                         src += buf;
                         hexf(src, op.m[6]);
                         src += ", ";
@@ -269,7 +270,8 @@ std::string generate(const FParams &p, int K, int RB) {
                     const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
                     const bool scalar = phase_mode == 2 || (phase_mode == 1 && !test.empty());
                     std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(make_float2(",
-                                  planar ? "pphase" : (scalar ? "phase_cs" : "phase_ct"), R, odd ? "true" : "false");
+                                  planar ? (test.empty() ? "pphase" : "pphase_cs") : (scalar ? "phase_cs" : "phase_ct"),
+                                  R, odd ? "true" : "false");
                     src += buf;
                     hexf(src, op.m[6]);
                     src += ", ";

@@ -66,17 +66,112 @@ def default_tile_qubits(num_qubits: int) -> int:
     return min(13, num_qubits)
 
 
-def plan(num_qubits: int, ops, tile_qubits: int | None = None) -> list[Pass]:
+def plan(num_qubits: int, ops, tile_qubits: int | None = None, reorder: bool = False) -> list[Pass]:
     """Greedy in-order grouping into passes of at most K tile qubits.  Without
     an explicit K: 12-qubit tiles (two persistent CTAs per SM) unless those
     need more than 25% more passes than 13-qubit ones.  (Measured on B200
     with the dynamic tile scheduler, scripts/qft_passes.py: QFT(28) 8.5 ms
-    on 12-qubit tiles vs 9.3 ms on 13, QFT(30) 36.3 vs 37.5 ms.)"""
+    on 12-qubit tiles vs 9.3 ms on 13, QFT(30) 36.3 vs 37.5 ms.)
+
+    reorder=True (opt-in, QSB_FUSE_REORDER=1 for execute()): the
+    commutation-aware planner _plan_reorder — gates on disjoint qubits are
+    exchanged freely.  That is exact in real arithmetic but NOT bit-exact in
+    floating point (e.g. H(a) H(b) sums (v0 + v1) + (v2 + v3) where H(b) H(a)
+    sums (v0 + v2) + (v1 + v3)), so results agree with the reference to
+    rounding (tested at rtol 1e-5, the north_star bar) instead of bit for
+    bit.  The default planner only moves permutations, which is exact."""
+    pl = _plan_reorder if reorder else _plan
     if tile_qubits is None and num_qubits >= 13:
-        p13 = _plan(num_qubits, ops, 13)
-        p12 = _plan(num_qubits, ops, 12)
+        p13 = pl(num_qubits, ops, 13)
+        p12 = pl(num_qubits, ops, 12)
         return p12 if 4 * len(p12) <= 5 * len(p13) else p13
-    return _plan(num_qubits, ops, tile_qubits)
+    return pl(num_qubits, ops, tile_qubits)
+
+
+def _plan_reorder(num_qubits: int, ops, tile_qubits: int | None) -> list[Pass]:
+    """Commutation-aware grouping: ops form a DAG (an op depends on the
+    latest earlier op sharing any qubit with it); a pass absorbs every READY
+    op that fits its tile (diagonal ops always, pair ops whose target is a
+    tile qubit), and while the tile has room it adds the qubit whose
+    addition unlocks the most ops (simulated absorption over the DAG).  Ops
+    sharing a qubit keep their order, so each qubit's gate sequence is the
+    circuit's."""
+    n = num_qubits
+    K = tile_qubits or default_tile_qubits(n)
+    if n < 10 or K < 10:
+        return [Pass(list(range(n)), list(ops))] if ops else []
+    ops = list(ops)
+    m = len(ops)
+    masks = [_qubits(op) for op in ops]
+    # successors through each op's qubits: op j waits for the latest earlier op on each of its qubits
+    last = {}
+    preds = [0] * m
+    succ = [[] for _ in range(m)]
+    for j, mk in enumerate(masks):
+        ps = set()
+        q = mk
+        while q:
+            b = q & -q
+            i = last.get(b)
+            if i is not None:
+                ps.add(i)
+            last[b] = j
+            q ^= b
+        preds[j] = len(ps)
+        for i in ps:
+            succ[i].append(j)
+    done = [False] * m
+    ready = {j for j in range(m) if preds[j] == 0}
+
+    def fits(j, tile):
+        kind, t = ops[j][0], ops[j][1]
+        return kind != N.QS_OP_PAIR or (tile >> t) & 1
+
+    def absorb(tile, rd, pc, dn, out):
+        """Take every ready op that fits, transitively (simulation when out is None)."""
+        stack = [j for j in rd if fits(j, tile)]
+        count = 0
+        while stack:
+            j = stack.pop()
+            if dn[j] or j not in rd:
+                continue
+            rd.discard(j)
+            dn[j] = True
+            count += 1
+            if out is not None:
+                out.append(j)
+            for k in succ[j]:
+                pc[k] -= 1
+                if pc[k] == 0:
+                    rd.add(k)
+                    if fits(k, tile):
+                        stack.append(k)
+        return count
+
+    base = (1 << min(LOW, n)) - 1
+    passes: list[Pass] = []
+    remaining = m
+    while remaining:
+        tile = base
+        taken: list[int] = []
+        remaining -= absorb(tile, ready, preds, done, taken)
+        while remaining and bin(tile).count("1") < K:
+            cands = {ops[j][1] for j in ready if ops[j][0] == N.QS_OP_PAIR and not (tile >> ops[j][1]) & 1}
+            if not cands:
+                break
+            best, best_gain = None, -1
+            for q in sorted(cands):
+                gain = absorb(tile | (1 << q), set(ready), list(preds), list(done), None)
+                if gain > best_gain:
+                    best, best_gain = q, gain
+            tile |= 1 << best
+            remaining -= absorb(tile, ready, preds, done, taken)
+        taken.sort()  # circuit order among independent ops (the DAG order holds: sorted is a topological order)
+        qs = [q for q in range(n) if (tile >> q) & 1]
+        extra = [q for q in range(n - 1, -1, -1) if not (tile >> q) & 1]
+        qs.extend(extra[: max(0, K - len(qs))])
+        passes.append(Pass(sorted(qs), [ops[j] for j in taken]))
+    return passes
 
 
 def is_permutation(m: np.ndarray) -> bool:

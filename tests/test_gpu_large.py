@@ -280,3 +280,35 @@ class TestShardedAt31:
                 assert device_equal(eng.view(), rv[r * half:(r + 1) * half]), (peer, r)
             sh.close()
         ref.close()
+
+
+class TestReorderedPlanner:
+    """The opt-in commutation-aware planner (fusion.plan(reorder=True)):
+    agreement with the reference to the north_star tolerance."""
+
+    @pytest.mark.parametrize("n", [20, 24])
+    def test_layered_to_tolerance(self, n):
+        circ = layered_random_circuit(n, 20, seed=32)
+        a, b = State(n), State(n)
+        execute(circ, a, fuse=True, reorder=True)
+        execute(circ, b, fuse=False)
+        x, y = a.amplitudes(), b.amplitudes()
+        np.testing.assert_allclose(x, y, rtol=1e-5, atol=1e-5 * 2.0 ** (-n / 2))
+        a.close()
+        b.close()
+
+    def test_config4_n32_to_tolerance(self):
+        need(66)
+        n = 32
+        circ = layered_random_circuit(n, 20, seed=32)
+        a, b = State(n), State(n)
+        execute(circ, a, fuse=True, reorder=True)
+        execute(circ, b, fuse=True)
+        va, vb = view(a), view(b)
+        chunk = 1 << 28
+        worst = 0.0
+        for off in range(0, va.numel(), chunk):
+            worst = max(worst, float((va[off: off + chunk] - vb[off: off + chunk]).abs().max()))
+        assert worst <= 1e-5 * 2.0 ** (-n / 2) * 4
+        a.close()
+        b.close()
