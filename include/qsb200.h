@@ -136,6 +136,16 @@ int qs_apply_controlled_controlled_gate_f64(qs_state *s, int c1, int c2, int tar
  * bits may be anywhere). */
 int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile,
                    const qs_op *ops, int nops);
+/* qs_apply_fused with flags.  QS_FUSED_COMBINE_PHASES (opt-in, NOT
+ * bit-exact): in the compiled pass programs, each run of consecutive
+ * unit-modulus diagonal ops (u1 / z / s / t and controlled forms) becomes one
+ * complex product per amplitude by the run's accumulated phase (angles summed
+ * exactly in fixed-point turns) instead of one product per op; results agree
+ * with the sequential ops to rounding (~1e-6 relative; tested at the
+ * north_star rtol 1e-5).  complex128 registers ignore the flag. */
+enum { QS_FUSED_COMBINE_PHASES = 1 };
+int qs_apply_fused_ex(qs_state *s, const int32_t *tile_qubits, int ntile,
+                      const qs_op *ops, int nops, int flags);
 /* Fused pass with fp64 gate entries (the form a complex128 register takes;
  * on a complex64 register the entries are rounded to float32 and the call
  * is qs_apply_fused). */

@@ -30,7 +30,7 @@ EXPORTS = (
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
     "qs_apply_controlled_controlled_gate", "qs_apply_gate_f64", "qs_apply_controlled_gate_f64",
-    "qs_apply_controlled_controlled_gate_f64", "qs_apply_fused", "qs_apply_fused_f64", "qs_swap_qubits",
+    "qs_apply_controlled_controlled_gate_f64", "qs_apply_fused", "qs_apply_fused_ex", "qs_apply_fused_f64", "qs_swap_qubits",
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
@@ -42,6 +42,7 @@ EXPORTS = (
     "qs_sharded_set_amplitudes", "qs_sharded_probabilities", "qs_sharded_norm_squared", "qs_sharded_sample",
 )
 QS_EXCHANGE_NCCL, QS_EXCHANGE_P2P = 1, 2
+QS_FUSED_COMBINE_PHASES = 1
 
 
 class qs_pcg64(ctypes.Structure):
@@ -97,6 +98,7 @@ def _declare(L):
         "qs_apply_controlled_controlled_gate_f64": ([vp, i32, i32, i32, f64p], i32),
         "qs_apply_fused": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
         "qs_apply_fused_f64": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
+        "qs_apply_fused_ex": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32, i32], i32),
         "qs_swap_qubits": ([vp, i32, i32], i32),
         "qs_get_amplitudes": ([vp, u64, u64, vp], i32),
         "qs_set_amplitudes": ([vp, u64, u64, vp], i32),

@@ -171,12 +171,16 @@ def lower_ops(circuit: Circuit, double: bool = False) -> list:
 
 
 def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: int | None = None,
-            reorder: bool | None = None):
+            reorder: bool | None = None, exact: bool = True):
     """Apply `circuit` to a device State in place; returns the per-draw outcomes
-    of a trailing SampleMeasure (or None).  reorder (default: QSB_FUSE_REORDER
-    == "1") lets the fused planner exchange gates on disjoint qubits: fewer
-    passes, results equal to the reference to rounding (rtol 1e-5) instead of
-    bit for bit (fusion.plan)."""
+    of a trailing SampleMeasure (or None).
+
+    exact=True (default): the reference's arithmetic bit for bit.
+    exact=False: results equal the reference to rounding (tested at the
+    north_star rtol 1e-5), faster: the fused planner may exchange gates on
+    disjoint qubits (reorder) and compiled passes combine runs of diagonal
+    gates into one product per amplitude (QS_FUSED_COMBINE_PHASES).
+    reorder alone (default: QSB_FUSE_REORDER == "1") enables only the first."""
     if circuit.num_qubits != state.num_qubits:
         raise ValueError("circuit and state widths differ")
     double = getattr(state, "is_double", False)
@@ -187,8 +191,9 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
         if reorder is None:
             import os
 
-            reorder = os.environ.get("QSB_FUSE_REORDER") == "1"
-        fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits, reorder=reorder))
+            reorder = os.environ.get("QSB_FUSE_REORDER") == "1" or not exact
+        fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits, reorder=reorder),
+                   combine=not exact and not double)
     else:
         for kind, t, cm, m in ops:
             fusion._single(state, kind, t, cm, m)

@@ -523,7 +523,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     return QS_OK;
 }
 
-int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops) {
+int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops, int flags) {
     const int n = s->num_qubits;
     uint64_t tile_mask = 0;
     for (int i = 0; i < ntile; ++i) {
@@ -585,6 +585,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         const int jrb = jit_rb(2 * nphase > nops ? 3 : 4);
         std::vector<FParams> groups;
         if (plan_pass(s, tile_mask, ops, nops, jrb, groups) == QS_OK) {
+            for (FParams &g : groups) g.combine = (flags & QS_FUSED_COMBINE_PHASES) ? 1 : 0;
             std::vector<void *> fns;
             for (const FParams &g : groups) {
                 void *fn = recording ? jit_lookup(s->device, g, K, jrb)

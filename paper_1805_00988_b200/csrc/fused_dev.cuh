@@ -64,6 +64,7 @@ struct FParams {
     int dry;    // probes (QSB_FUSED_DRY): 1 skip the ops, 2 also the register stages, 3 also the stores
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
     int l2hint;  // TMA copies with an L2 evict_first policy
+    int combine;  // generated programs: combine runs of unit-modulus diagonal ops (exact = False)
     uint64_t ntiles;
     // Dynamic tile scheduler: the producers take tiles from this counter
     // (zero at launch; the last CTA to find it exhausted zeroes it again).
@@ -459,6 +460,18 @@ __device__ __forceinline__ void pphase(float2 d, float4 (&v)[1 << RB]) {
 template <int RNEED, bool ODD, int RB>
 __device__ __forceinline__ void pphase_sel(bool on, float2 d, float4 (&v)[1 << RB]) {
     pphase<RNEED, ODD, RB>(make_float2(on ? d.x : 1.0f, on ? d.y : 0.0f), v);
+}
+
+// Combined diagonal run (opt-in, not bit-exact): multiply by e^{2 pi i t / 2^32}
+// for an accumulated phase t in fixed-point turns (exact modular sum of the
+// run's angles); one complex product per amplitude instead of one per op.
+__device__ __forceinline__ void turns_mul(uint32_t t, float &re, float &im) {
+    const float ang = (float)(int)t * 1.46291807926715968e-9f;  // 2 pi / 2^32
+    float sn, cs;
+    __sincosf(ang, &sn, &cs);
+    const float nr = __fmaf_rn(re, cs, -__fmul_rn(im, sn));
+    im = __fmaf_rn(re, sn, __fmul_rn(im, cs));
+    re = nr;
 }
 
 // The planar phase inside a (warp-uniform) branch: scalar in-place FMUL /

@@ -26,6 +26,7 @@
 #include <dlfcn.h>
 #include <pthread.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -174,6 +175,17 @@ std::string op_test(const FOp &op) {
     return u + " && " + l;
 }
 
+// A unit-modulus diagonal entry d = e^{i theta} as fixed-point turns
+// (theta / 2 pi * 2^32, modulo 2^32); false when |d| is not 1.
+bool unit_turns(const FOp &op, uint32_t *turns) {
+    const double x = op.m[6], y = op.m[7];
+    if (std::fabs(std::sqrt(x * x + y * y) - 1.0) > 1e-6) return false;
+    double t = std::atan2(y, x) / (2.0 * 3.14159265358979323846);
+    if (t < 0) t += 1.0;
+    *turns = (uint32_t)(uint64_t)std::llround(t * 4294967296.0);
+    return true;
+}
+
 std::string generate(const FParams &p, int K, int RB) {
     // diagonal ops inside a test: 1 (default) scalar phase_cs, 0 packed
     // phase_ct, 2 scalar everywhere (QSB_JIT_PHASE, for measurements)
@@ -193,6 +205,15 @@ std::string generate(const FParams &p, int K, int RB) {
     for (int o = 0; o < p.nops; ++o) nphase += p.ops[o].variant >= kPhaseVariant;
     const bool planar = planar_mode == 1 || (planar_mode == 2 && 2 * nphase > p.nops);
     if (planar) loop_run = 1 << 30;  // the op-table loops (run_phase / run_pair) are interleaved-layout code
+    // Runs of >= tile_loop diagonal ops tested only on TILE bits (QFT rows:
+    // the controls outside the tile) become one loop over the ops that
+    // apply to this tile (a uniform bit mask), entries from a __constant__
+    // table: no branch per op, skipped ops cost nothing, small code.  The
+    // applicable ops run in circuit order, so the bits are unchanged.
+    int tile_loop = 3;
+    if (const char *e = std::getenv("QSB_JIT_TILE_LOOP")) tile_loop = std::atoi(e);
+    std::string consts;
+    int nconst = 0;
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 200);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n";
@@ -214,6 +235,110 @@ std::string generate(const FParams &p, int K, int RB) {
         src += buf;
         for (int o = st.op_begin; o < st.op_end;) {
             const FOp &op = p.ops[o];
+            // combined diagonal runs (QS_FUSED_COMBINE_PHASES, not bit-exact):
+            // accumulate each op's angle (fixed-point turns, exact modular
+            // sums) into one accumulator per register pattern under its
+            // thread / tile predicate, then one complex product per amplitude
+            uint32_t t0;
+            if (p.combine && op.variant >= kPhaseVariant && unit_turns(op, &t0)) {
+                int e2 = o;
+                uint32_t tt;
+                while (e2 < st.op_end && p.ops[e2].variant >= kPhaseVariant && unit_turns(p.ops[e2], &tt)) ++e2;
+                if (e2 - o >= 2) {
+                    std::vector<std::pair<uint32_t, uint32_t>> pats;  // (reg_need, half_need)
+                    std::vector<uint32_t> cst;                      // folded unconditional turns
+                    std::string adds;
+                    for (int i = o; i < e2; ++i) {
+                        const FOp &x = p.ops[i];
+                        const std::pair<uint32_t, uint32_t> key(x.reg_need, x.half_need ? 1u : 0u);
+                        size_t a = std::find(pats.begin(), pats.end(), key) - pats.begin();
+                        if (a == pats.size()) {
+                            pats.push_back(key);
+                            cst.push_back(0);
+                        }
+                        unit_turns(x, &tt);
+                        const std::string cond = op_test(x);
+                        if (cond.empty()) {
+                            cst[a] += tt;
+                        } else {
+                            std::snprintf(buf, sizeof buf, "        a%zu += (%s) ? 0x%08xu : 0u;\n", a, cond.c_str(), tt);
+                            adds += buf;
+                        }
+                    }
+                    std::snprintf(buf, sizeof buf, "      { // %d diagonal ops combined\n", e2 - o);
+                    src += buf;
+                    for (size_t a = 0; a < pats.size(); ++a) {
+                        std::snprintf(buf, sizeof buf, "        uint32_t a%zu = 0x%08xu;\n", a, cst[a]);
+                        src += buf;
+                    }
+                    src += adds;
+                    const char *re[2] = {planar ? "x" : "x", planar ? "y" : "z"};
+                    const char *im[2] = {planar ? "z" : "y", planar ? "w" : "w"};
+                    for (int j = 0; j < (1 << RB); ++j)
+                        for (int h = 0; h < 2; ++h) {
+                            std::string sum;
+                            for (size_t a = 0; a < pats.size(); ++a)
+                                if (((uint32_t)j & pats[a].first) == pats[a].first && (!pats[a].second || h == 1))
+                                    sum += (sum.empty() ? "a" : " + a") + std::to_string(a);
+                            if (sum.empty()) continue;
+                            std::snprintf(buf, sizeof buf, "        if constexpr (%d < (1 << RB)) turns_mul(%s, v[%d].%s, v[%d].%s);\n",
+                                          j, sum.c_str(), j, re[h], j, im[h]);
+                            src += buf;
+                        }
+                    src += "      }\n";
+                    o = e2;
+                    continue;
+                }
+            }
+            auto tile_only = [&](const FOp &x) {
+                return x.variant >= kPhaseVariant && x.ext_need != 0 && x.tid_need == 0 &&
+                       x.reg_need == op.reg_need && x.half_need == op.half_need;
+            };
+            if (tile_loop > 0 && tile_only(op)) {
+                int e2 = o;
+                while (e2 < st.op_end && e2 - o < 32 && tile_only(p.ops[e2])) ++e2;
+                const int len = e2 - o;
+                if (len >= tile_loop) {
+                    const int id = nconst++;
+                    std::snprintf(buf, sizeof buf, "__constant__ unsigned kT%d[%d] = {", id, 2 * len);
+                    consts += buf;
+                    for (int i = 0; i < len; ++i) {
+                        uint32_t bx, by;
+                        std::memcpy(&bx, &p.ops[o + i].m[6], 4);
+                        std::memcpy(&by, &p.ops[o + i].m[7], 4);
+                        std::snprintf(buf, sizeof buf, "%s0x%08xu, 0x%08xu", i ? ", " : "", bx, by);
+                        consts += buf;
+                    }
+                    consts += "};\n";
+                    // applicable-op mask of this tile: consecutive single
+                    // tile bits in ascending order are one shift
+                    bool consecutive = true;
+                    const int b0 = __builtin_ctzll(p.ops[o].ext_need);
+                    for (int i = 0; i < len; ++i)
+                        if (p.ops[o + i].ext_need != (1ull << (b0 + i))) consecutive = false;
+                    src += "      { uint32_t m = ";
+                    if (consecutive) {
+                        std::snprintf(buf, sizeof buf, "(uint32_t)(ub >> %d) & 0x%xu;", b0,
+                                      len == 32 ? 0xffffffffu : ((1u << len) - 1u));
+                        src += buf;
+                    } else {
+                        src += "0u;";
+                        for (int i = 0; i < len; ++i) {
+                            const unsigned long long E = p.ops[o + i].ext_need;
+                            std::snprintf(buf, sizeof buf, " m |= (uint32_t)((ub & 0x%llxull) == 0x%llxull) << %d;", E, E, i);
+                            src += buf;
+                        }
+                    }
+                    const int R = (int)op.reg_need;
+                    std::snprintf(buf, sizeof buf,
+                                  "\n        while (m) { const int i = __ffs(m) - 1; m &= m - 1u;"
+                                  " %s<%d, %s, RB>(make_float2(__uint_as_float(kT%d[2 * i]), __uint_as_float(kT%d[2 * i + 1])), v); } }\n",
+                                  planar ? "pphase" : "phase_cs", R, op.half_need ? "true" : "false", id, id);
+                    src += buf;
+                    o = e2;
+                    continue;
+                }
+            }
             // optionally (QSB_JIT_LOOP_RUN, see kJitLoopRun) a long run of
             // one variant stays a loop over the shared-memory op table
             int e = o + 1;
@@ -298,6 +423,11 @@ std::string generate(const FParams &p, int K, int RB) {
                   "    const __grid_constant__ FParams p) {\n  fused_body<%d, %d, GenProg>(amps, p);\n}\n",
                   RB == 4 ? 168 : 96, K, RB);
     src += buf;
+    if (!consts.empty()) {  // the constant tables go before the program that reads them
+        const std::string head = "using namespace qsb;\n";
+        const size_t at = src.find(head) + head.size();
+        src.insert(at, consts);
+    }
     return src;
 }
 

@@ -349,8 +349,8 @@ int qs_apply_controlled_controlled_gate_f64(qs_state *s, int c1, int c2, int tar
     return rc ? rc : sweep_f64(s, target, (1ull << c1) | (1ull << c2), m);
 }
 
-int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops,
-                   int nops) {
+int qs_apply_fused_ex(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops,
+                      int flags) {
     CHECK_HANDLE(s);
     if (nops == 0) return QS_OK;
     if (!ops || !tile_qubits) return set_error(QS_ERR_NULL, "null op list or tile qubit list");
@@ -365,7 +365,11 @@ int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_
         }
         return run_fused_d(s, tile_qubits, ntile, wide.data(), nops);
     }
-    return run_fused(s, tile_qubits, ntile, ops, nops);
+    return run_fused(s, tile_qubits, ntile, ops, nops, flags);
+}
+
+int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops) {
+    return qs_apply_fused_ex(s, tile_qubits, ntile, ops, nops, 0);
 }
 
 int qs_apply_fused_f64(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops,

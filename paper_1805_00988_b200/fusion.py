@@ -246,12 +246,16 @@ def jit_sync(device: int = -1) -> None:
     N.check(N.lib().qs_jit_sync(int(device)))
 
 
-def run(state, passes: list[Pass]) -> None:
-    """Launch the planned passes on a State (asynchronous on its stream)."""
+def run(state, passes: list[Pass], combine: bool = False) -> None:
+    """Launch the planned passes on a State (asynchronous on its stream).
+    combine=True: runs of unit-modulus diagonal ops as one product per
+    amplitude (State.apply_fused; not bit-exact)."""
     for p in passes:
         if len(p.ops) == 1:
             kind, t, cm, m = p.ops[0]
             _single(state, kind, t, cm, m)
+        elif combine:
+            state.apply_fused(p.tile, p.op_array(), combine=True)
         else:
             state.apply_fused(p.tile, p.op_array())
 

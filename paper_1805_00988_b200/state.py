@@ -209,16 +209,23 @@ class State:
         N.check(fn(self.handle, int(control1), int(control2), int(target), mp))
         return self
 
-    def apply_fused(self, tile_qubits, ops: np.ndarray) -> "State":
+    def apply_fused(self, tile_qubits, ops: np.ndarray, combine: bool = False) -> "State":
         """One fused HBM pass (see fusion.py for the planner).  `ops` is an
-        OP_DTYPE (float32 entries) or OP64_DTYPE (fp64 entries) record array."""
+        OP_DTYPE (float32 entries) or OP64_DTYPE (fp64 entries) record array.
+        combine=True (not bit-exact, QS_FUSED_COMBINE_PHASES): runs of
+        unit-modulus diagonal ops become one product per amplitude."""
         tq = np.ascontiguousarray(np.asarray(tile_qubits, dtype=np.int32))
         wide = np.asarray(ops).dtype == N.OP64_DTYPE
         ops = np.ascontiguousarray(ops, dtype=N.OP64_DTYPE if wide else N.OP_DTYPE)
         L = N.lib()
-        fn = L.qs_apply_fused_f64 if wide else L.qs_apply_fused
-        N.check(fn(self.handle, tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                   int(tq.size), ops.ctypes.data, int(ops.size)))
+        tp = tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        if wide:
+            N.check(L.qs_apply_fused_f64(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size)))
+        elif combine:
+            N.check(L.qs_apply_fused_ex(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size),
+                                        N.QS_FUSED_COMBINE_PHASES))
+        else:
+            N.check(L.qs_apply_fused(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size)))
         return self
 
     def record(self) -> "_Recording":

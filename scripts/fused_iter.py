@@ -23,19 +23,19 @@ import numpy as np, torch
 from paper_1805_00988_b200 import State, build_qft, build_hadamard_layer, layered_random_circuit, fusion, execute
 from paper_1805_00988_b200.circuits import lower_ops
 out = {{}}
-def timed(n, circ, reps=3):
+def timed(n, circ, reps=3, exact=True):
     st = State(n)
     s = torch.cuda.ExternalStream(st.stream())
-    passes = fusion.plan(n, lower_ops(circ))
+    passes = fusion.plan(n, lower_ops(circ), reorder=not exact)
     t0 = time.perf_counter()
-    fusion.run(st, passes); st.flush()
+    fusion.run(st, passes, combine=not exact); st.flush()
     cold = time.perf_counter() - t0
     fusion.jit_sync()
-    fusion.run(st, passes); st.flush()
+    fusion.run(st, passes, combine=not exact); st.flush()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s)
     for _ in range(reps):
-        fusion.run(st, passes)
+        fusion.run(st, passes, combine=not exact)
     b.record(s); st.flush()
     st.close()
     return {{"ms": a.elapsed_time(b) / reps, "passes": len(passes), "cold_ms": cold * 1e3}}
@@ -51,8 +51,11 @@ out["exact_layered22"] = exact(22, layered_random_circuit(22, 12, seed=5))
 out["qft28"] = timed(28, build_qft(28))
 out["qft30"] = timed(30, build_qft(30))
 out["hlayer30"] = timed(30, build_hadamard_layer(30))
+out["qft28_inexact"] = timed(28, build_qft(28), exact=False)
+out["qft30_inexact"] = timed(30, build_qft(30), exact=False)
 if {big!r}:
     out["config4_32"] = timed(32, layered_random_circuit(32, 20, seed=32), reps=1)
+    out["config4_32_inexact"] = timed(32, layered_random_circuit(32, 20, seed=32), reps=1, exact=False)
 print(json.dumps(out))
 '''
 

@@ -312,3 +312,49 @@ class TestReorderedPlanner:
         assert worst <= 1e-5 * 2.0 ** (-n / 2) * 4
         a.close()
         b.close()
+
+
+class TestInexactMode:
+    """execute(..., exact=False): commutation-aware passes + combined diagonal
+    runs (QS_FUSED_COMBINE_PHASES) — equal to the reference to the north_star
+    tolerance (rtol 1e-5), not bit for bit.  Compiled programs only, so the
+    compiles are waited for before the timed/compared run."""
+
+    @pytest.mark.parametrize("n,name", [(20, "qft"), (24, "qft"), (22, "layered"), (21, "random")])
+    def test_matches_exact_to_tolerance(self, n, name):
+        from paper_1805_00988_b200 import fusion, random_circuit
+
+        circ = {"qft": lambda: build_qft(n), "layered": lambda: layered_random_circuit(n, 12, seed=3),
+                "random": lambda: random_circuit(n, 300, np.random.default_rng(5))}[name]()
+        a, b = State(n), State(n)
+        rng = np.random.default_rng(n)
+        v = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)).astype(np.complex64)
+        v /= np.float32(np.linalg.norm(v))
+        a.set_amplitudes(v)
+        execute(circ, a, fuse=True, exact=False)
+        fusion.jit_sync()
+        a.set_amplitudes(v)
+        execute(circ, a, fuse=True, exact=False)
+        b.set_amplitudes(v)
+        execute(circ, b, fuse=False)
+        np.testing.assert_allclose(a.amplitudes(), b.amplitudes(), rtol=1e-5, atol=1e-5 * 2.0 ** (-n / 2))
+        a.close()
+        b.close()
+
+    def test_qft30_analytic(self):
+        """QFT|x> (no swaps) = exp(2 pi i k rev(x) / N) / sqrt(N) at n = 30."""
+        from paper_1805_00988_b200 import fusion
+
+        n = 30
+        x = 0b101100111000111100001011010110
+        st = State(n).reset(x)
+        execute(build_qft(n), st, fuse=True, exact=False)
+        fusion.jit_sync()
+        st.reset(x)
+        execute(build_qft(n), st, fuse=True, exact=False)
+        rev = int(format(x, f"0{n}b")[::-1], 2)
+        ks = np.arange(0, 1 << n, 1 << 17, dtype=np.int64)[:300] + 12345
+        got = np.array([st.amplitude(int(k)) for k in ks])
+        want = np.exp(2j * np.pi * ((ks * rev) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
+        np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * abs(want[0]))
+        st.close()
