@@ -234,7 +234,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     p.tile_ctr = s->tile_ctr;
     {
         const char *d = std::getenv("QSB_FUSED_DRY");
-        p.dry = d && *d >= '1' && *d <= '3' ? *d - '0' : 0;
+        p.dry = d && *d >= '1' && *d <= '4' ? *d - '0' : 0;
         const char *h = std::getenv("QSB_FUSED_L2HINT");
         p.l2hint = h && *h == '1';
     }
@@ -429,6 +429,10 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
             FOp o;
             std::memset(&o, 0, sizeof o);
             std::memcpy(o.m, op.m, sizeof o.m);
+            if (fault_flip_c() && op.kind == QS_OP_PAIR) {  // debug fault injection (QSB_FAULT_FLIP_C)
+                o.m[4] = -o.m[4];
+                o.m[5] = -o.m[5];
+            }
             o.one = 1.0f;
             uint64_t need = op.ctrl_mask;
             if (op.kind == QS_OP_PHASE) need |= 1ull << op.target;
@@ -452,7 +456,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
             } else {
                 const int lb = local_of[op.target];
                 const int slot = is_half(lb) ? -1 : reg_of[f_of(lb)];
-                o.variant = ((slot + 1) * 4 + gate_class(op.m)) * 2 + has_need;
+                o.variant = ((slot + 1) * 4 + gate_class(o.m)) * 2 + has_need;
             }
             fops.push_back(o);
         }

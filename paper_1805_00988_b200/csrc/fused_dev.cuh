@@ -61,7 +61,8 @@ struct FParams {
     int ncopies;       // TMA copies per tile (2^(K-9))
     int crow[4];       // row-index bit of copy-index bit i
     int n, K, nwbits, nstages, nruns, nops;
-    int dry;    // probes (QSB_FUSED_DRY): 1 skip the ops, 2 also the register stages, 3 also the stores
+    int dry;    // probes (QSB_FUSED_DRY): 1 skip the ops, 2 also the register stages, 3 also the stores,
+                // 4 no HBM traffic at all (compute only; the register content is garbage)
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
     int l2hint;  // TMA copies with an L2 evict_first policy
     int combine;  // generated programs: combine runs of unit-modulus diagonal ops (exact = False)
@@ -683,7 +684,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
                 mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
                 const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
-                for (int c = lane; c < (p.dry == 3 ? 0 : p.ncopies); c += 32) {
+                for (int c = lane; c < (p.dry >= 3 ? 0 : p.ncopies); c += 32) {
                     uint32_t row = row0;
                     for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
                     if (p.l2hint)
@@ -712,11 +713,14 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             pending[b] = base;
             if (lane == 0) {
                 tile_id[b] = t;
-                mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
+                if (p.dry == 4)
+                    mbar_arrive(&full[b]);  // probe: compute only, no HBM traffic
+                else
+                    mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
             }
             __syncwarp();
             const uint32_t row0 = (uint32_t)(base >> kLowQ);
-            for (int c = lane; c < p.ncopies; c += 32) {
+            for (int c = lane; c < (p.dry == 4 ? 0 : p.ncopies); c += 32) {
                 uint32_t row = row0;
                 for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
                 if (p.l2hint)
@@ -730,7 +734,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             const int b = k % kNB;
             mbar_wait(&done[b], (k / kNB) & 1);
             const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
-            for (int c = lane; c < (p.dry == 3 ? 0 : p.ncopies); c += 32) {
+            for (int c = lane; c < (p.dry >= 3 ? 0 : p.ncopies); c += 32) {
                 uint32_t row = row0;
                 for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
                 if (p.l2hint)
@@ -752,7 +756,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         const uint64_t t = tile_id[b];
         if (t == ~0ull) break;
         const uint64_t base = tile_base(t, p);
-        for (int s = 0; s < (p.dry >= 2 ? 0 : p.nstages); ++s) {
+        for (int s = 0; s < (p.dry == 2 || p.dry == 3 ? 0 : p.nstages); ++s) {
             const FStage &st = p.stages[s];
             uint32_t fb = 0;
 #pragma unroll
@@ -777,7 +781,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                     for (int j = 0; j < (1 << RB); ++j) v[j] = to_planar(v[j]);
                 }
             }
-            if (!p.dry) Prog::template run<RB>(s, st, sops, (uint32_t)tid, base, p.one, v);
+            if (!p.dry || p.dry == 4) Prog::template run<RB>(s, st, sops, (uint32_t)tid, base, p.one, v);
             if constexpr (Prog::kPlanar && UnitTraits<V>::kHalf) {
                 if (s + 1 == p.nstages) {
 #pragma unroll

@@ -287,8 +287,17 @@ int launch_phase(qs_state *s, uint64_t mask, float2 d) {
     return QS_OK;
 }
 
-int launch_sweep(qs_state *s, int target, uint64_t ctrl_mask, const float m[8]) {
+int launch_sweep(qs_state *s, int target, uint64_t ctrl_mask, const float m_in[8]) {
     const int n = s->num_qubits;
+    float mf[8];
+    for (int i = 0; i < 8; ++i) mf[i] = m_in[i];
+    const float *m = mf;
+    const bool is_diag = mf[0] == 1.0f && mf[1] == 0.0f && mf[2] == 0.0f && mf[3] == 0.0f && mf[4] == 0.0f &&
+                         mf[5] == 0.0f;
+    if (fault_flip_c() && !is_diag) {  // debug fault injection (QSB_FAULT_FLIP_C)
+        mf[4] = -mf[4];
+        mf[5] = -mf[5];
+    }
     const Gate2 g = gate_from(m);
     const uint64_t tbit = 1ull << target;
     int ncontrols = __builtin_popcountll(ctrl_mask);

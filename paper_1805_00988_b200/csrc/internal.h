@@ -39,6 +39,10 @@ inline uint64_t amp_bytes(const qs_state *s) { return s->prec == QS_DOUBLE ? 16u
 inline uint64_t state_bytes(const qs_state *s) { return amp_bytes(s) << s->num_qubits; }
 inline double2 *amps_d(const qs_state *s) { return reinterpret_cast<double2 *>(s->amps); }
 int cuda_fail(cudaError_t e, const char *what);
+// Fault injection for the parity suite (the sign-flipped `c` of
+// pkg/tests/test_cli.py:151-160): QSB_FAULT_FLIP_C=1 negates the c entry of
+// every pair gate in the sweep and fused paths.  Debug only.
+bool fault_flip_c();
 // raise a kernel's max dynamic shared memory on the current device (once per size)
 int ensure_smem_attr(const void *fn, int bytes);
 

@@ -6,6 +6,7 @@
 // same exception types.
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -38,6 +39,14 @@ int ensure_smem_attr(const void *fn, int bytes) {
     QS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     have = bytes;
     return QS_OK;
+}
+
+bool fault_flip_c() {
+    static const bool on = [] {
+        const char *e = std::getenv("QSB_FAULT_FLIP_C");
+        return e && *e == '1';
+    }();
+    return on;
 }
 
 int cuda_fail(cudaError_t e, const char *what) {
