@@ -89,6 +89,11 @@ int qs_device_count(int *out);
  * bounded per-device cache (QSB_CACHE_BYTES, default 1/4 of HBM) so that
  * new_state-style create/destroy cycles skip cudaMalloc/cudaFree. */
 int qs_release_cached(int device);
+/* Page-locked host memory (cudaMallocHost): readouts into it (qs_probabilities,
+ * qs_get_amplitudes) go straight to it by DMA, without staging copies or page
+ * faults — for callers that read large registers repeatedly. */
+int qs_host_alloc(uint64_t bytes, void **out);
+int qs_host_free(void *ptr);
 
 /* ---- lifecycle: pkg/src/pairsim/state.py:122-143 (new_state) ------------ */
 /* Allocates 8 * 2^n bytes on `device` and initialises |0...0>.

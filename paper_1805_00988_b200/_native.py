@@ -25,7 +25,8 @@ QS_SINGLE, QS_DOUBLE = 0, 1
 
 # Every symbol include/qsb200.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
-    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_release_cached", "qs_create", "qs_create_ex",
+    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_release_cached", "qs_host_alloc", "qs_host_free",
+    "qs_create", "qs_create_ex",
     "qs_precision", "qs_destroy",
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
@@ -80,6 +81,8 @@ def _declare(L):
         "qs_last_error": ([], ctypes.c_char_p),
         "qs_device_count": ([ctypes.POINTER(i32)], i32),
         "qs_release_cached": ([i32], i32),
+        "qs_host_alloc": ([u64, ctypes.POINTER(vp)], i32),
+        "qs_host_free": ([vp], i32),
         "qs_create": ([i32, i32, u64, ctypes.POINTER(vp)], i32),
         "qs_create_ex": ([i32, i32, u64, i32, ctypes.POINTER(vp)], i32),
         "qs_precision": ([vp, ctypes.POINTER(i32)], i32),
@@ -206,6 +209,20 @@ def consume_draws(seed, k: int) -> None:
     stream by k 64-bit outputs; ints and None leave nothing to advance."""
     if isinstance(seed, (np.random.Generator, np.random.BitGenerator)):
         np.random.default_rng(seed).bit_generator.advance(int(k))
+
+
+def pinned_empty(count: int, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (qs_host_alloc), freed when the
+    array (and every view of it) is gone.  Readouts into it are plain DMA."""
+    import weakref
+
+    dt = np.dtype(dtype)
+    nbytes = int(count) * dt.itemsize
+    ptr = ctypes.c_void_p()
+    check(lib().qs_host_alloc(nbytes, ctypes.byref(ptr)))
+    buf = (ctypes.c_char * max(1, nbytes)).from_address(ptr.value)
+    weakref.finalize(buf, lib().qs_host_free, ctypes.c_void_p(ptr.value))
+    return np.frombuffer(buf, dtype=dt, count=int(count))
 
 
 def f32ptr(a: np.ndarray):

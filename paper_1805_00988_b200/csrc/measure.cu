@@ -601,6 +601,29 @@ int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host
     const uint64_t step = count < piece ? count : piece;
     int rc = ensure_scratch(s, 2 * step * sizeof(double));
     if (rc) return rc;
+    {
+        // pinned destination (qs_host_alloc / cudaHostRegister): |a|^2 pieces
+        // go straight to it by DMA, no staging copy and no page faults
+        cudaPointerAttributes attr;
+        if (cudaPointerGetAttributes(&attr, host) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+            double *dev[2] = {(double *)s->scratch, (double *)s->scratch + step};
+            for (uint64_t done = 0, i = 0; done < count; done += step, ++i) {
+                const uint64_t m = (count - done) < step ? (count - done) : step;
+                unsigned grid = (unsigned)((m + 255) / 256);
+                if (grid > (unsigned)s->num_sms * 16) grid = s->num_sms * 16;
+                double *d = dev[i & 1];
+                if (s->prec == QS_DOUBLE)
+                    k_probs<<<grid, 256, 0, s->stream>>>(amps_d(s) + offset + done, d, m);
+                else
+                    k_probs<<<grid, 256, 0, s->stream>>>(s->amps + offset + done, d, m);
+                QS_CUDA(cudaGetLastError());
+                QS_CUDA(cudaMemcpyAsync(host + done, d, m * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+            }
+            QS_CUDA(cudaStreamSynchronize(s->stream));
+            return QS_OK;
+        }
+        cudaGetLastError();
+    }
     rc = ensure_pinned(s, 2 * step * sizeof(double));
     if (rc) return rc;
     // A fresh numpy result page-faults 4-KiB pages during the host copy: ask

@@ -127,6 +127,19 @@ void stream_release(int device, cudaStream_t s) {
 
 }  // namespace qsb
 
+extern "C" int qs_host_alloc(uint64_t bytes, void **out) {
+    if (!out) return qsb::set_error(QS_ERR_NULL, "null output pointer");
+    *out = nullptr;
+    const cudaError_t e = cudaMallocHost(out, bytes ? bytes : 1);
+    if (e != cudaSuccess) return qsb::cuda_fail(e, "cudaMallocHost");
+    return QS_OK;
+}
+
+extern "C" int qs_host_free(void *ptr) {
+    if (ptr) cudaFreeHost(ptr);
+    return QS_OK;
+}
+
 extern "C" int qs_release_cached(int device) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess) {

@@ -79,13 +79,23 @@ def plan(num_qubits: int, ops, tile_qubits: int | None = None, reorder: bool = F
     floating point (e.g. H(a) H(b) sums (v0 + v1) + (v2 + v3) where H(b) H(a)
     sums (v0 + v2) + (v1 + v3)), so results agree with the reference to
     rounding (tested at rtol 1e-5, the north_star bar) instead of bit for
-    bit.  The default planner only moves permutations, which is exact."""
-    pl = _plan_reorder if reorder else _plan
-    if tile_qubits is None and num_qubits >= 13:
-        p13 = pl(num_qubits, ops, 13)
-        p12 = pl(num_qubits, ops, 12)
-        return p12 if 4 * len(p12) <= 5 * len(p13) else p13
-    return pl(num_qubits, ops, tile_qubits)
+    bit.  The default planner only moves permutations, which is exact.  With
+    reorder=True the in-order plan is still used when it needs no more
+    passes (QFT: the reordered plan pulls later rows' phases forward into
+    heavier passes for no pass saved)."""
+    def choose(pl):
+        if tile_qubits is None and num_qubits >= 13:
+            p13 = pl(num_qubits, ops, 13)
+            p12 = pl(num_qubits, ops, 12)
+            return p12 if 4 * len(p12) <= 5 * len(p13) else p13
+        return pl(num_qubits, ops, tile_qubits)
+
+    ops = list(ops)
+    base = choose(_plan)
+    if not reorder:
+        return base
+    alt = choose(_plan_reorder)
+    return alt if len(alt) < len(base) else base
 
 
 def _plan_reorder(num_qubits: int, ops, tile_qubits: int | None) -> list[Pass]:

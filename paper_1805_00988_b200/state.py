@@ -307,9 +307,15 @@ class State:
             raise IndexError(f"basis index {index} out of range [0, {self.dim})")
         return complex(self.amplitudes(index, 1)[0])
 
-    def probabilities(self, offset: int = 0, count: int | None = None) -> np.ndarray:
+    def probabilities(self, offset: int = 0, count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        """fp64 |a|^2 (measure.py:29-34).  `out`: a float64 array to fill (e.g.
+        _native.pinned_empty(2**n): page-locked, filled by DMA with no staging
+        copy), else a fresh array."""
         count = self.dim - offset if count is None else count
-        out = np.empty(count, dtype=np.float64)
+        if out is None:
+            out = np.empty(count, dtype=np.float64)
+        elif out.dtype != np.float64 or out.size != count or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of `count` elements")
         N.check(N.lib().qs_probabilities(self.handle, int(offset), int(count), out.ctypes.data))
         return out
 

@@ -23,6 +23,7 @@ ap.add_argument("--n", type=int, default=30)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--k", type=int, default=None)
 ap.add_argument("--circuit", default="qft")
+ap.add_argument("--inexact", action="store_true", help="reorder planner + combined diagonal runs")
 a = ap.parse_args()
 n = a.n
 st = State(n)
@@ -31,7 +32,7 @@ if a.circuit == "qft":
 else:
     from paper_1805_00988_b200 import layered_random_circuit
     circ = layered_random_circuit(n, 20, seed=32)
-passes = fusion.plan(n, lower_ops(circ), a.k)
+passes = fusion.plan(n, lower_ops(circ), a.k, reorder=a.inexact)
 s = torch.cuda.ExternalStream(st.stream())
 out = []
 dump = os.environ.pop("QSB_FUSED_DUMP", None)
@@ -39,14 +40,14 @@ for i, p in enumerate(passes):
     arr = p.op_array()
     if dump:
         os.environ["QSB_FUSED_DUMP"] = dump
-    st.apply_fused(p.tile, arr)  # compile + warm (+ dump this pass's plan once)
+    st.apply_fused(p.tile, arr, combine=a.inexact)  # compile + warm (+ dump this pass's plan once)
     st.flush()
     os.environ.pop("QSB_FUSED_DUMP", None)
     ts = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        st.apply_fused(p.tile, arr)
+        st.apply_fused(p.tile, arr, combine=a.inexact)
         e1.record(s)
         st.flush()
         ts.append(e0.elapsed_time(e1))

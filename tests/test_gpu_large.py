@@ -358,3 +358,25 @@ class TestInexactMode:
         want = np.exp(2j * np.pi * ((ks * rev) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
         np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * abs(want[0]))
         st.close()
+
+
+class TestReadout:
+    def test_probabilities_into_pinned_array(self):
+        """State.probabilities(out=pinned_empty(...)): the DMA path gives the
+        bytes of the staged path (and of the oracle)."""
+        from paper_1805_00988_b200 import _native as N
+
+        n = 21
+        rng = np.random.default_rng(21)
+        v = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)).astype(np.complex64)
+        st = State(n)
+        st.set_amplitudes(v)
+        fresh = st.probabilities()
+        pin = N.pinned_empty(1 << n)
+        got = st.probabilities(out=pin)
+        assert got is pin and got.tobytes() == fresh.tobytes() == oc.probabilities(v).tobytes()
+        part = N.pinned_empty(1000)
+        assert st.probabilities(12345, 1000, out=part).tobytes() == fresh[12345:13345].tobytes()
+        with pytest.raises(ValueError):
+            st.probabilities(out=np.empty(10))
+        st.close()
