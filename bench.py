@@ -463,6 +463,8 @@ def run_sharded(args):
             extras["strong34"] = measure_strong(34, world, local, 1, 1)
         except Exception as exc:  # noqa: BLE001
             extras["strong34"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if not args.no_extras:
+        extras["single_process_c_abi"] = run_single_process(n, world, rank)
     if world >= 4 and not args.no_extras:
         extras["config5_hlayer_qft36"] = run_config5(st, eng, local, world)
     line = None
@@ -635,6 +637,51 @@ def run_strong(args):
         print(line)
 
 
+def run_single_process(n, world, rank):
+    """The same register driven by ONE process over all N GPUs through the C
+    ABI (qs_create_sharded: ncclCommInitAll communicators, NCCL or peer
+    exchanges).  Rank 0 runs it while the other ranks wait at a barrier.
+    Host wall clock around device-synchronised calls."""
+    import torch.distributed as dist
+
+    out = None
+    if rank == 0:
+        try:
+            from paper_1805_00988_b200 import build_qft
+            from paper_1805_00988_b200.multigpu import MultiDeviceState
+
+            out = {"n_qubits": n, "devices": world}
+            for label, exch, peer in (("nccl_swaps", "nccl", False), ("p2p_swaps", "p2p", False),
+                                      ("peer_gates", "p2p", True)):
+                md = MultiDeviceState(n, list(range(world)))
+                try:
+                    md.set_mode(peer_gates=peer, exchange=exch)
+                except Exception as exc:  # noqa: BLE001  (e.g. no NCCL communicators)
+                    out[label] = {"error": f"{type(exc).__name__}: {exc}"}
+                    md.close()
+                    continue
+                for q in range(n):
+                    md.h(q)
+                md.flush()
+                md.reset(0)
+                md.flush()
+                t0 = time.perf_counter()
+                for q in range(n):
+                    md.h(q)
+                md.flush()
+                t_layer = time.perf_counter() - t0
+                t0 = time.perf_counter()
+                md.run(build_qft(n))
+                md.flush()
+                t_qft = time.perf_counter() - t0
+                out[label] = {"hlayer_ms": t_layer * 1e3, "qft_unfused_ms": t_qft * 1e3, **md.stats()}
+                md.close()
+        except Exception as exc:  # noqa: BLE001
+            out = {"error": f"{type(exc).__name__}: {exc}"}
+    dist.barrier()
+    return out
+
+
 def run_global_gate_probe(n, local, world, reps=3):
     """H on each of the log2(N) global qubits from the identity qubit map:
     NCCL qubit swaps + local sweeps (default path) vs one peer-memory kernel
@@ -747,30 +794,43 @@ def run_extras(st, stream, n, cpu=True, harness=True):
     from paper_1805_00988_b200 import State, build_hadamard_layer, build_qft, fusion, layered_random_circuit
     from paper_1805_00988_b200.circuits import lower_ops
 
-    def timed(state, strm, passes, reps=3):
-        # untimed run (queues the pass programs' compiles, csrc/jit.cu), then
-        # wait for them so the timed runs launch compiled programs only
-        fusion.run(state, passes)
+    def timed(state, strm, passes, reps=3, combine=False, cold=None):
+        # first run = the cold number (pass programs' compiles queued on host
+        # threads, csrc/jit.cu, the passes meanwhile on the interpreter
+        # kernel); then wait for the compiles so the timed runs launch
+        # compiled programs only
+        t0 = time.perf_counter()
+        fusion.run(state, passes, combine=combine)
+        state.flush()
+        if cold is not None:
+            cold.append((time.perf_counter() - t0) * 1e3)
         fusion.jit_sync()
-        fusion.run(state, passes)
+        fusion.run(state, passes, combine=combine)
         state.flush()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(strm)
         for _ in range(reps):
-            fusion.run(state, passes)
+            fusion.run(state, passes, combine=combine)
         b.record(strm)
         state.flush()
         return a.elapsed_time(b) / reps
 
+    def fused_entry(circ, nq, state, strm, exact=True, reps=3):
+        passes = fusion.plan(nq, lower_ops(circ), reorder=not exact)
+        cold = []
+        ms = timed(state, strm, passes, reps=reps, combine=not exact, cold=cold)
+        return {"gates": circ.gate_count(), "passes": len(passes), "ms": ms, "cold_first_run_ms": cold[0],
+                "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
+                "pass_bytes": len(passes) * 16 * (1 << nq),
+                "achieved_GBps": len(passes) * 16 * (1 << nq) / (ms / 1e3) / 1e9,
+                "mode": "exact (bit-identical to the reference)" if exact else
+                        "exact=False (reordered passes + combined diagonal runs; rtol 1e-5 vs the reference)"}
+
     res = {}
-    for name, circ in (("hlayer30_fused", build_hadamard_layer(n)), ("qft30_fused", build_qft(n))):
-        passes = fusion.plan(n, lower_ops(circ))
-        ms = timed(st, stream, passes)
-        res[name] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
-                     "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
-                     "pass_bytes": len(passes) * 16 * (1 << n),
-                     "achieved_GBps": len(passes) * 16 * (1 << n) / (ms / 1e3) / 1e9}
+    res["hlayer30_fused"] = fused_entry(build_hadamard_layer(n), n, st, stream)
+    res["qft30_fused"] = fused_entry(build_qft(n), n, st, stream)
+    res["qft30_fused_inexact"] = fused_entry(build_qft(n), n, st, stream, exact=False)
 
     # K2 / K3 / K4 single-op sweeps at full size (touched bytes
     # and the full-sweep equivalent reported separately)
@@ -871,34 +931,59 @@ def run_extras(st, stream, n, cpu=True, harness=True):
                                   "note": "host wall clock per circuit, 10 reps; direct = one ctypes call + "
                                           "launch per gate, graph = State.record() once, Graph.replay()"}
 
-    # measure path on the 30-qubit register (after the fused layers above it
-    # holds a generic state): exact sampling chain (M1-M6, device-only) and
-    # probabilities streamed to a host array
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    st.sample_outcomes(1000, 1)
-    a.record(stream)
-    st.sample_outcomes(1_000_000, 2)
-    b.record(stream)
-    st.flush()
+    # measure path on the 30-qubit register: the exact sampling chain (M1-M6,
+    # device-only; cost depends on the state's CDF) on a generic state, the
+    # uniform state and a basis state, and probabilities to the host into a
+    # fresh pageable array (first touch included) and into a reused pinned one
+    from paper_1805_00988_b200 import _native as _Nm
+
+    samp = {}
+    for kind in ("generic", "uniform", "basis"):
+        if kind == "uniform":
+            st.reset(0)
+            for q in range(n):
+                st.h(q)
+        elif kind == "basis":
+            st.reset(123456789)
+        st.sample_outcomes(1000, 1)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        st.sample_outcomes(1_000_000, 2)
+        b.record(stream)
+        st.flush()
+        samp[kind] = a.elapsed_time(b)
+    st.reset(0)
+    for q in range(n):
+        st.h(q)
+    st.t(3)
     t0 = time.perf_counter()
     pr = st.probabilities()
     t_pr = time.perf_counter() - t0
-    res["measure30"] = {"sample_1e6_ms": a.elapsed_time(b), "probabilities_to_host_ms": t_pr * 1e3,
-                        "probabilities_bytes": pr.nbytes,
-                        "note": "sample: exact sequential-CDF chain + 1e6 PCG64 draws (bit-exact with "
-                                "pairsim.sample), events around the call; probabilities: fp64 |a|^2 "
-                                "streamed D2H into a pageable numpy array, host wall clock"}
     del pr
+    pin = _Nm.pinned_empty(1 << n)
+    st.probabilities(out=pin)
+    t0 = time.perf_counter()
+    st.probabilities(out=pin)
+    t_pin = time.perf_counter() - t0
+    res["measure30"] = {"sample_1e6_ms": samp, "probabilities_to_host_ms": t_pr * 1e3,
+                        "probabilities_to_pinned_ms": t_pin * 1e3,
+                        "probabilities_bytes": 8 << n,
+                        "probabilities_GBps": {"fresh_pageable": (8 << n) / t_pr / 1e9,
+                                               "reused_pinned": (8 << n) / t_pin / 1e9},
+                        "note": "sample: exact sequential-CDF chain + 1e6 PCG64 draws (bit-exact with "
+                                "pairsim.sample), CUDA events, per state kind (generic = after the fused "
+                                "circuits above, uniform = H layer, basis = |123456789>); probabilities: fp64 "
+                                "|a|^2 to a fresh numpy array (staged through pinned buffers, page faults "
+                                "included) and into a reused pinned array (State.probabilities(out=...), "
+                                "direct DMA), host wall clock"}
+    del pin
 
     # config 3: 28-qubit QFT (fused), parity vs pairsim is in tests/test_gpu_parity.py
     s28 = State(28)
     s28_stream = torch.cuda.ExternalStream(s28.stream())
-    circ = build_qft(28)
-    passes = fusion.plan(28, lower_ops(circ))
-    ms = timed(s28, s28_stream, passes)
-    res["config3_qft28_fused"] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
-                                  "effective_gates_per_s": circ.gate_count() / (ms / 1e3)}
+    res["config3_qft28_fused"] = fused_entry(build_qft(28), 28, s28, s28_stream)
+    res["config3_qft28_fused_inexact"] = fused_entry(build_qft(28), 28, s28, s28_stream, exact=False)
     s28.close()
 
     # complex128 (Precision.DOUBLE) sweeps: a 29-qubit register is 8 GiB like
@@ -955,8 +1040,9 @@ def run_extras(st, stream, n, cpu=True, harness=True):
     from paper_1805_00988_b200 import _native as _N
 
     sv = {}
-    for mode, peer in (("swap", False), ("peer", True)):
-        vs = ShardedState.virtual(31, 2, peer_gates=peer)
+    for mode, peer, exch in (("swap_copy", False, "nccl"), ("swap_peer_kernel", False, "peer"),
+                             ("peer_gates", True, "peer")):
+        vs = ShardedState.virtual(31, 2, peer_gates=peer, exchange=exch)
         for q in range(31):
             vs.apply_gate(_Hg, q)
         vs.synchronize()
@@ -968,7 +1054,24 @@ def run_extras(st, stream, n, cpu=True, harness=True):
         vs.synchronize()
         sv[mode] = {"layer_ms": (time.perf_counter() - t0) * 1e3, "swaps": vs.swaps,
                     "peer_gates": vs.peer_gate_count}
-        del vs
+        vs.close()
+        _N.lib().qs_release_cached(-1)
+    # the same layer through the single-process C ABI (qs_create_sharded)
+    from paper_1805_00988_b200.multigpu import MultiDeviceState
+
+    for mode, peer in (("c_abi_swap", False), ("c_abi_peer_gates", True)):
+        md = MultiDeviceState(31, [0, 0], peer_gates=peer)
+        for q in range(31):
+            md.h(q)
+        md.flush()
+        md.reset(0)
+        md.flush()
+        t0 = time.perf_counter()
+        for q in range(31):
+            md.h(q)
+        md.flush()
+        sv[mode] = {"layer_ms": (time.perf_counter() - t0) * 1e3, **md.stats()}
+        md.close()
         _N.lib().qs_release_cached(-1)
     res["sharded_virtual_31q_2shards"] = {**sv, "note": "H layer over 31 qubits as 2 virtual shards on one "
                                           "B200 (host wall clock incl. per-gate syncs of the sharded layer)"}
@@ -1011,12 +1114,39 @@ def run_extras(st, stream, n, cpu=True, harness=True):
         return res
     s32_stream = torch.cuda.ExternalStream(s32.stream())
     circ = layered_random_circuit(32, 20, seed=32)
-    passes = fusion.plan(32, lower_ops(circ))
-    ms = timed(s32, s32_stream, passes, reps=1)
-    res["config4_random32_fused"] = {"gates": circ.gate_count(), "passes": len(passes), "ms": ms,
-                                     "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
-                                     "pass_bytes": len(passes) * 16 * (1 << 32),
-                                     "achieved_GBps": len(passes) * 16 * (1 << 32) / (ms / 1e3) / 1e9}
+    res["config4_random32_fused"] = fused_entry(circ, 32, s32, s32_stream, reps=1)
+    try:
+        s32b = State(32)
+        s32b_stream = torch.cuda.ExternalStream(s32b.stream())
+        ent = fused_entry(circ, 32, s32b, s32b_stream, exact=False, reps=1)
+        # agreement with the exact result (both registers hold the circuit
+        # applied to the previous contents: reset and run once more each)
+        for s_, ex in ((s32, True), (s32b, False)):
+            s_.reset(0)
+            fusion.run(s_, fusion.plan(32, lower_ops(circ), reorder=not ex), combine=not ex)
+            s_.flush()
+
+        def tview(s_):
+            ptr, nf = s_.device_pointer(), 2 << 32
+
+            class _CAI:
+                __cuda_array_interface__ = {"shape": (nf,), "typestr": "<f4", "data": (ptr, False),
+                                            "version": 3, "strides": None}
+
+            return torch.as_tensor(_CAI(), device=torch.device("cuda", torch.cuda.current_device()))
+
+        va, vb = tview(s32), tview(s32b)
+        worst, peak = 0.0, 0.0
+        for off in range(0, va.numel(), 1 << 28):
+            worst = max(worst, float((va[off: off + (1 << 28)] - vb[off: off + (1 << 28)]).abs().max()))
+            peak = max(peak, float(va[off: off + (1 << 28)].abs().max()))
+        ent["max_abs_diff_vs_exact"] = worst
+        ent["max_abs_amplitude"] = peak
+        res["config4_random32_fused_inexact"] = ent
+        del va, vb
+        s32b.close()
+    except Exception as exc:  # noqa: BLE001
+        res["config4_random32_fused_inexact"] = {"error": f"{type(exc).__name__}: {exc}"}
     s32.close()
 
     # strong-scaling reference point: one 34-qubit register (128 GiB) on this GPU

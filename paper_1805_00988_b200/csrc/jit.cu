@@ -197,9 +197,11 @@ std::string generate(const FParams &p, int K, int RB) {
     // swap_sel: no divergent branch), 0 a branch around the body
     int sel_mode = 1;
     if (const char *e = std::getenv("QSB_JIT_SEL")) sel_mode = std::atoi(e);
-    // planar register layout (fused_dev.cuh: pphase / ppair): 2 (default)
-    // for phase-dominated passes, 1 always, 0 never
-    int planar_mode = 2;
+    // planar register layout (fused_dev.cuh: pphase / ppair): 0 (default:
+    // measured slower on B200 — the packed results land in fresh register
+    // pairs and ptxas copies them home around the uniform branches; QFT(30)
+    // 34.0 -> 38.3 ms), 1 always, 2 for phase-dominated passes
+    int planar_mode = 0;
     if (const char *e = std::getenv("QSB_JIT_PLANAR")) planar_mode = std::atoi(e);
     int nphase = 0;
     for (int o = 0; o < p.nops; ++o) nphase += p.ops[o].variant >= kPhaseVariant;
