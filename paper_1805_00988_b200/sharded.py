@@ -433,6 +433,7 @@ class ShardedState:
         self._peers = None
         self.peer_gate_count = 0
         self.peer_swaps = 0
+        self.shard_phases = 0
 
     # ---- constructors ------------------------------------------------------
     @classmethod
@@ -535,6 +536,21 @@ class ShardedState:
                 self.exchange = "nccl"
         return bool(self._peers)
 
+    def _shard_phase(self, rank_bits, m: np.ndarray) -> None:
+        """A diagonal gate whose bits are all global: every amplitude of the
+        shards whose rank bits are all 1 is multiplied by d — no exchange.
+        Applied as the pair sweep of diag(d, d) (v_a' = d v_a + 0 v_b, the
+        same product bit for bit up to the sign of zero)."""
+        need = 0
+        for b in rank_bits:
+            need |= 1 << b
+        dd = np.zeros(8, np.float32)
+        dd[0], dd[1], dd[6], dd[7] = m[6], m[7], m[6], m[7]
+        for eng, r in zip(self.engines, self.ranks):
+            if (r & need) == need:
+                eng.apply(N.QS_OP_PAIR, 0, 0, dd)
+        self.shard_phases += 1
+
     def _peer_gate(self, rank_bit: int, cmask: int, need: int, m: np.ndarray) -> None:
         """Pair update with the target on global rank bit `rank_bit`, applied by
         both partners in one peer-memory kernel each (csrc/peer.cu)."""
@@ -567,7 +583,10 @@ class ShardedState:
             if local:
                 target = local[0]
                 controls = [q for q in qs if q != target]
-        if kind == N.QS_OP_PAIR and not lay.is_local(target) and self._peer_ready():
+        if kind == N.QS_OP_PHASE and not any(lay.is_local(q) for q in qs):
+            self._shard_phase([lay.pos[q] - lay.L for q in qs], m)
+            return self
+        if kind == N.QS_OP_PAIR and not lay.is_local(target) and self.peer_gates and self._peer_ready():
             cmask, need = self._control_masks(controls)
             self._peer_gate(lay.pos[target] - lay.L, cmask, need, m)
             return self
@@ -648,9 +667,13 @@ class ShardedState:
                 if local:
                     target = local[0]
                     controls = tuple(q for q in qs if q != target)
+            if kind == N.QS_OP_PHASE and not any(lay.is_local(q) for q in qs):
+                flush()
+                self._shard_phase([lay.pos[q] - lay.L for q in qs], m)
+                continue
             if not lay.is_local(target):
                 flush()
-                if kind == N.QS_OP_PAIR and self._peer_ready():
+                if kind == N.QS_OP_PAIR and self.peer_gates and self._peer_ready():
                     cmask, need = self._control_masks(controls)
                     self._peer_gate(lay.pos[target] - lay.L, cmask, need, m)
                     continue

@@ -279,3 +279,26 @@ def test_gloo_distributed_matches_oracle(world, n, peer, chunk):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     amps_ok, probs_ok, norm_ok, swaps, draws_ok = q.get(timeout=5)
     assert amps_ok and probs_ok and norm_ok and swaps > 0 and draws_ok
+
+
+def test_all_global_diagonal_gates_need_no_exchange():
+    """A diagonal gate whose bits are all global multiplies whole shards in
+    place (no qubit swap), with the oracle's values."""
+    n, shards = 7, 4
+    basis = (1 << (n - 1)) | (1 << (n - 2)) | 5
+    ins = (ControlledApply(u1(0.37), n - 1, n - 2), Apply(FIXED_GATES["t"], n - 1),
+           ControlledApply(FIXED_GATES["s"], n - 2, n - 1), Apply(FIXED_GATES["h"], 0))
+    circ = Circuit(n, ins)
+    for use_run in (False, True):
+        st = ShardedState.virtual(n, shards, engine_factory=OracleEngine)
+        st.reset(basis)
+        if use_run:
+            st.run(circ)
+        else:
+            for i in ins:
+                if isinstance(i, Apply):
+                    st.apply_gate(i.gate, i.target)
+                else:
+                    st.apply_controlled_gate(i.gate, i.control, i.target)
+        assert st.shard_phases == 3 and st.swaps == 0
+        assert same_values(st.amplitudes(), oracle_run(circ, basis))
