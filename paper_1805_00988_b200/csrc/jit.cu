@@ -24,6 +24,7 @@
 // CPU fallback).
 
 #include <dlfcn.h>
+#include <sys/stat.h>
 #include <pthread.h>
 
 #include <cmath>
@@ -364,7 +365,9 @@ std::string generate(const FParams &p, int K, int RB) {
                 o = e;
                 continue;
             }
-            for (; o < e; ++o) {
+            // one op per iteration: the next op may start a combined run or
+            // a tile loop (the variant run above is only for the loop form)
+            for (e = o + 1; o < e; ++o) {
                 const FOp &op = p.ops[o];
                 const std::string test = op_test(op), utest = uniform_test(op), ltest = lane_test(op);
                 const bool is_phase = op.variant >= kPhaseVariant;
@@ -499,6 +502,9 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
 // loaded into the device context by the next launching thread that asks for
 // it (or by qs_jit_sync), so no host thread blocks on a compile unless the
 // caller asks for it (QSB_FUSED_JIT=2, qs_jit_sync).
+struct Job;
+bool compile_nvrtc(Job &job);
+
 struct Job {
     int device = 0;
     std::string src;
@@ -524,7 +530,99 @@ int jit_mode() {
     return std::atoi(e);
 }
 
+// On-disk cache of compiled pass programs: a process that runs a circuit
+// compiled before (same generated source, same options) loads the cubin
+// instead of recompiling.  File = [u64 source length][source][cubin], so a
+// hash collision is detected by comparing the source.  Directory:
+// QSB_JIT_CACHE_DIR, else $XDG_CACHE_HOME/qsb200-jit or ~/.cache/qsb200-jit;
+// QSB_JIT_CACHE=0 disables it.
+std::string cache_path(const std::string &src) {
+    const char *off = std::getenv("QSB_JIT_CACHE");
+    if (off && *off == '0') return "";
+    std::string dir;
+    if (const char *d = std::getenv("QSB_JIT_CACHE_DIR")) {
+        dir = d;
+    } else if (const char *x = std::getenv("XDG_CACHE_HOME")) {
+        dir = std::string(x) + "/qsb200-jit";
+    } else if (const char *h = std::getenv("HOME")) {
+        dir = std::string(h) + "/.cache/qsb200-jit";
+    } else {
+        return "";
+    }
+    uint64_t hsh = 1469598103934665603ull;  // FNV-1a over the source + the target
+    for (unsigned char c : src + "|sm_100a|v1") hsh = (hsh ^ c) * 1099511628211ull;
+    char name[40];
+    std::snprintf(name, sizeof name, "/%016llx.bin", (unsigned long long)hsh);
+    return dir + name;
+}
+
+bool cache_load(const std::string &path, const std::string &src, std::vector<char> &cubin) {
+    if (path.empty()) return false;
+    FILE *f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    bool ok = false;
+    uint64_t len = 0;
+    if (std::fread(&len, 8, 1, f) == 1 && len == src.size()) {
+        std::string got(len, '\0');
+        if (std::fread(&got[0], 1, len, f) == len && got == src) {
+            std::vector<char> rest;
+            char buf[65536];
+            size_t k;
+            while ((k = std::fread(buf, 1, sizeof buf, f)) > 0) rest.insert(rest.end(), buf, buf + k);
+            if (!rest.empty()) {
+                cubin.swap(rest);
+                ok = true;
+            }
+        }
+    }
+    std::fclose(f);
+    return ok;
+}
+
+void cache_store(const std::string &path, const std::string &src, const std::vector<char> &cubin) {
+    if (path.empty()) return;
+    const size_t slash = path.rfind('/');
+    const std::string dir = path.substr(0, slash);
+    std::string cmd;
+    for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+        if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)pthread_self());
+    FILE *f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const uint64_t len = src.size();
+    bool ok = std::fwrite(&len, 8, 1, f) == 1 && std::fwrite(src.data(), 1, len, f) == len &&
+              std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+    ok = std::fclose(f) == 0 && ok;
+    if (ok)
+        std::rename(tmp.c_str(), path.c_str());
+    else
+        std::remove(tmp.c_str());
+}
+
+// the cache key: the generated source plus the device headers it includes
+// (a rebuilt library with changed headers must not load stale programs)
+std::string cache_key(const std::string &src) {
+    static const std::string tag = [] {
+        uint64_t h = 1469598103934665603ull;
+        for (const char *t : {kJitCommon, kJitFusedDev})
+            for (const char *c = t; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;
+        char b[40];
+        std::snprintf(b, sizeof b, "\n// headers %016llx\n", (unsigned long long)h);
+        return std::string(b);
+    }();
+    return src + tag;
+}
+
 bool compile_cubin(Job &job) {
+    const std::string key = cache_key(job.src);
+    const std::string cpath = cache_path(key);
+    if (cache_load(cpath, key, job.cubin)) return true;
+    const bool ok = compile_nvrtc(job);
+    if (ok) cache_store(cpath, key, job.cubin);
+    return ok;
+}
+
+bool compile_nvrtc(Job &job) {
     const Nvrtc &nv = nvrtc();
     const char *hdrs[2] = {kJitCommon, kJitFusedDev};
     const char *names[2] = {"common.cuh", "fused_dev.cuh"};
