@@ -232,6 +232,67 @@ std::string generate(const FParams &p, int K, int RB) {
            "                        __reduce_or_sync(0xffffffffu, (unsigned)base);\n"
            "    (void)wid;\n    (void)ub;\n    switch (s) {\n";
     char buf[256];
+    int group_uniform = 1;  // QSB_JIT_GROUP=0: one branch per op
+    if (const char *e = std::getenv("QSB_JIT_GROUP")) group_uniform = std::atoi(e);
+    // One op as generated source.  grouped: the caller has already branched
+    // on the op's warp-uniform test; only the lane part remains.
+    auto emit_one = [&](const FOp &op, bool grouped) -> std::string {
+        std::string out;
+        char b[256];
+        const std::string utest = grouped ? std::string() : uniform_test(op), ltest = lane_test(op);
+        std::string test = utest;
+        if (!ltest.empty()) test = test.empty() ? ltest : test + " && " + ltest;
+        const bool in_branch = grouped || !utest.empty();
+        const bool is_phase = op.variant >= kPhaseVariant;
+        const int cls = is_phase ? -1 : (op.variant / 2) % 4;
+        if (sel_mode && !ltest.empty() && (is_phase || cls == kSwap)) {
+            // predicated selection under the lane test, branch only on the
+            // (warp-uniform) rest
+            out += utest.empty() ? "      {" : "      if (" + utest + ") {";
+            if (is_phase) {
+                const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
+                std::snprintf(b, sizeof b, " %s<%d, %s, RB>(%s, make_float2(",
+                              planar ? (in_branch ? "pphase_sel_cs" : "pphase_sel") : "phase_sel", R,
+                              odd ? "true" : "false", ltest.c_str());
+                out += b;
+                hexf(out, op.m[6]);
+                out += ", ";
+                hexf(out, op.m[7]);
+                out += "), v); }\n";
+            } else {
+                const int slot = (op.variant / 2) / 4 - 1;
+                std::snprintf(b, sizeof b, " %s<%d, %u, %s, RB>(%s, v); }\n", planar ? "pswap_sel" : "swap_sel", slot,
+                              op.reg_need, op.half_need ? "true" : "false", ltest.c_str());
+                out += b;
+            }
+            return out;
+        }
+        out += test.empty() ? "      {" : "      if (" + test + ") {";
+        if (is_phase) {
+            const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
+            const bool scalar = phase_mode == 2 || (phase_mode == 1 && (in_branch || !test.empty()));
+            std::snprintf(b, sizeof b, " %s<%d, %s, RB>(make_float2(",
+                          planar ? (in_branch || !test.empty() ? "pphase_cs" : "pphase")
+                                 : (scalar ? "phase_cs" : "phase_ct"),
+                          R, odd ? "true" : "false");
+            out += b;
+            hexf(out, op.m[6]);
+            out += ", ";
+            hexf(out, op.m[7]);
+            out += "), v); }\n";
+        } else {
+            const int slot = (op.variant / 2) / 4 - 1;
+            out += " const float m[8] = {";
+            for (int i = 0; i < 8; ++i) {
+                if (i) out += ", ";
+                hexf(out, op.m[i]);
+            }
+            std::snprintf(b, sizeof b, "}; %s<%d, %d, %u, %s, RB>(m, one, v); }\n", planar ? "ppair" : "pair_ct", slot,
+                          cls, op.reg_need, op.half_need ? "true" : "false");
+            out += b;
+        }
+        return out;
+    };
     for (int k = 0; k < p.nstages; ++k) {
         const FStage &st = p.stages[k];
         std::snprintf(buf, sizeof buf, "    case %d: {\n", k);
@@ -365,59 +426,31 @@ std::string generate(const FParams &p, int K, int RB) {
                 o = e;
                 continue;
             }
-            // one op per iteration: the next op may start a combined run or
-            // a tile loop (the variant run above is only for the loop form)
-            for (e = o + 1; o < e; ++o) {
-                const FOp &op = p.ops[o];
-                const std::string test = op_test(op), utest = uniform_test(op), ltest = lane_test(op);
-                const bool is_phase = op.variant >= kPhaseVariant;
-                const int cls = is_phase ? -1 : (op.variant / 2) % 4;
-                if (sel_mode && !ltest.empty() && (is_phase || cls == kSwap)) {
-                    // predicated selection under the lane test, branch only on
-                    // the (warp-uniform) rest
-                    src += utest.empty() ? "      {" : "      if (" + utest + ") {";
-                    if (is_phase) {
-                        const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
-                        std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(%s, make_float2(",
-                                      planar ? (utest.empty() ? "pphase_sel" : "pphase_sel_cs") : "phase_sel", R,
-                                      odd ? "true" : "false", ltest.c_str());
-                        src += buf;
-                        hexf(src, op.m[6]);
-                        src += ", ";
-                        hexf(src, op.m[7]);
-                        src += "), v); }\n";
-                    } else {
-                        const int slot = (op.variant / 2) / 4 - 1;
-                        std::snprintf(buf, sizeof buf, " %s<%d, %u, %s, RB>(%s, v); }\n",
-                                      planar ? "pswap_sel" : "swap_sel", slot, op.reg_need,
-                                      op.half_need ? "true" : "false", ltest.c_str());
-                        src += buf;
-                    }
-                    continue;
-                }
-                src += test.empty() ? "      {" : "      if (" + test + ") {";
-                if (is_phase) {
-                    const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
-                    const bool scalar = phase_mode == 2 || (phase_mode == 1 && !test.empty());
-                    std::snprintf(buf, sizeof buf, " %s<%d, %s, RB>(make_float2(",
-                                  planar ? (test.empty() ? "pphase" : "pphase_cs") : (scalar ? "phase_cs" : "phase_ct"),
-                                  R, odd ? "true" : "false");
-                    src += buf;
-                    hexf(src, op.m[6]);
-                    src += ", ";
-                    hexf(src, op.m[7]);
-                    src += "), v); }\n";
-                } else {
-                    const int slot = (op.variant / 2) / 4 - 1;
-                    src += " const float m[8] = {";
-                    for (int i = 0; i < 8; ++i) {
-                        if (i) src += ", ";
-                        hexf(src, op.m[i]);
-                    }
-                    std::snprintf(buf, sizeof buf, "}; %s<%d, %d, %u, %s, RB>(m, one, v); }\n",
-                                  planar ? "ppair" : "pair_ct", slot, cls, op.reg_need, op.half_need ? "true" : "false");
-                    src += buf;
-                }
+            // one op per iteration (the next op may start a combined run or a
+            // tile loop); consecutive ops under the SAME warp-uniform test
+            // (a tile bit or warp bit) share one branch
+            const std::string ut0 = uniform_test(op);
+            int e3 = o + 1;
+            if (group_uniform && !p.combine && !ut0.empty()) {
+                auto loop_start = [&](int i) {
+                    const FOp &x = p.ops[i];
+                    if (!(tile_loop > 0 && x.variant >= kPhaseVariant && x.ext_need && !x.tid_need)) return false;
+                    int k = i;
+                    while (k < st.op_end && k - i < tile_loop && p.ops[k].variant >= kPhaseVariant &&
+                           p.ops[k].ext_need && !p.ops[k].tid_need && p.ops[k].reg_need == x.reg_need &&
+                           p.ops[k].half_need == x.half_need)
+                        ++k;
+                    return k - i >= tile_loop;
+                };
+                while (e3 < st.op_end && uniform_test(p.ops[e3]) == ut0 && !loop_start(e3)) ++e3;
+            }
+            if (e3 - o >= 2) {
+                src += "      if (" + ut0 + ") {\n";
+                for (; o < e3; ++o) src += emit_one(p.ops[o], true);
+                src += "      }\n";
+            } else {
+                src += emit_one(op, false);
+                ++o;
             }
         }
         src += "    } break;\n";
