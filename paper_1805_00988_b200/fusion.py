@@ -180,8 +180,90 @@ def _plan_reorder(num_qubits: int, ops, tile_qubits: int | None) -> list[Pass]:
         qs = [q for q in range(n) if (tile >> q) & 1]
         extra = [q for q in range(n - 1, -1, -1) if not (tile >> q) & 1]
         qs.extend(extra[: max(0, K - len(qs))])
-        passes.append(Pass(sorted(qs), [ops[j] for j in taken]))
+        qs.sort()
+        passes.append(Pass(qs, _order_for_stages([ops[j] for j in taken], qs)))
     return passes
+
+
+def _order_for_stages(pops, tile) -> list:
+    """Reorder a reordered pass's ops (DAG order kept: ops sharing a qubit
+    stay in order) so that the kernel's stage planner (csrc/fused.cu
+    plan_pass: a stage holds its pair targets in RB register bits and
+    leaves one of the f-bit triples {0,1,2} / {5,6,7} to the lanes) needs as
+    few stages as possible: every stage is a shared-memory round trip of
+    the whole tile (~3 ms per extra stage at 32 qubits).  Greedy: absorb
+    every ready op whose target bit is in the current register set; grow the
+    set by the bit that unlocks the most ops; else start a new stage."""
+    m = len(pops)
+    if m < 3:
+        return pops
+    local = {q: i for i, q in enumerate(tile)}
+    nphase = sum(1 for op in pops if op[0] != N.QS_OP_PAIR)
+    RB = 3 if 2 * nphase > m else 4
+
+    def fbit(op):
+        kind, t = op[0], op[1]
+        if kind != N.QS_OP_PAIR:
+            return None
+        lb = local.get(t)
+        return None if lb is None or lb == 0 else lb - 1
+
+    def triple_ok(rs):
+        return not (rs & {0, 1, 2}) or (len(tile) - 1 > 7 and not (rs & {5, 6, 7}))
+
+    masks = [_qubits(op) for op in pops]
+    preds = [0] * m
+    succ = [[] for _ in range(m)]
+    last = {}
+    for j, mk in enumerate(masks):
+        ps = set()
+        q = mk
+        while q:
+            b = q & -q
+            if b in last:
+                ps.add(last[b])
+            last[b] = j
+            q ^= b
+        preds[j] = len(ps)
+        for i in ps:
+            succ[i].append(j)
+    fb = [fbit(op) for op in pops]
+    ready = {j for j in range(m) if preds[j] == 0}
+    out: list = []
+
+    def absorb(regs, rd, pc, sim):
+        stack = [j for j in rd if fb[j] is None or fb[j] in regs]
+        got = 0
+        while stack:
+            j = stack.pop()
+            if j not in rd:
+                continue
+            rd.discard(j)
+            got += 1
+            if not sim:
+                out.append(j)
+            for k in succ[j]:
+                pc[k] -= 1
+                if pc[k] == 0:
+                    rd.add(k)
+                    if fb[k] is None or fb[k] in regs:
+                        stack.append(k)
+        return got
+
+    regs: set = set()
+    while len(out) < m:
+        absorb(regs, ready, preds, False)
+        if len(out) == m:
+            break
+        cands = {fb[j] for j in ready if fb[j] is not None and fb[j] not in regs}
+        cands = [f for f in cands if len(regs) < RB and triple_ok(regs | {f})]
+        if not cands:
+            regs = set()  # next stage
+            continue
+        best = max(sorted(cands), key=lambda f: absorb(regs | {f}, set(ready), list(preds), True))
+        regs = regs | {best}
+    # keep circuit order inside each maximal run the greedy emitted (cosmetic)
+    return [pops[j] for j in out]
 
 
 def is_permutation(m: np.ndarray) -> bool:
