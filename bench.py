@@ -460,7 +460,8 @@ def run_sharded(args):
         extras["global_gates"] = run_global_gate_probe(n, local, world)
         try:
             eng.state.close()  # the weak-scaling register is done: room for the 34-qubit one
-            extras["strong34"] = measure_strong(34, world, local, 1, 1)
+            extras["strong34"] = measure_strong(int(os.environ.get("QSB_BENCH_STRONG_QUBITS", "34")), world, local,
+                                                1, 1)
         except Exception as exc:  # noqa: BLE001
             extras["strong34"] = {"error": f"{type(exc).__name__}: {exc}"}
     if not args.no_extras:
@@ -502,8 +503,12 @@ def init_dist() -> int:
     _, _, local = _dist_env()
     local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only with QSB_BENCH_SHARE_GPU
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local),
-                            timeout=datetime.timedelta(minutes=10))
+    backend = os.environ.get("QSB_BENCH_BACKEND", "nccl")  # gloo: test runs with ranks sharing one GPU
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(minutes=10))
+    else:
+        dist.init_process_group(backend, timeout=datetime.timedelta(minutes=10))
     return local
 
 
@@ -653,7 +658,9 @@ def run_single_process(n, world, rank):
             out = {"n_qubits": n, "devices": world}
             for label, exch, peer in (("nccl_swaps", "nccl", False), ("p2p_swaps", "p2p", False),
                                       ("peer_gates", "p2p", True)):
-                md = MultiDeviceState(n, list(range(world)))
+                import torch
+
+                md = MultiDeviceState(n, [r % torch.cuda.device_count() for r in range(world)])
                 try:
                     md.set_mode(peer_gates=peer, exchange=exch)
                 except Exception as exc:  # noqa: BLE001  (e.g. no NCCL communicators)
@@ -1181,7 +1188,7 @@ def main():
         # `python bench.py --gpus N` without a launcher: start N ranks (one
         # process per GPU) under torch.distributed.run ourselves
         have = _visible_gpus()
-        if have < args.gpus:
+        if have < args.gpus and os.environ.get("QSB_BENCH_SHARE_GPU") != "1":
             sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} GPU(s) are visible\n")
             sys.exit(2)
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
