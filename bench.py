@@ -702,7 +702,7 @@ def run_global_gate_probe(n, local, world, reps=3):
 
     g = int(round(math.log2(world)))
     out = {"n_qubits": n, "global_qubits": g}
-    for name, peer in (("swap_nccl", False), ("peer_nvlink", True)):
+    for name, peer in (("swap_nccl", False), ("peer_nvlink", True), ("auto_calibrated", "auto")):
         try:
             st = ShardedState.distributed(n, device=local, peer_gates=peer)
             best = float("inf")
@@ -723,7 +723,7 @@ def run_global_gate_probe(n, local, world, reps=3):
             out[name] = {"ms_per_global_gate": float(t.item()) * 1e3 / g,
                          "swaps_per_rep": st.swaps // (reps + 1),
                          "peer_gates_per_rep": st.peer_gate_count // (reps + 1),
-                         "peer_mode_active": st.peer_gates}
+                         "peer_mode_active": st.peer_gates, "calibration": st.calibration}
             del st
         except Exception as exc:  # noqa: BLE001
             out[name] = {"error": f"{type(exc).__name__}: {exc}"}

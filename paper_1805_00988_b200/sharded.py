@@ -414,9 +414,14 @@ class ShardedState:
         if peer_gates is None:
             import os
 
-            peer_gates = os.environ.get("QSB_SHARD_PEER", "0") == "1"
+            env = os.environ.get("QSB_SHARD_PEER", "0")
+            peer_gates = "auto" if env == "auto" else env == "1"
         can_peer = g > 0 and all(hasattr(e, "peer_gate") for e in self.engines)
-        self.peer_gates = bool(peer_gates) and can_peer
+        # "auto": decided at the first global-target pair gate by timing both
+        # paths on the live register (calibrate_global_gates)
+        self._auto_peer = peer_gates == "auto" and can_peer
+        self.peer_gates = (peer_gates is True or self._auto_peer) and can_peer
+        self.calibration = None
         # Qubit-swap data movement: "nccl" (transport send/recv; in-process
         # copies for virtual shards) or "peer" (qs_swap_peer: one kernel per
         # partner over mapped peer memory, no staging).  Default: "peer" when
@@ -536,6 +541,58 @@ class ShardedState:
                 self.exchange = "nccl"
         return bool(self._peers)
 
+    def _global_pair_via_peer(self, rank_bit: int) -> bool:
+        """Should a pair gate on global rank bit `rank_bit` run as a peer gate?"""
+        if not (self.peer_gates and self._peer_ready()):
+            return False
+        if self._auto_peer and self.calibration is None:
+            self.calibrate_global_gates(rank_bit)
+        return self.peer_gates
+
+    def calibrate_global_gates(self, rank_bit: int, reps: int = 1) -> dict:
+        """Time both ways of a global-target pair gate on the live register and
+        keep the faster (all ranks agree: max over ranks): a peer gate (one
+        kernel over NVLink) vs a qubit swap + local sweep.  Uses X twice per
+        path — an exact permutation, so the register's bits are unchanged
+        and the qubit map is restored."""
+        import time
+
+        from .gates import FIXED_GATES
+
+        X = m8(FIXED_GATES["x"])
+        L = self.L
+
+        def timed(fn):
+            self.transport.peer_barrier(self.engines)
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                fn()
+                fn()
+            self.transport.peer_barrier(self.engines)
+            return (time.perf_counter() - t0) / (2 * reps)
+
+        def peer_once():
+            self._peer_gate(rank_bit, 0, 0, X)
+            self.peer_gate_count -= 1
+
+        def swap_once():  # (exchange + sweep) twice: X X on the swapped-in qubit, then swap back
+            self._exchange(rank_bit)
+            for _ in range(2):
+                for eng in self.engines:
+                    eng.apply(N.QS_OP_PAIR, L - 1, 0, X)
+            self._exchange(rank_bit)
+
+        counters = (self.peer_swaps,)
+        t_peer = timed(peer_once)
+        t_swap = timed(swap_once) / 2  # one call = two (exchange + sweep)
+        (self.peer_swaps,) = counters
+        t = self.transport.combine_max([np.array([t_peer, t_swap])])
+        t_peer, t_swap = float(t[0]), float(t[1])
+        self.peer_gates = t_peer <= t_swap
+        self.calibration = {"peer_gate_ms": t_peer * 1e3, "swap_and_sweep_ms": t_swap * 1e3,
+                            "chosen": "peer" if self.peer_gates else "swap"}
+        return self.calibration
+
     def _shard_phase(self, rank_bits, m: np.ndarray) -> None:
         """A diagonal gate whose bits are all global: every amplitude of the
         shards whose rank bits are all 1 is multiplied by d — no exchange.
@@ -586,7 +643,7 @@ class ShardedState:
         if kind == N.QS_OP_PHASE and not any(lay.is_local(q) for q in qs):
             self._shard_phase([lay.pos[q] - lay.L for q in qs], m)
             return self
-        if kind == N.QS_OP_PAIR and not lay.is_local(target) and self.peer_gates and self._peer_ready():
+        if kind == N.QS_OP_PAIR and not lay.is_local(target) and self._global_pair_via_peer(lay.pos[target] - lay.L):
             cmask, need = self._control_masks(controls)
             self._peer_gate(lay.pos[target] - lay.L, cmask, need, m)
             return self
@@ -673,7 +730,7 @@ class ShardedState:
                 continue
             if not lay.is_local(target):
                 flush()
-                if kind == N.QS_OP_PAIR and self.peer_gates and self._peer_ready():
+                if kind == N.QS_OP_PAIR and self._global_pair_via_peer(lay.pos[target] - lay.L):
                     cmask, need = self._control_masks(controls)
                     self._peer_gate(lay.pos[target] - lay.L, cmask, need, m)
                     continue

@@ -302,3 +302,16 @@ def test_all_global_diagonal_gates_need_no_exchange():
                     st.apply_controlled_gate(i.gate, i.control, i.target)
         assert st.shard_phases == 3 and st.swaps == 0
         assert same_values(st.amplitudes(), oracle_run(circ, basis))
+
+
+def test_auto_global_gate_mode_calibrates_and_keeps_bits():
+    """peer_gates="auto": the first global-target pair gate times a peer gate
+    against swap + sweep (X twice each: the register's bits and the qubit map
+    are unchanged) and keeps the faster; results stay bit-exact."""
+    n, shards = 8, 4
+    circ = mixed_circuit(n, 80, 77)
+    st = ShardedState.virtual(n, shards, engine_factory=OracleEngine, peer_gates="auto")
+    st.run(circ)
+    assert st.calibration is not None and st.calibration["chosen"] in ("peer", "swap")
+    assert st.calibration["peer_gate_ms"] > 0 and st.calibration["swap_and_sweep_ms"] > 0
+    assert same_values(st.amplitudes(), oracle_run(circ))
