@@ -828,6 +828,7 @@ def run_extras(st, stream, n, cpu=True, harness=True):
         cold = []
         ms = timed(state, strm, passes, reps=reps, combine=not exact, cold=cold)
         return {"gates": circ.gate_count(), "passes": len(passes), "ms": ms, "cold_first_run_ms": cold[0],
+                "jit_programs_so_far": fusion.jit_stats(),
                 "effective_gates_per_s": circ.gate_count() / (ms / 1e3),
                 "pass_bytes": len(passes) * 16 * (1 << nq),
                 "achieved_GBps": len(passes) * 16 * (1 << nq) / (ms / 1e3) / 1e9,

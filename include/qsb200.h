@@ -161,6 +161,10 @@ int qs_apply_fused_f64(qs_state *s, const int32_t *tile_qubits, int ntile,
  * interpreter kernel, with the same bits.  Wait for every queued compile and
  * load the programs of `device` (< 0: all).  Not needed for correctness. */
 int qs_jit_sync(int device);
+/* Pass programs this process compiled with NVRTC, loaded from the on-disk
+ * program cache (QSB_JIT_CACHE_DIR / ~/.cache/qsb200-jit; QSB_JIT_CACHE=0
+ * disables it), and failed to build. */
+int qs_jit_stats(uint64_t *compiled, uint64_t *cache_hits, uint64_t *failed);
 /* Drop queued compiles, let an in-flight one finish and stop the compile
  * threads (call before process teardown; the Python layer registers it with
  * atexit).  Later fused passes run on the interpreter kernel. */

@@ -35,7 +35,7 @@ EXPORTS = (
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
-    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_swap_peer", "qs_jit_sync",
+    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_swap_peer", "qs_jit_sync", "qs_jit_stats",
     "qs_jit_shutdown", "qs_begin_capture", "qs_end_capture", "qs_graph_launch", "qs_graph_destroy",
     "qs_create_sharded", "qs_sharded_destroy", "qs_sharded_info", "qs_sharded_shard", "qs_sharded_set_mode",
     "qs_sharded_stats", "qs_sharded_reset", "qs_sharded_apply_gate", "qs_sharded_apply_controlled_gate",
@@ -136,6 +136,7 @@ def _declare(L):
         "qs_sharded_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sharded_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),
         "qs_jit_sync": ([i32], i32),
+        "qs_jit_stats": ([ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)], i32),
         "qs_jit_shutdown": ([], i32),
         "qs_begin_capture": ([vp], i32),
         "qs_end_capture": ([vp, ctypes.POINTER(vp)], i32),

@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -646,12 +647,22 @@ std::string cache_key(const std::string &src) {
     return src + tag;
 }
 
+std::atomic<unsigned long long> g_compiled{0}, g_cache_hits{0}, g_compile_failed{0};
+
 bool compile_cubin(Job &job) {
     const std::string key = cache_key(job.src);
     const std::string cpath = cache_path(key);
-    if (cache_load(cpath, key, job.cubin)) return true;
+    if (cache_load(cpath, key, job.cubin)) {
+        ++g_cache_hits;
+        return true;
+    }
     const bool ok = compile_nvrtc(job);
-    if (ok) cache_store(cpath, key, job.cubin);
+    if (ok) {
+        ++g_compiled;
+        cache_store(cpath, key, job.cubin);
+    } else {
+        ++g_compile_failed;
+    }
     return ok;
 }
 
@@ -861,6 +872,13 @@ extern "C" int qs_jit_sync(int device) {
     const int failed = qsb::jit_sync(device);
     return failed ? qsb::set_error(QS_ERR_CUDA, std::to_string(failed) + " pass program(s) failed to compile")
                   : QS_OK;
+}
+
+extern "C" int qs_jit_stats(uint64_t *compiled, uint64_t *cache_hits, uint64_t *failed) {
+    if (compiled) *compiled = qsb::g_compiled.load();
+    if (cache_hits) *cache_hits = qsb::g_cache_hits.load();
+    if (failed) *failed = qsb::g_compile_failed.load();
+    return QS_OK;
 }
 
 extern "C" int qs_jit_shutdown(void) {

@@ -338,6 +338,16 @@ def jit_sync(device: int = -1) -> None:
     N.check(N.lib().qs_jit_sync(int(device)))
 
 
+def jit_stats() -> dict:
+    """{"compiled", "cache_hits", "failed"}: pass programs built with NVRTC by
+    this process, loaded from the on-disk program cache, failed."""
+    import ctypes
+
+    c, h, f = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    N.check(N.lib().qs_jit_stats(ctypes.byref(c), ctypes.byref(h), ctypes.byref(f)))
+    return {"compiled": c.value, "cache_hits": h.value, "failed": f.value}
+
+
 def run(state, passes: list[Pass], combine: bool = False) -> None:
     """Launch the planned passes on a State (asynchronous on its stream).
     combine=True: runs of unit-modulus diagonal ops as one product per

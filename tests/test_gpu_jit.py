@@ -142,3 +142,34 @@ def test_background_compile_policy():
         for _ in range(3):
             execute(circ, ref, fuse=True)
         assert same_values(got, ref.amplitudes())
+
+
+def test_program_disk_cache_across_processes(tmp_path):
+    """A second process running the same fused circuit loads the compiled
+    pass programs from the on-disk cache (no NVRTC), with the same bits."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    child = (
+        "import sys, json, numpy as np\n"
+        f"sys.path.insert(0, {str(root)!r})\n"
+        "from paper_1805_00988_b200 import State, build_qft, fusion\n"
+        "from paper_1805_00988_b200.circuits import lower_ops\n"
+        "st = State(16)\n"
+        "for q in range(16): st.h(q)\n"
+        "fusion.run(st, fusion.plan(16, lower_ops(build_qft(16)), 11))\n"
+        "a = st.amplitudes()\n"
+        "print(json.dumps({**fusion.jit_stats(), 'digest': a.tobytes().hex()[:64] + str(float(np.abs(a).sum()))}))\n")
+    env = dict(__import__("os").environ, QSB_JIT_CACHE_DIR=str(tmp_path), QSB_FUSED_JIT="2")
+    outs = []
+    for _ in range(2):
+        r = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0]["compiled"] >= 1 and outs[0]["cache_hits"] == 0
+    assert outs[1]["compiled"] == 0 and outs[1]["cache_hits"] == outs[0]["compiled"]
+    assert outs[0]["digest"] == outs[1]["digest"]
+    assert any(p.suffix == ".bin" for p in tmp_path.iterdir())

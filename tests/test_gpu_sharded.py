@@ -69,3 +69,15 @@ def test_peer_gates_equal_unsharded(n, shards):
     st.run(circ)
     assert st.peer_gate_count > 0
     assert same_values(st.amplitudes(), ref.amplitudes())
+
+
+def test_auto_global_gate_mode_equals_unsharded():
+    n = 16
+    circ = Circuit(n, build_hadamard_layer(n).instructions + mixed_circuit(n, 100, 5).instructions)
+    ref = State(n)
+    execute(circ, ref, fuse=False)
+    st = ShardedState.virtual(n, 4, peer_gates="auto")
+    st.run(circ)
+    assert st.calibration is not None
+    assert same_values(st.amplitudes(), ref.amplitudes())
+    st.close()
