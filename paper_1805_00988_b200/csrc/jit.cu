@@ -36,6 +36,7 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -188,7 +189,7 @@ bool unit_turns(const FOp &op, uint32_t *turns) {
     return true;
 }
 
-std::string generate(const FParams &p, int K, int RB) {
+std::string generate(const FParams &p, int K, int RB, bool param = false) {
     // diagonal ops inside a test: 1 (default) scalar phase_cs, 0 packed
     // phase_ct, 2 scalar everywhere (QSB_JIT_PHASE, for measurements)
     int phase_mode = 1;
@@ -237,7 +238,18 @@ std::string generate(const FParams &p, int K, int RB) {
     if (const char *e = std::getenv("QSB_JIT_GROUP")) group_uniform = std::atoi(e);
     // One op as generated source.  grouped: the caller has already branched
     // on the op's warp-uniform test; only the lane part remains.
-    auto emit_one = [&](const FOp &op, bool grouped) -> std::string {
+    // a gate entry: a literal of the generated source, or (parametric
+    // programs) a load from the op table staged in shared memory, so a
+    // circuit of the same structure with other angles reuses the program
+    auto ent = [&](std::string &out, int oi, int i) {
+        if (param) {
+            out += "ops[" + std::to_string(oi) + "].m[" + std::to_string(i) + "]";
+        } else {
+            hexf(out, p.ops[oi].m[i]);
+        }
+    };
+    auto emit_one = [&](int oi, bool grouped) -> std::string {
+        const FOp &op = p.ops[oi];
         std::string out;
         char b[256];
         const std::string utest = grouped ? std::string() : uniform_test(op), ltest = lane_test(op);
@@ -256,9 +268,9 @@ std::string generate(const FParams &p, int K, int RB) {
                               planar ? (in_branch ? "pphase_sel_cs" : "pphase_sel") : "phase_sel", R,
                               odd ? "true" : "false", ltest.c_str());
                 out += b;
-                hexf(out, op.m[6]);
+                ent(out, oi, 6);
                 out += ", ";
-                hexf(out, op.m[7]);
+                ent(out, oi, 7);
                 out += "), v); }\n";
             } else {
                 const int slot = (op.variant / 2) / 4 - 1;
@@ -277,16 +289,16 @@ std::string generate(const FParams &p, int K, int RB) {
                                  : (scalar ? "phase_cs" : "phase_ct"),
                           R, odd ? "true" : "false");
             out += b;
-            hexf(out, op.m[6]);
+            ent(out, oi, 6);
             out += ", ";
-            hexf(out, op.m[7]);
+            ent(out, oi, 7);
             out += "), v); }\n";
         } else {
             const int slot = (op.variant / 2) / 4 - 1;
             out += " const float m[8] = {";
             for (int i = 0; i < 8; ++i) {
                 if (i) out += ", ";
-                hexf(out, op.m[i]);
+                ent(out, oi, i);
             }
             std::snprintf(b, sizeof b, "}; %s<%d, %d, %u, %s, RB>(m, one, v); }\n", planar ? "ppair" : "pair_ct", slot,
                           cls, op.reg_need, op.half_need ? "true" : "false");
@@ -363,6 +375,21 @@ std::string generate(const FParams &p, int K, int RB) {
                 int e2 = o;
                 while (e2 < st.op_end && e2 - o < 32 && tile_only(p.ops[e2])) ++e2;
                 const int len = e2 - o;
+                if (len >= tile_loop && param) {  // entries from the op table
+                    src += "      { uint32_t m = 0u;";
+                    for (int i = 0; i < len; ++i) {
+                        const unsigned long long E = p.ops[o + i].ext_need;
+                        std::snprintf(buf, sizeof buf, " m |= (uint32_t)((ub & 0x%llxull) == 0x%llxull) << %d;", E, E, i);
+                        src += buf;
+                    }
+                    std::snprintf(buf, sizeof buf,
+                                  "\n        while (m) { const int i = __ffs(m) - 1; m &= m - 1u;"
+                                  " %s<%d, %s, RB>(make_float2(ops[%d + i].m[6], ops[%d + i].m[7]), v); } }\n",
+                                  planar ? "pphase" : "phase_cs", (int)op.reg_need, op.half_need ? "true" : "false", o, o);
+                    src += buf;
+                    o = e2;
+                    continue;
+                }
                 if (len >= tile_loop) {
                     const int id = nconst++;
                     std::snprintf(buf, sizeof buf, "__constant__ unsigned kT%d[%d] = {", id, 2 * len);
@@ -447,10 +474,10 @@ std::string generate(const FParams &p, int K, int RB) {
             }
             if (e3 - o >= 2) {
                 src += "      if (" + ut0 + ") {\n";
-                for (; o < e3; ++o) src += emit_one(p.ops[o], true);
+                for (; o < e3; ++o) src += emit_one(o, true);
                 src += "      }\n";
             } else {
-                src += emit_one(op, false);
+                src += emit_one(o, false);
                 ++o;
             }
         }
@@ -782,9 +809,52 @@ int jit_rb(int dflt) {
 // The compiled program for one planned launch group, or nullptr while it is
 // still compiling (the compile is queued on first request) or if it cannot be
 // built.  wait = true blocks until the compile has finished (policy 2).
+// Parametric programs (QSB_JIT_PARAMETRIC: 1 = auto, the default; 2 =
+// always; 0 = never).  A literal program bakes the gate entries in (fastest:
+// immediate operands); a parametric one reads them from the op table, so
+// every circuit of the same STRUCTURE (op kinds, slots, classes, masks) runs
+// it — a variational loop changing only angles compiles nothing new.  Auto:
+// once a second distinct literal program of one structure is requested, that
+// structure switches to its parametric program.
+std::map<Key, std::set<size_t>> g_struct_lits;  // parametric key -> hashes of the literal sources seen (g_mu)
+
+int param_policy() {
+    const char *e = std::getenv("QSB_JIT_PARAMETRIC");
+    return e && *e ? std::atoi(e) : 1;
+}
+
+// The key to run for this launch group: the literal program, or the
+// parametric one of its structure (g_mu held).
+Key choose_key(int device, const FParams &p, int K, int RB, bool *is_param) {
+    *is_param = false;
+    Key lit(device, generate(p, K, RB, false));
+    const int pol = param_policy();
+    if (pol == 0 || p.combine) return lit;
+    if (g_fns.count(lit) && pol == 1) return lit;
+    Key par(device, generate(p, K, RB, true));
+    if (pol == 2 || g_fns.count(par)) {
+        *is_param = true;
+        return par;
+    }
+    std::set<size_t> &seen = g_struct_lits[par];
+    seen.insert(std::hash<std::string>()(lit.second));
+    if (seen.size() >= 2) {
+        *is_param = true;
+        return par;
+    }
+    return lit;
+}
+
 void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool wait,
               const qs_op64 *ops64) {
-    Key key(device, ops64 ? generate_d(p, K, RB, ops64) : generate(p, K, RB));
+    Key key;
+    if (ops64) {
+        key = Key(device, generate_d(p, K, RB, ops64));
+    } else {
+        std::lock_guard<std::mutex> lock(g_mu);
+        bool is_param = false;
+        key = choose_key(device, p, K, RB, &is_param);
+    }
     if (const char *dir = std::getenv("QSB_FUSED_JIT_DUMP")) {  // tooling: keep the generated sources
         static int count = 0;
         const std::string path = std::string(dir) + "/qsb_pass_" + std::to_string(count++) + ".cu";
@@ -823,10 +893,18 @@ void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool
 // An already loaded program, without queueing or loading anything (used while
 // the stream is being recorded into a CUDA graph).
 void *jit_lookup(int device, const FParams &p, int K, int RB, const qs_op64 *ops64) {
-    Key key(device, ops64 ? generate_d(p, K, RB, ops64) : generate(p, K, RB));
     std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_fns.find(key);
-    return it == g_fns.end() ? nullptr : (void *)it->second;
+    if (ops64) {
+        auto it = g_fns.find(Key(device, generate_d(p, K, RB, ops64)));
+        return it == g_fns.end() ? nullptr : (void *)it->second;
+    }
+    auto it = g_fns.find(Key(device, generate(p, K, RB, false)));
+    if (it != g_fns.end()) return (void *)it->second;
+    if (param_policy() != 0 && !p.combine) {
+        it = g_fns.find(Key(device, generate(p, K, RB, true)));
+        if (it != g_fns.end()) return (void *)it->second;
+    }
+    return nullptr;
 }
 
 // Wait for every queued compile and load the programs of `device` (< 0: the

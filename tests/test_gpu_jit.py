@@ -173,3 +173,45 @@ def test_program_disk_cache_across_processes(tmp_path):
     assert outs[1]["compiled"] == 0 and outs[1]["cache_hits"] == outs[0]["compiled"]
     assert outs[0]["digest"] == outs[1]["digest"]
     assert any(p.suffix == ".bin" for p in tmp_path.iterdir())
+
+
+def test_parametric_programs_reuse_structure(tmp_path):
+    """Circuits with the same structure and other angles (a variational loop):
+    the second distinct literal program of a structure switches it to its
+    parametric program (entries read from the op table), and every later
+    circuit of that structure compiles nothing.  Bits equal the sweeps."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    child = (
+        "import sys, json, math, numpy as np\n"
+        f"sys.path.insert(0, {str(root)!r})\n"
+        "from paper_1805_00988_b200 import State, fusion, u1, execute\n"
+        "from paper_1805_00988_b200.circuits import Apply, ControlledApply, Circuit, lower_ops\n"
+        "from paper_1805_00988_b200.gates import H\n"
+        "n = 16\n"
+        "def circ(th):\n"
+        "    ins = [Apply(H, q) for q in range(n)]\n"
+        "    ins += [ControlledApply(u1(th * (j + 1) / (k + 2)), j, k) for j in range(n) for k in range(j)]\n"
+        "    ins += [Apply(H, q) for q in range(n)]\n"
+        "    return Circuit(n, tuple(ins))\n"
+        "out = []\n"
+        "for th in (0.3, 0.7, 1.1, 1.9):\n"
+        "    before = fusion.jit_stats()['compiled']\n"
+        "    a, b = State(n), State(n)\n"
+        "    c = circ(th)\n"
+        "    fusion.run(a, fusion.plan(n, lower_ops(c), 11))\n"
+        "    execute(c, b, fuse=False)\n"
+        "    out.append({'new': fusion.jit_stats()['compiled'] - before,\n"
+        "                'same': bool(np.all(a.amplitudes() == b.amplitudes()))})\n"
+        "print(json.dumps(out))\n")
+    env = dict(__import__("os").environ, QSB_JIT_CACHE="0", QSB_FUSED_JIT="2")
+    r = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(o["same"] for o in out)
+    assert out[0]["new"] >= 1 and out[1]["new"] >= 1  # literal, then the parametric programs
+    assert out[2]["new"] == 0 and out[3]["new"] == 0
