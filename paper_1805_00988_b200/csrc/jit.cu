@@ -874,9 +874,17 @@ void *jit_get(int device, const FParams &p, int K, int RB, size_t smem_max, bool
         job->device = device;
         job->src = key.second;
         job->smem_max = smem_max;
-        ensure_workers();
-        g_queue.push_back(job);
-        g_cv.notify_all();
+        // a program in the on-disk cache is loaded right away (a file read),
+        // so even the first launch of a known pass runs compiled
+        const std::string ck = cache_key(job->src);
+        if (cache_load(cache_path(ck), ck, job->cubin)) {
+            ++g_cache_hits;
+            job->state = 1;
+        } else {
+            ensure_workers();
+            g_queue.push_back(job);
+            g_cv.notify_all();
+        }
     }
     std::shared_ptr<Job> j = job;
     if (wait) g_cv.wait(lock, [&] { return j->state != 0; });
