@@ -117,6 +117,62 @@ def _device() -> int:
     return int(os.environ.get("QSB_DEVICE", "0"))
 
 
+class _Mirror(np.ndarray):
+    """Host copy of a register handed out as `StateVector.amps`.  Every write
+    through it — item / slice assignment, in-place operators and ufuncs with
+    `out=`, ndarray's mutating methods, np.copyto / np.put / np.place /
+    np.putmask — marks it dirty (views share the flag), so the next device
+    operation uploads it; an untouched mirror is not re-uploaded."""
+
+    _MUTATORS = ("fill", "put", "sort", "partition", "resize", "setfield", "byteswap")
+
+    def __array_finalize__(self, obj):
+        self._flag = getattr(obj, "_flag", None)
+
+    def _touch(self):
+        if self._flag is not None:
+            self._flag[0] = True
+
+    def __setitem__(self, key, value):
+        self._touch()
+        super().__setitem__(key, value)
+
+    def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kwargs):
+        plain = tuple(np.asarray(x) if isinstance(x, _Mirror) else x for x in inputs)
+        if out is not None:
+            for o in out:
+                if isinstance(o, _Mirror):
+                    o._touch()
+            kwargs["out"] = tuple(np.asarray(o) if isinstance(o, _Mirror) else o for o in out)
+        res = getattr(ufunc, method)(*plain, **kwargs)
+        if out is not None and len(out) == 1 and isinstance(out[0], _Mirror):
+            return out[0]  # in-place operators keep the tracked object
+        return res
+
+    def __array_function__(self, func, types, args, kwargs):
+        if func in (np.copyto, np.put, np.place, np.putmask, np.fill_diagonal) and args and \
+                isinstance(args[0], _Mirror):
+            args[0]._touch()
+        return super().__array_function__(func, types, args, kwargs)
+
+    def __reduce__(self):  # pickles as a plain array
+        return np.asarray(self).__reduce__()
+
+
+def _mutator(name):
+    def method(self, *a, **k):
+        if name != "byteswap" or k.get("inplace") or (a and a[0]):
+            self._touch()
+        return getattr(np.ndarray, name)(self, *a, **k)
+
+    method.__name__ = name
+    return method
+
+
+for _name in _Mirror._MUTATORS:
+    setattr(_Mirror, _name, _mutator(_name))
+
+
 class StateVector:
     """Register handle (state.py:45-68) whose amplitudes live in HBM."""
 
@@ -125,6 +181,8 @@ class StateVector:
             raise ValueError("num_qubits must be >= 1")
         self.num_qubits = int(num_qubits)
         self._mirror: np.ndarray | None = None
+        self._dirty = [False]  # the handed-out mirror was written since the last sync
+        self._uploads = 0  # host -> device re-uploads of a written mirror (diagnostics)
         if _dev is not None:
             self._dev = _dev
             return
@@ -152,7 +210,10 @@ class StateVector:
     @property
     def amps(self) -> np.ndarray:
         if self._mirror is None:
-            self._mirror = self._dev.amplitudes()
+            m = self._dev.amplitudes().view(_Mirror)
+            m._flag = self._dirty
+            self._dirty[0] = False
+            self._mirror = m
         return self._mirror
 
     @amps.setter
@@ -160,18 +221,29 @@ class StateVector:
         arr = np.asarray(value)
         if arr.shape != (self.dim,) or arr.dtype != self._dev.dtype:
             raise ValueError(f"amps must be a {self._dev.dtype} array of length 2^n")
-        self._mirror = arr
+        if isinstance(value, _Mirror) and value._flag is self._dirty:
+            self._mirror = value  # `state.amps op= x` hands the tracked mirror back
+        else:
+            self._mirror = arr  # a caller's plain array: untracked, so always treated as written
         self._dev.set_amplitudes(arr)
+        self._dirty[0] = False
 
-    # device-op bracket: keep a handed-out mirror coherent
+    def _host_written(self) -> bool:
+        return not isinstance(self._mirror, _Mirror) or self._dirty[0]
+
+    # device-op bracket: keep a handed-out mirror coherent (upload only what
+    # the host wrote; download the result into the same array object)
     def _before(self) -> State:
-        if self._mirror is not None:
-            self._dev.set_amplitudes(self._mirror)
+        if self._mirror is not None and self._host_written():
+            self._dev.set_amplitudes(np.asarray(self._mirror))
+            self._dirty[0] = False
+            self._uploads += 1
         return self._dev
 
     def _after(self) -> None:
         if self._mirror is not None:
-            self._mirror[:] = self._dev.amplitudes()
+            np.asarray(self._mirror)[:] = self._dev.amplitudes()
+            self._dirty[0] = False
 
 
 def new_state(num_qubits: int, precision: Precision = Precision.SINGLE, memory_budget: int | None = None) -> StateVector:

@@ -280,3 +280,45 @@ class TestCircuits:  # pkg/tests/test_circuits.py
             else:
                 dev.apply_gate(g, t)
         assert abs(ps.norm_squared(st) - 1.0) < 1e-3
+
+
+class TestMirrorTracking:
+    """A handed-out `amps` is re-uploaded only after the host wrote to it."""
+
+    def test_reads_do_not_force_uploads(self):
+        st = ps.new_state(8)
+        ps.apply_gate(st, 0, ps.H)
+        a = st.amps  # handed out
+        for t in range(1, 8):
+            ps.apply_gate(st, t, ps.H)
+        assert st._uploads == 0 and a is st.amps
+        assert np.allclose(a, np.full(256, 1 / 16, np.complex64), atol=1e-6)
+        _ = float(np.abs(a).sum()), a.tobytes(), a.copy()
+        ps.apply_gate(st, 3, ps.H)
+        assert st._uploads == 0
+
+    @pytest.mark.parametrize("write", ["setitem", "slice_view", "inplace", "copyto", "fill", "real"])
+    def test_every_write_path_reaches_the_device(self, write):
+        st = ps.new_state(5)
+        a = st.amps
+        if write == "setitem":
+            a[3] = 1
+        elif write == "slice_view":
+            v = a[2:6]
+            v[1] = 1
+        elif write == "inplace":
+            a += np.eye(1, 32, 3, dtype=np.complex64)[0]
+        elif write == "copyto":
+            np.copyto(a, np.eye(1, 32, 3, dtype=np.complex64)[0])
+        elif write == "fill":
+            a.fill(0)
+            a[3] = 1
+        else:
+            a.real[3] = 1
+        if write != "copyto" and write != "fill":
+            a[0] = 0
+        ps.apply_gate(st, 1, ps.X)
+        assert st._uploads == 1
+        expect = np.zeros(32, np.complex64)
+        expect[3 ^ 2] = 1
+        np.testing.assert_array_equal(st.amps, expect)
