@@ -593,7 +593,15 @@ def measure_strong(n: int, world: int, local: int, steps: int, warmup: int) -> d
     st.reset(0)
     t_fused = timed(lambda: st.run(hl), 1)
     t_qft = timed(lambda: st.run(qft), 1)
-    vals = [t_layer, t_fused, t_qft]
+    st.run(qft, exact=False)  # compiles of the inexact programs
+    fusion.jit_sync()
+    st.reset(0)
+    st.run(hl)
+    t_qft_inexact = timed(lambda: st.run(qft, exact=False), 1)
+    st.reset(0)
+    st.run(hl)
+    st.run(qft)  # the exact result again for the analytic check below
+    vals = [t_layer, t_fused, t_qft, t_qft_inexact]
     if world > 1:
         import torch.distributed as dist
 
@@ -603,7 +611,8 @@ def measure_strong(n: int, world: int, local: int, steps: int, warmup: int) -> d
     st.canonicalize()
     a0 = complex(eng.state.amplitude(0)) if st.ranks[0] == 0 else None
     out = {"n_qubits": n, "n_gpus": world, "shard_qubits": n - g, "hlayer_s": vals[0], "hlayer_fused_s": vals[1],
-           "qft_s": vals[2], "qft_gates": qft.gate_count(), "global_qubit_swaps_per_layer": swaps,
+           "qft_s": vals[2], "qft_inexact_s": vals[3], "qft_gates": qft.gate_count(),
+           "global_qubit_swaps_per_layer": swaps,
            "timing": "CUDA events on each rank's register stream, max over ranks"}
     if a0 is not None:
         out["amp0_after_hlayer_qft"] = [a0.real, a0.imag]

@@ -103,10 +103,10 @@ class CudaEngine:
 
         fusion._single(self.state, kind, target, ctrl_mask, m)
 
-    def apply_ops(self, ops) -> None:
+    def apply_ops(self, ops, exact: bool = True) -> None:
         from . import fusion
 
-        fusion.run(self.state, fusion.plan(self.num_qubits, ops))
+        fusion.run(self.state, fusion.plan(self.num_qubits, ops, reorder=not exact), combine=not exact)
 
     def swap_qubits(self, a: int, b: int) -> None:
         self.state.swap_qubits(a, b)
@@ -689,9 +689,11 @@ class ShardedState:
     def ccx(self, c1, c2, t):
         return self.apply_op(FIXED_GATES["x"], t, (c1, c2))
 
-    def run(self, circuit) -> "ShardedState":
+    def run(self, circuit, exact: bool = True) -> "ShardedState":
         """Apply a circuit: maximal runs of local ops go to each shard's fused
-        planner in one call; global targets trigger a swap in between."""
+        planner in one call; global targets trigger a swap in between.
+        exact=False: the shards' passes run in the inexact mode (reordered
+        passes, combined diagonal runs; circuits.execute)."""
         from .circuits import Apply, ControlledApply, ControlledControlledApply
 
         pending: list = []
@@ -701,7 +703,10 @@ class ShardedState:
                 for eng, r in zip(self.engines, self.ranks):
                     ops = [(k, t, cm, m) for (k, t, cm, m, need) in pending if (r & need) == need]
                     if ops:
-                        eng.apply_ops(ops)
+                        if exact:
+                            eng.apply_ops(ops)
+                        else:
+                            eng.apply_ops(ops, exact=False)
                 pending.clear()
 
         for ins in circuit.instructions:

@@ -33,7 +33,7 @@ class OracleEngine:
         else:
             raise NotImplementedError
 
-    def apply_ops(self, ops):
+    def apply_ops(self, ops, exact=True):
         for kind, t, cm, m in ops:
             self.apply(kind, t, cm, m)
 

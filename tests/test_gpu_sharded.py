@@ -81,3 +81,19 @@ def test_auto_global_gate_mode_equals_unsharded():
     assert st.calibration is not None
     assert same_values(st.amplitudes(), ref.amplitudes())
     st.close()
+
+
+def test_inexact_sharded_run_to_tolerance():
+    from paper_1805_00988_b200 import fusion
+
+    n = 18
+    circ = Circuit(n, build_hadamard_layer(n).instructions + build_qft(n).instructions)
+    ref = State(n)
+    execute(circ, ref, fuse=False)
+    st = ShardedState.virtual(n, 4)
+    st.run(circ, exact=False)
+    fusion.jit_sync()
+    st.reset(0)
+    st.run(circ, exact=False)
+    np.testing.assert_allclose(st.amplitudes(), ref.amplitudes(), rtol=1e-5, atol=1e-5 * 2.0 ** (-n / 2))
+    st.close()
