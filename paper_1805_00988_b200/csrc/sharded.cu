@@ -112,6 +112,7 @@ struct qs_sharded {
     std::vector<float2 *> staging;
     int exchange = QS_EXCHANGE_P2P;
     int peer_gates = 0;
+    bool p2p_ok = true;  // every shard's device can load / store every other's memory
     uint64_t swaps = 0, peer_gate_count = 0;
 };
 
@@ -422,6 +423,7 @@ int qs_create_sharded(int num_qubits, int nshards, const int *devs, uint64_t mem
             h->comms.clear();
         }
     }
+    h->p2p_ok = p2p;  // repeated devices are trivially peers; distinct ones need P2P access
     if (h->exchange != QS_EXCHANGE_NCCL && !p2p && nshards > 1)
         return fail(set_error(QS_ERR_CUDA, "shards cannot exchange data: no NCCL communicator and no peer access"));
     if (const char *pg = std::getenv("QSB_SHARD_PEER")) h->peer_gates = *pg == '1' && (p2p || !distinct);
@@ -468,6 +470,8 @@ int qs_sharded_set_mode(qs_sharded *h, int peer_gates, int exchange) {
     if (!h) return set_error(QS_ERR_NULL, "null qs_sharded handle");
     if (exchange == QS_EXCHANGE_NCCL && h->comms.empty())
         return set_error(QS_ERR_VALUE, "no NCCL communicators (devices repeat or libnccl missing)");
+    if ((exchange == QS_EXCHANGE_P2P || peer_gates == 1) && !h->p2p_ok)
+        return set_error(QS_ERR_VALUE, "peer-memory kernels need P2P access between every pair of devices");
     if (exchange == QS_EXCHANGE_NCCL || exchange == QS_EXCHANGE_P2P) h->exchange = exchange;
     if (peer_gates >= 0) h->peer_gates = peer_gates != 0;
     return QS_OK;
