@@ -396,7 +396,10 @@ def run_sharded(args):
         raise SystemExit("--gpus must be a power of two")
     L = args.qubits or N_QUBITS
     n = L + g
-    st = ShardedState.distributed(n, device=local)
+    # global-target gates: peer gate or NCCL qubit swap + sweep, whichever
+    # the calibration on this register measures faster (ShardedState
+    # peer_gates="auto"; the global-gate probe below times both)
+    st = ShardedState.distributed(n, device=local, peer_gates=os.environ.get("QSB_BENCH_GLOBAL", "auto"))
     eng = st.engines[0]
     stream = torch.cuda.ExternalStream(eng.state.stream(), device=torch.device("cuda", local))
 
@@ -477,6 +480,7 @@ def run_sharded(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
             "config": {"workload": "hlayer_sweep_unfused_sharded", "n_qubits": n, "shard_qubits": L,
                        "gates_per_step": n, "global_qubit_swaps_per_step": swaps,
+                       "global_gate_mode": st.calibration or ("peer" if st.peer_gates else "swap"),
                        "parallelism": f"shard{world} (top {g} qubits)",
                        "value_unit": "shard sweeps (2^%d amplitudes) per second, summed over GPUs" % L,
                        "l2": "shards (8 GiB) larger than L2; no flush needed"},

@@ -217,6 +217,11 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
     // applicable ops run in circuit order, so the bits are unchanged.
     int tile_loop = 3;
     if (const char *e = std::getenv("QSB_JIT_TILE_LOOP")) tile_loop = std::atoi(e);
+    // the loop body's complex product: scalar in place (phase_cs, default) or
+    // packed (phase_ct: FMUL, FMUL, FFMA2 per amplitude)
+    const char *loop_form = "phase_cs";
+    if (const char *e = std::getenv("QSB_JIT_LOOP_FORM"))
+        if (!std::strcmp(e, "ct")) loop_form = "phase_ct";
     std::string consts;
     int nconst = 0;
     std::string src;
@@ -385,7 +390,7 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
                     std::snprintf(buf, sizeof buf,
                                   "\n        while (m) { const int i = __ffs(m) - 1; m &= m - 1u;"
                                   " %s<%d, %s, RB>(make_float2(ops[%d + i].m[6], ops[%d + i].m[7]), v); } }\n",
-                                  planar ? "pphase" : "phase_cs", (int)op.reg_need, op.half_need ? "true" : "false", o, o);
+                                  planar ? "pphase" : loop_form, (int)op.reg_need, op.half_need ? "true" : "false", o, o);
                     src += buf;
                     o = e2;
                     continue;
@@ -425,7 +430,7 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
                     std::snprintf(buf, sizeof buf,
                                   "\n        while (m) { const int i = __ffs(m) - 1; m &= m - 1u;"
                                   " %s<%d, %s, RB>(make_float2(__uint_as_float(kT%d[2 * i]), __uint_as_float(kT%d[2 * i + 1])), v); } }\n",
-                                  planar ? "pphase" : "phase_cs", R, op.half_need ? "true" : "false", id, id);
+                                  planar ? "pphase" : loop_form, R, op.half_need ? "true" : "false", id, id);
                     src += buf;
                     o = e2;
                     continue;
