@@ -649,7 +649,6 @@ void cache_store(const std::string &path, const std::string &src, const std::vec
     if (path.empty()) return;
     const size_t slash = path.rfind('/');
     const std::string dir = path.substr(0, slash);
-    std::string cmd;
     for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
         if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
     const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)pthread_self());

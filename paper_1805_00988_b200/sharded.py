@@ -420,7 +420,7 @@ class ShardedState:
         # "auto": decided at the first global-target pair gate by timing both
         # paths on the live register (calibrate_global_gates)
         self._auto_peer = peer_gates == "auto" and can_peer
-        self.peer_gates = (peer_gates is True or self._auto_peer) and can_peer
+        self.peer_gates = (self._auto_peer or (peer_gates != "auto" and bool(peer_gates))) and can_peer
         self.calibration = None
         # Qubit-swap data movement: "nccl" (transport send/recv; in-process
         # copies for virtual shards) or "peer" (qs_swap_peer: one kernel per
