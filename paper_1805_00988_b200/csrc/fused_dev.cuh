@@ -681,6 +681,13 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         for (;; ++i) {
             const int b = i % kNB;
             float4 *buf = buf0 + b * kBufF4;
+            // the next tile's index first (warp-wide), so that afterwards each
+            // lane moves from its store copy to its load copy on its own: a
+            // lane's load into a copy region waits only for ITS store of that
+            // region to have been read out (no warp-wide barrier in between)
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(p.tile_ctr, 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
             if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
                 mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
                 const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
@@ -693,12 +700,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                         tma_store_5d(map, (int)row, buf + c * kCopyF4);
                 }
                 bulk_commit();
-                bulk_wait_read0();  // buffer b may be overwritten
-                __syncwarp();
             }
-            unsigned long long t = 0;
-            if (lane == 0) t = atomicAdd(p.tile_ctr, 1ull);
-            t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= p.ntiles) {
                 if (lane == 0) {
                     // every CTA draws exactly one index >= ntiles; the largest
@@ -718,11 +720,11 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                 else
                     mbar_arrive_expect_tx(&full[b], kBoxBytes * (uint32_t)p.ncopies);
             }
-            __syncwarp();
             const uint32_t row0 = (uint32_t)(base >> kLowQ);
             for (int c = lane; c < (p.dry == 4 ? 0 : p.ncopies); c += 32) {
                 uint32_t row = row0;
                 for (int k = 0; k < 4; ++k) row |= (uint32_t)((c >> k) & 1) << p.crow[k];
+                if (i >= kNB && c == lane) bulk_wait_read0();  // this lane's store of the region is read out
                 if (p.l2hint)
                     tma_load_5d_hint(buf + c * kCopyF4, map, (int)row, &full[b], pol);
                 else
