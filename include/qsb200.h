@@ -236,6 +236,9 @@ int qs_ipc_close(int device, void *ptr);
  * on other global qubits are rank predicates of the caller).  The caller
  * orders the two shards' streams before and after. */
 int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const float m[8]);
+/* The same with fp64 entries (complex128 shards; on complex64 shards the
+ * entries are rounded to float32).  qs_swap_peer works on either precision. */
+int qs_apply_gate_peer_f64(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const double m[8]);
 /* Qubit-swap exchange over peer memory (the data movement of a global-target
  * swap, sharded.py's exchange_plan): amplitudes [own_offset, own_offset +
  * count) of this shard trade places with [peer_offset, peer_offset + count)

@@ -35,7 +35,7 @@ EXPORTS = (
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
-    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_swap_peer", "qs_jit_sync", "qs_jit_stats",
+    "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_apply_gate_peer_f64", "qs_swap_peer", "qs_jit_sync", "qs_jit_stats",
     "qs_jit_shutdown", "qs_begin_capture", "qs_end_capture", "qs_graph_launch", "qs_graph_destroy",
     "qs_create_sharded", "qs_sharded_destroy", "qs_sharded_info", "qs_sharded_shard", "qs_sharded_set_mode",
     "qs_sharded_stats", "qs_sharded_reset", "qs_sharded_apply_gate", "qs_sharded_apply_controlled_gate",
@@ -119,6 +119,7 @@ def _declare(L):
         "qs_ipc_close": ([i32, vp], i32),
         "qs_apply_gate_peer": ([vp, vp, i32, u64, f32p], i32),
         "qs_swap_peer": ([vp, vp, u64, u64, u64], i32),
+        "qs_apply_gate_peer_f64": ([vp, vp, i32, u64, f64p], i32),
         "qs_create_sharded": ([i32, i32, ctypes.POINTER(i32), u64, ctypes.POINTER(vp)], i32),
         "qs_sharded_destroy": ([vp], i32),
         "qs_sharded_info": ([vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),

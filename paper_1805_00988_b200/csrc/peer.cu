@@ -96,6 +96,42 @@ __global__ void __launch_bounds__(256) k_peer_pair16(float4 *__restrict__ own, f
     }
 }
 
+// complex128 shards: the same pair update on 16-B amplitudes (the sweep's
+// fp64 arithmetic, gates64.cu pair_update_d)
+struct PeerGateD {
+    double2 a, b, c, d;
+};
+
+template <int U>
+__global__ void __launch_bounds__(256) k_peer_pair_d(double2 *__restrict__ own, double2 *__restrict__ peer,
+                                                     uint64_t nitems, FixedBits fb, uint64_t set_mask,
+                                                     int own_is_a, PeerGateD g) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = tid; base < nitems; base += nthreads * U) {
+        double2 x[U], y[U];
+        uint64_t idx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t item = base + u * nthreads;
+            idx[u] = deposit(item, fb) | set_mask;
+            if (item < nitems) {
+                x[u] = __ldcs(own + idx[u]);
+                y[u] = __ldcg(peer + idx[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (base + u * nthreads >= nitems) continue;
+            const double2 va = own_is_a ? x[u] : y[u], vb = own_is_a ? y[u] : x[u];
+            const double2 na = cadd_d(cmul_d(g.a, va), cmul_d(g.b, vb));
+            const double2 nb = cadd_d(cmul_d(g.d, vb), cmul_d(g.c, va));
+            __stcs(own + idx[u], own_is_a ? na : nb);
+            __stcg(peer + idx[u], own_is_a ? nb : na);
+        }
+    }
+}
+
 // Qubit-swap exchange over peer memory: own[i] <-> peer[i] for i < n units
 // of 16 B (two complex64 amplitudes).  Both partners run it at once on
 // disjoint halves of the exchanged range, so the swap is one pass with no
@@ -190,10 +226,11 @@ int qs_ipc_close(int device, void *ptr) {
     return QS_OK;
 }
 
-int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const float m[8]) {
+static int apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const float *m,
+                           const double *md) {
     if (!s) return set_error(QS_ERR_NULL, "null qs_state handle");
-    if (!peer_amps || !m) return set_error(QS_ERR_NULL, "null peer buffer or gate matrix");
-    if (s->prec != QS_SINGLE) return set_error(QS_ERR_VALUE, "peer gates need complex64 shards");
+    if (!peer_amps || (!m && !md)) return set_error(QS_ERR_NULL, "null peer buffer or gate matrix");
+    const bool dbl = s->prec == QS_DOUBLE;
     const int L = s->num_qubits;
     if (L < 64 && (ctrl_mask >> L)) return set_error(QS_ERR_INDEX, "local control out of range");
     if (__builtin_popcountll(ctrl_mask) + 1 > kMaxFixed) return set_error(QS_ERR_VALUE, "too many control qubits");
@@ -224,11 +261,27 @@ int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl
         }
     DeviceGuard guard(s->device);
     constexpr int U = 4;
+    if (dbl) {  // complex128: 16-B amplitudes
+        double e[8];
+        for (int i = 0; i < 8; ++i) e[i] = md ? md[i] : (double)m[i];
+        PeerGateD g{make_double2(e[0], e[1]), make_double2(e[2], e[3]), make_double2(e[4], e[5]),
+                    make_double2(e[6], e[7])};
+        FixedBits fb;
+        fb.n = np;
+        for (int i = 0; i < kMaxFixed; ++i) fb.pos[i] = i < np ? pos[i] : 0;
+        const uint64_t nitems = 1ull << (L - np);
+        k_peer_pair_d<U><<<grid_for(s, nitems, U), 256, 0, s->stream>>>((double2 *)s->amps, (double2 *)peer_amps,
+                                                                         nitems, fb, set_mask, own_is_a, g);
+        QS_CUDA(cudaGetLastError());
+        return QS_OK;
+    }
+    float mf[8];
+    for (int i = 0; i < 8; ++i) mf[i] = m ? m[i] : (float)md[i];
     const bool wide = np == 0 || pos[0] > 0;  // local bit 0 free: 16-B units
     FixedBits fb;
     fb.n = np;
     for (int i = 0; i < kMaxFixed; ++i) fb.pos[i] = i < np ? pos[i] - (wide ? 1 : 0) : 0;
-    const Gate2 g = gate_from(m);
+    const Gate2 g = gate_from(mf);
     if (wide) {
         const uint64_t nitems = 1ull << (L - 1 - np);
         k_peer_pair16<U><<<grid_for(s, nitems, U), 256, 0, s->stream>>>(
@@ -242,14 +295,23 @@ int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl
     return QS_OK;
 }
 
+int qs_apply_gate_peer(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const float m[8]) {
+    return apply_gate_peer(s, peer_amps, own_is_a, ctrl_mask, m, nullptr);
+}
+
+int qs_apply_gate_peer_f64(qs_state *s, void *peer_amps, int own_is_a, uint64_t ctrl_mask, const double m[8]) {
+    return apply_gate_peer(s, peer_amps, own_is_a, ctrl_mask, nullptr, m);
+}
+
 int qs_swap_peer(qs_state *s, void *peer_amps, uint64_t own_offset, uint64_t peer_offset, uint64_t count) {
     if (!s) return set_error(QS_ERR_NULL, "null qs_state handle");
     if (!peer_amps) return set_error(QS_ERR_NULL, "null peer buffer");
-    if (s->prec != QS_SINGLE) return set_error(QS_ERR_VALUE, "peer swaps need complex64 shards");
     const uint64_t dim = 1ull << s->num_qubits;
     if (own_offset > dim || count > dim - own_offset) return set_error(QS_ERR_INDEX, "swap range out of bounds");
     if (count == 0) return QS_OK;
     DeviceGuard guard(s->device);
+    if (s->prec == QS_DOUBLE)  // 16-B amplitudes = two float2 units each
+        return launch_peer_swap(s, s->amps + 2 * own_offset, (float2 *)peer_amps + 2 * peer_offset, 2 * count);
     return launch_peer_swap(s, s->amps + own_offset, (float2 *)peer_amps + peer_offset, count);
 }
 

@@ -84,19 +84,22 @@ def exchange_plan(rank: int, rank_bit: int, L: int) -> tuple[int, int, int]:
 class CudaEngine:
     """One shard on a GPU: a libqsb200 State of L qubits."""
 
-    def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None):
+    def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None,
+                 precision: str = "single"):
         from .state import State
 
-        self.state = State(num_qubits, device=device, memory_budget=memory_budget)
+        self.state = State(num_qubits, device=device, memory_budget=memory_budget, precision=precision)
         self.num_qubits = num_qubits
         self.device = device
+        self.double = self.state.is_double
+        self.unit = 4 if self.double else 2  # float32 words per amplitude (exchange views)
         self._view = None
 
     def reset(self, basis: int | None) -> None:
         """e_basis, or the zero vector for basis=None (a shard not holding |basis>)."""
         self.state.reset(0 if basis is None else basis)
         if basis is None:
-            self.state.set_amplitudes(np.zeros(1, np.complex64), offset=0)
+            self.state.set_amplitudes(np.zeros(1, np.complex128 if self.double else np.complex64), offset=0)
 
     def apply(self, kind: int, target: int, ctrl_mask: int, m: np.ndarray) -> None:
         from . import fusion
@@ -106,18 +109,19 @@ class CudaEngine:
     def apply_ops(self, ops, exact: bool = True) -> None:
         from . import fusion
 
-        fusion.run(self.state, fusion.plan(self.num_qubits, ops, reorder=not exact), combine=not exact)
+        K = 12 if self.double else None  # complex128 tiles: 2^12 amplitudes (64 KiB)
+        fusion.run(self.state, fusion.plan(self.num_qubits, ops, K, reorder=not exact), combine=not exact)
 
     def swap_qubits(self, a: int, b: int) -> None:
         self.state.swap_qubits(a, b)
 
     def view(self):
-        """torch float32 view (2 * 2^L,) of the device amplitudes (zero-copy)."""
+        """torch float32 view (unit * 2^L,) of the device amplitudes (zero-copy)."""
         import torch
 
         if self._view is None:
             ptr = self.state.device_pointer()
-            nfloat = 2 << self.num_qubits
+            nfloat = self.unit << self.num_qubits
 
             class _CAI:
                 __cuda_array_interface__ = {"shape": (nfloat,), "typestr": "<f4", "data": (ptr, False),
@@ -188,6 +192,11 @@ class CudaEngine:
         N.check(N.lib().qs_swap_peer(self.state.handle, peer, int(own_off), int(peer_off), int(count)))
 
     def peer_gate(self, peer, own_is_a: bool, ctrl_mask: int, m: np.ndarray) -> None:
+        if m.dtype == np.float64:
+            mm = np.ascontiguousarray(m)
+            N.check(N.lib().qs_apply_gate_peer_f64(self.state.handle, peer, int(bool(own_is_a)), int(ctrl_mask),
+                                                   N.f64ptr(mm)))
+            return
         mm = np.ascontiguousarray(m, dtype=np.float32)
         N.check(N.lib().qs_apply_gate_peer(self.state.handle, peer, int(bool(own_is_a)), int(ctrl_mask),
                                            N.f32ptr(mm)))
@@ -210,8 +219,9 @@ class LocalTransport:
             a.comm_begin()
             b.comm_begin()
             va, vb = a.view(), b.view()
-            sa = va[2 * off: 2 * (off + cnt)]
-            sb = vb[2 * poff: 2 * (poff + cnt)]
+            u = getattr(a, "unit", 2)  # float32 words per amplitude
+            sa = va[u * off: u * (off + cnt)]
+            sb = vb[u * poff: u * (poff + cnt)]
             tmp = sa.clone()
             sa.copy_(sb)
             sb.copy_(tmp)
@@ -270,17 +280,18 @@ class DistTransport:
         partner, off, cnt = exchange_plan(self.rank, rank_bit, L)
         eng.comm_begin()
         v = eng.view()
+        u = getattr(eng, "unit", 2)  # float32 words per amplitude
         step = min(cnt, chunk)
         nbuf = 2 if cnt > step else 1
-        if self._staging is None or self._staging.numel() < 2 * step * nbuf or self._staging.device != v.device:
-            self._staging = v.new_empty(2 * step * nbuf)
+        if self._staging is None or self._staging.numel() < u * step * nbuf or self._staging.device != v.device:
+            self._staging = v.new_empty(u * step * nbuf)
         peer = dist.get_global_rank(self.group, partner) if self.group is not None else partner
         starts = list(range(off, off + cnt, step))
 
         def post(i):
             c = starts[i]
-            mine = v[2 * c: 2 * (c + step)]
-            stg = self._staging[2 * step * (i % nbuf): 2 * step * (i % nbuf + 1)]
+            mine = v[u * c: u * (c + step)]
+            stg = self._staging[u * step * (i % nbuf): u * step * (i % nbuf + 1)]
             ops = [dist.P2POp(dist.isend, mine, peer, self.group), dist.P2POp(dist.irecv, stg, peer, self.group)]
             return dist.batch_isend_irecv(ops), mine, stg
 
@@ -439,11 +450,19 @@ class ShardedState:
         self.peer_gate_count = 0
         self.peer_swaps = 0
         self.shard_phases = 0
+        self.double = bool(getattr(self.engines[0], "double", False)) if self.engines else False
+
+    def _m8(self, gate) -> np.ndarray:
+        """Gate entries rounded to the shards' precision (kernel.py:118-119)."""
+        from .gates import m8_for
+
+        return m8_for(gate, self.double)
 
     # ---- constructors ------------------------------------------------------
     @classmethod
     def distributed(cls, num_qubits: int, group=None, device: int | None = None, engine_factory=None,
-                    peer_gates: bool | None = None, memory_budget: int | None = None, exchange: str | None = None):
+                    peer_gates: bool | None = None, memory_budget: int | None = None, exchange: str | None = None,
+                    precision: str = "single"):
         import torch.distributed as dist
 
         tr = DistTransport(group)
@@ -453,7 +472,7 @@ class ShardedState:
             import torch
 
             dev = torch.cuda.current_device() if device is None else device
-            eng = CudaEngine(L, dev, memory_budget=memory_budget)
+            eng = CudaEngine(L, dev, memory_budget=memory_budget, precision=precision)
         else:
             eng = engine_factory(L)
         st = cls(num_qubits, [eng], tr, [tr.rank], tr.world, peer_gates=peer_gates, exchange=exchange)
@@ -462,10 +481,12 @@ class ShardedState:
 
     @classmethod
     def virtual(cls, num_qubits: int, shards: int, device: int = 0, engine_factory=None,
-                peer_gates: bool | None = None, memory_budget: int | None = None, exchange: str | None = None):
+                peer_gates: bool | None = None, memory_budget: int | None = None, exchange: str | None = None,
+                precision: str = "single"):
         g = int(round(math.log2(shards)))
         L = num_qubits - g
-        make = engine_factory or (lambda L_: CudaEngine(L_, device, memory_budget=memory_budget))
+        make = engine_factory or (lambda L_: CudaEngine(L_, device, memory_budget=memory_budget,
+                                                        precision=precision))
         engines = [make(L) for _ in range(shards)]
         st = cls(num_qubits, engines, LocalTransport(shards), list(range(shards)), shards, peer_gates=peer_gates,
                  exchange=exchange)
@@ -559,7 +580,7 @@ class ShardedState:
 
         from .gates import FIXED_GATES
 
-        X = m8(FIXED_GATES["x"])
+        X = self._m8(FIXED_GATES["x"])
         L = self.L
 
         def timed(fn):
@@ -601,7 +622,7 @@ class ShardedState:
         need = 0
         for b in rank_bits:
             need |= 1 << b
-        dd = np.zeros(8, np.float32)
+        dd = np.zeros(8, m.dtype)
         dd[0], dd[1], dd[6], dd[7] = m[6], m[7], m[6], m[7]
         for eng, r in zip(self.engines, self.ranks):
             if (r & need) == need:
@@ -628,7 +649,7 @@ class ShardedState:
                 raise IndexError(f"qubit {q} out of range for {n} qubits")
         if len(set(qs)) != len(qs):
             raise ValueError("control and target must differ")
-        m = m8(gate)
+        m = self._m8(gate)
         from .gates import is_phase
 
         kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
@@ -718,7 +739,7 @@ class ShardedState:
                 gate, target, controls = ins.gate, ins.target, (ins.control1, ins.control2)
             else:
                 continue
-            m = m8(gate)
+            m = self._m8(gate)
             from .gates import is_phase
 
             kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
@@ -798,7 +819,7 @@ class ShardedState:
         parts = self.local_amplitudes()
         if len(parts) == self.world:
             return np.concatenate([parts[r] for r in range(self.world)])
-        return self._gather(parts, np.complex64)
+        return self._gather(parts, np.complex128 if self.double else np.complex64)
 
     def probabilities(self) -> np.ndarray:
         self.canonicalize()

@@ -97,3 +97,23 @@ def test_inexact_sharded_run_to_tolerance():
     st.run(circ, exact=False)
     np.testing.assert_allclose(st.amplitudes(), ref.amplitudes(), rtol=1e-5, atol=1e-5 * 2.0 ** (-n / 2))
     st.close()
+
+
+@pytest.mark.parametrize("peer_gates,exchange", [(False, "nccl"), (False, "peer"), (True, "peer")])
+def test_complex128_shards_equal_unsharded(peer_gates, exchange):
+    """Precision.DOUBLE registers sharded: swaps (copies or the peer swap
+    kernel) and peer gates on 16-B amplitudes, bit-exact vs the unsharded
+    complex128 register, probabilities and draws included."""
+    n = 14
+    circ = Circuit(n, build_hadamard_layer(n).instructions + mixed_circuit(n, 90, 21).instructions
+                   + build_qft(n).instructions[-30:])
+    ref = State(n, precision="double")
+    execute(circ, ref, fuse=False)
+    st = ShardedState.virtual(n, 4, peer_gates=peer_gates, exchange=exchange, precision="double")
+    st.run(circ)
+    a = st.amplitudes()
+    assert a.dtype == np.complex128 and same_values(a, ref.amplitudes())
+    assert st.probabilities().tobytes() == ref.probabilities().tobytes()
+    assert np.array_equal(st.sample_outcomes(3000, 5), ref.sample_outcomes(3000, 5))
+    st.close()
+    ref.close()
