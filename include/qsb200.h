@@ -275,6 +275,12 @@ int qs_sharded_apply_gate(qs_sharded *h, int target, const float m[8]);
 int qs_sharded_apply_controlled_gate(qs_sharded *h, int control, int target, const float m[8]);
 int qs_sharded_apply_controlled_controlled_gate(qs_sharded *h, int c1, int c2, int target, const float m[8]);
 int qs_sharded_synchronize(qs_sharded *h);
+/* The lazy qubit map (pos[logical] = physical position; >= shard_qubits =
+ * global) and a qubit swap bringing `qubit` to a local position: with
+ * qs_sharded_shard, what a caller needs to run fused passes of local ops on
+ * the shards between global-target gates (multigpu.MultiDeviceState.run). */
+int qs_sharded_qubit_map(const qs_sharded *h, int32_t *pos);
+int qs_sharded_localize(qs_sharded *h, int qubit);
 int qs_sharded_get_amplitudes(qs_sharded *h, uint64_t offset, uint64_t count, void *host);
 int qs_sharded_set_amplitudes(qs_sharded *h, uint64_t offset, uint64_t count, const void *host);
 int qs_sharded_probabilities(qs_sharded *h, uint64_t offset, uint64_t count, double *host);

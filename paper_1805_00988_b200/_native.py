@@ -41,6 +41,7 @@ EXPORTS = (
     "qs_sharded_stats", "qs_sharded_reset", "qs_sharded_apply_gate", "qs_sharded_apply_controlled_gate",
     "qs_sharded_apply_controlled_controlled_gate", "qs_sharded_synchronize", "qs_sharded_get_amplitudes",
     "qs_sharded_set_amplitudes", "qs_sharded_probabilities", "qs_sharded_norm_squared", "qs_sharded_sample",
+    "qs_sharded_qubit_map", "qs_sharded_localize",
 )
 QS_EXCHANGE_NCCL, QS_EXCHANGE_P2P = 1, 2
 QS_FUSED_COMBINE_PHASES = 1
@@ -136,6 +137,8 @@ def _declare(L):
         "qs_sharded_probabilities": ([vp, u64, u64, vp], i32),
         "qs_sharded_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sharded_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),
+        "qs_sharded_qubit_map": ([vp, ctypes.POINTER(ctypes.c_int32)], i32),
+        "qs_sharded_localize": ([vp, i32], i32),
         "qs_jit_sync": ([i32], i32),
         "qs_jit_stats": ([ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64)], i32),
         "qs_jit_shutdown": ([], i32),

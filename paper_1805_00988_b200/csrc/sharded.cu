@@ -512,6 +512,18 @@ int qs_sharded_apply_controlled_controlled_gate(qs_sharded *h, int c1, int c2, i
     return apply(h, target, 2, c, m);
 }
 
+int qs_sharded_qubit_map(const qs_sharded *h, int32_t *pos) {
+    if (!h || !pos) return set_error(QS_ERR_NULL, "null handle or output buffer");
+    for (int q = 0; q < h->n; ++q) pos[q] = h->pos[q];
+    return QS_OK;
+}
+
+int qs_sharded_localize(qs_sharded *h, int qubit) {
+    if (!h) return set_error(QS_ERR_NULL, "null qs_sharded handle");
+    if (qubit < 0 || qubit >= h->n) return set_error(QS_ERR_INDEX, "qubit out of range");
+    return ensure_local(h, qubit);
+}
+
 int qs_sharded_synchronize(qs_sharded *h) {
     if (!h) return set_error(QS_ERR_NULL, "null qs_sharded handle");
     return sync_all(h);

@@ -23,6 +23,23 @@ from . import _native as N
 from .gates import FIXED_GATES, m8, u1 as _u1
 
 
+class _Shard:
+    """One shard's qs_state as the object fusion.run drives (State's fused-pass
+    entry points on a borrowed handle; the register owns the shard)."""
+
+    def __init__(self, reg: "MultiDeviceState", rank: int, num_qubits: int):
+        ptr = ctypes.c_void_p()
+        N.check(N.lib().qs_sharded_shard(reg.handle, int(rank), ctypes.byref(ptr)))
+        self.handle = ptr
+        self.num_qubits = num_qubits
+        self.is_double = False
+
+    def apply_fused(self, tile_qubits, ops, combine: bool = False):
+        from .state import State
+
+        return State.apply_fused(self, tile_qubits, ops, combine)
+
+
 class MultiDeviceState:
     def __init__(self, num_qubits: int, devices, memory_budget: int | None = None,
                  peer_gates: bool | None = None, exchange: str | None = None):
@@ -126,16 +143,82 @@ class MultiDeviceState:
     def ccx(self, c1, c2, target):
         return self.apply_controlled_controlled_gate(FIXED_GATES["x"], c1, c2, target)
 
-    def run(self, circuit) -> "MultiDeviceState":
-        from .circuits import Apply, ControlledApply, ControlledControlledApply
+    def qubit_map(self) -> list[int]:
+        """pos[logical qubit] = physical position (>= shard_qubits: global)."""
+        arr = (ctypes.c_int32 * self.num_qubits)()
+        N.check(N.lib().qs_sharded_qubit_map(self.handle, arr))
+        return list(arr)
 
-        for ins in circuit.instructions:
+    def run(self, circuit, fuse: bool = True, exact: bool = True) -> "MultiDeviceState":
+        """Apply a circuit.  fuse=True: maximal runs of local ops run as fused
+        passes on every shard (the single-device planner and kernels, through
+        each shard's qs_state); a pair gate on a global qubit (qubit swap or
+        peer gate) and a diagonal gate on global-only bits go through the C
+        ABI in between.  exact=False as in circuits.execute."""
+        from . import fusion
+        from .circuits import Apply, ControlledApply, ControlledControlledApply
+        from .gates import is_phase
+
+        def split(ins):
             if isinstance(ins, Apply):
-                self.apply_gate(ins.gate, ins.target)
-            elif isinstance(ins, ControlledApply):
-                self.apply_controlled_gate(ins.gate, ins.control, ins.target)
-            elif isinstance(ins, ControlledControlledApply):
-                self.apply_controlled_controlled_gate(ins.gate, ins.control1, ins.control2, ins.target)
+                return ins.gate, ins.target, ()
+            if isinstance(ins, ControlledApply):
+                return ins.gate, ins.target, (ins.control,)
+            if isinstance(ins, ControlledControlledApply):
+                return ins.gate, ins.target, (ins.control1, ins.control2)
+            return None
+
+        def one(gate, target, controls):
+            if not controls:
+                self.apply_gate(gate, target)
+            elif len(controls) == 1:
+                self.apply_controlled_gate(gate, controls[0], target)
+            else:
+                self.apply_controlled_controlled_gate(gate, controls[0], controls[1], target)
+
+        if not fuse:
+            for ins in circuit.instructions:
+                g = split(ins)
+                if g is not None:
+                    one(*g)
+            return self
+        L = self.shard_qubits
+        shards = [_Shard(self, r, L) for r in range(len(self.devices))]
+        pending: list = []
+
+        def flush():
+            for r, sh in enumerate(shards):
+                ops = [(k, t, cm, m) for (k, t, cm, m, need) in pending if (r & need) == need]
+                if ops:
+                    fusion.run(sh, fusion.plan(L, ops, reorder=not exact), combine=not exact)
+            pending.clear()
+
+        pos = self.qubit_map()
+        for ins in circuit.instructions:
+            g = split(ins)
+            if g is None:
+                continue
+            gate, target, controls = g
+            m = m8(gate)
+            kind = N.QS_OP_PHASE if is_phase(m) else N.QS_OP_PAIR
+            qs = [target, *controls]
+            if kind == N.QS_OP_PHASE and pos[target] >= L:
+                local = [q for q in qs if pos[q] < L]
+                if local:
+                    target, controls = local[0], tuple(q for q in qs if q != local[0])
+            if pos[target] >= L:  # global pair target, or a diagonal gate on global-only bits
+                flush()
+                one(gate, *g[1:])
+                pos = self.qubit_map()
+                continue
+            cmask, need = 0, 0
+            for c in controls:
+                if pos[c] < L:
+                    cmask |= 1 << pos[c]
+                else:
+                    need |= 1 << (pos[c] - L)
+            pending.append((kind, pos[target], cmask, m, need))
+        flush()
         return self
 
     def flush(self) -> None:

@@ -108,3 +108,33 @@ def test_fused_passes_on_two_devices_in_one_process():
         outs.append(st.amplitudes())
         st.close()
     assert same_values(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n,shards,peer_gates", [(14, 4, False), (16, 2, True), (22, 4, False)])
+def test_fused_run_equals_unsharded(n, shards, peer_gates):
+    """MultiDeviceState.run with fused local passes on the shards between the
+    C ABI's global gates == the unsharded register, bitwise."""
+    circ = _circ(n, 3 * n + shards)
+    ref = State(n)
+    execute(circ, ref, fuse=False)
+    with MultiDeviceState(n, [0] * shards, peer_gates=peer_gates) as reg:
+        reg.run(circ, fuse=True)
+        assert same_values(reg.amplitudes(), ref.amplitudes())
+        assert np.array_equal(reg.sample_outcomes(2000, 3), ref.sample_outcomes(2000, 3))
+    ref.close()
+
+
+def test_fused_run_inexact_to_tolerance():
+    from paper_1805_00988_b200 import fusion
+
+    n = 20
+    circ = Circuit(n, build_hadamard_layer(n).instructions + build_qft(n).instructions)
+    ref = State(n)
+    execute(circ, ref, fuse=False)
+    with MultiDeviceState(n, [0, 0, 0, 0]) as reg:
+        reg.run(circ, exact=False)
+        fusion.jit_sync()
+        reg.reset(0)
+        reg.run(circ, exact=False)
+        np.testing.assert_allclose(reg.amplitudes(), ref.amplitudes(), rtol=1e-5, atol=1e-5 * 2.0 ** (-n / 2))
+    ref.close()
