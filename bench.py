@@ -665,7 +665,7 @@ def run_single_process(n, world, rank):
     out = None
     if rank == 0:
         try:
-            from paper_1805_00988_b200 import build_qft
+            from paper_1805_00988_b200 import build_qft, fusion
             from paper_1805_00988_b200.multigpu import MultiDeviceState
 
             out = {"n_qubits": n, "devices": world}
@@ -691,10 +691,45 @@ def run_single_process(n, world, rank):
                 md.flush()
                 t_layer = time.perf_counter() - t0
                 t0 = time.perf_counter()
-                md.run(build_qft(n))
+                md.run(build_qft(n), fuse=False)
                 md.flush()
                 t_qft = time.perf_counter() - t0
-                out[label] = {"hlayer_ms": t_layer * 1e3, "qft_unfused_ms": t_qft * 1e3, **md.stats()}
+                md.run(build_qft(n))  # fused local passes: compiles, then timed
+                fusion.jit_sync()
+                md.flush()
+                t0 = time.perf_counter()
+                md.run(build_qft(n))
+                md.flush()
+                t_qft_f = time.perf_counter() - t0
+                out[label] = {"hlayer_ms": t_layer * 1e3, "qft_unfused_ms": t_qft * 1e3,
+                              "qft_fused_ms": t_qft_f * 1e3, **md.stats()}
+                md.close()
+            if world >= 4:  # config 5 through the single-process C ABI
+                import torch
+
+                from paper_1805_00988_b200 import _native as N
+                from paper_1805_00988_b200 import build_hadamard_layer
+
+                N.lib().qs_release_cached(-1)
+                free_b = min(torch.cuda.mem_get_info(d)[0] for d in range(torch.cuda.device_count()))
+                md = MultiDeviceState(36, [r % torch.cuda.device_count() for r in range(world)],
+                                      memory_budget=max(1, free_b - (6 << 30)))
+                md.run(build_hadamard_layer(36))
+                md.run(build_qft(36))
+                fusion.jit_sync()
+                md.reset(0)
+                md.flush()
+                t0 = time.perf_counter()
+                md.run(build_hadamard_layer(36))
+                md.flush()
+                t1 = time.perf_counter()
+                md.run(build_qft(36))
+                md.flush()
+                t2 = time.perf_counter()
+                a0 = complex(md.amplitudes(0, 1)[0])
+                out["config5_hlayer_qft36"] = {"hlayer_s": t1 - t0, "qft_s": t2 - t1, **md.stats(),
+                                               "amp0_after_qft": [a0.real, a0.imag],
+                                               "analytic_check_ok": bool(abs(abs(a0) - 1.0) < 1e-2)}
                 md.close()
         except Exception as exc:  # noqa: BLE001
             out = {"error": f"{type(exc).__name__}: {exc}"}
