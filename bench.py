@@ -705,36 +705,48 @@ def run_single_process(n, world, rank):
                               "qft_fused_ms": t_qft_f * 1e3, **md.stats()}
                 md.close()
             if world >= 4:  # config 5 through the single-process C ABI
-                import torch
-
-                from paper_1805_00988_b200 import _native as N
-                from paper_1805_00988_b200 import build_hadamard_layer
-
-                N.lib().qs_release_cached(-1)
-                free_b = min(torch.cuda.mem_get_info(d)[0] for d in range(torch.cuda.device_count()))
-                md = MultiDeviceState(36, [r % torch.cuda.device_count() for r in range(world)],
-                                      memory_budget=max(1, free_b - (6 << 30)))
-                md.run(build_hadamard_layer(36))
-                md.run(build_qft(36))
-                fusion.jit_sync()
-                md.reset(0)
-                md.flush()
-                t0 = time.perf_counter()
-                md.run(build_hadamard_layer(36))
-                md.flush()
-                t1 = time.perf_counter()
-                md.run(build_qft(36))
-                md.flush()
-                t2 = time.perf_counter()
-                a0 = complex(md.amplitudes(0, 1)[0])
-                out["config5_hlayer_qft36"] = {"hlayer_s": t1 - t0, "qft_s": t2 - t1, **md.stats(),
-                                               "amp0_after_qft": [a0.real, a0.imag],
-                                               "analytic_check_ok": bool(abs(abs(a0) - 1.0) < 1e-2)}
-                md.close()
+                out["config5_hlayer_qft36"] = _config5_single_process(world)
         except Exception as exc:  # noqa: BLE001
             out = {"error": f"{type(exc).__name__}: {exc}"}
     dist.barrier()
     return out
+
+
+def _config5_single_process(world):
+    """BASELINE config 5 driven by one process (qs_create_sharded over the N
+    devices): H on all 36 qubits, then QFT(36) with fused local passes;
+    analytic check |amplitude(0)| ~ 1."""
+    try:
+        import torch
+
+        from paper_1805_00988_b200 import _native as N
+        from paper_1805_00988_b200 import build_hadamard_layer, build_qft, fusion
+        from paper_1805_00988_b200.multigpu import MultiDeviceState
+
+        N.lib().qs_release_cached(-1)
+        ndev = torch.cuda.device_count()
+        free_b = min(torch.cuda.mem_get_info(d)[0] for d in range(ndev))
+        md = MultiDeviceState(36, [r % ndev for r in range(world)], memory_budget=max(1, free_b - (6 << 30)))
+        try:
+            md.run(build_hadamard_layer(36))
+            md.run(build_qft(36))
+            fusion.jit_sync()
+            md.reset(0)
+            md.flush()
+            t0 = time.perf_counter()
+            md.run(build_hadamard_layer(36))
+            md.flush()
+            t1 = time.perf_counter()
+            md.run(build_qft(36))
+            md.flush()
+            t2 = time.perf_counter()
+            a0 = complex(md.amplitudes(0, 1)[0])
+            return {"hlayer_s": t1 - t0, "qft_s": t2 - t1, **md.stats(), "amp0_after_qft": [a0.real, a0.imag],
+                    "analytic_check_ok": bool(abs(abs(a0) - 1.0) < 1e-2), "timing": "host wall clock, synchronised"}
+        finally:
+            md.close()
+    except Exception as exc:  # noqa: BLE001
+        return {"error": f"{type(exc).__name__}: {exc}"}
 
 
 def run_global_gate_probe(n, local, world, reps=3):

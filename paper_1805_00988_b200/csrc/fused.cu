@@ -528,6 +528,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
 }
 
 int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops, int flags) {
+    NvtxRange nvtx_range("qsb fused pass");
     const int n = s->num_qubits;
     uint64_t tile_mask = 0;
     for (int i = 0; i < ntile; ++i) {

@@ -288,6 +288,7 @@ int launch_phase(qs_state *s, uint64_t mask, float2 d) {
 }
 
 int launch_sweep(qs_state *s, int target, uint64_t ctrl_mask, const float m_in[8]) {
+    NvtxRange nvtx_range("qsb sweep");
     const int n = s->num_qubits;
     float mf[8];
     for (int i = 0; i < 8; ++i) mf[i] = m_in[i];

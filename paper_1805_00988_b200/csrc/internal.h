@@ -30,7 +30,16 @@ struct qs_state {
     int ipc_exported;
 };
 
+#include <nvtx3/nvToolsExt.h>  // header-only; a no-op unless a tool (ncu / nsys) is attached
+
 namespace qsb {
+
+// NVTX range for the duration of a scope (SURVEY 5 tracing: per pass,
+// exchange, readout) — visible to ncu --nvtx / nsys timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int set_error(int code, const std::string &msg);
 

@@ -596,6 +596,7 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
 // next piece is in flight.  The team lives for the whole call: spawning
 // threads per piece cost more than the copies.
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host) {
+    NvtxRange nvtx_range("qsb probabilities");
     uint64_t piece = 1ull << 23;  // 64 MiB of fp64 per staging round
     if (const char *e = std::getenv("QSB_PROB_PIECE_LOG")) piece = 1ull << std::atoi(e);
     const uint64_t step = count < piece ? count : piece;
@@ -829,6 +830,7 @@ static int draw(qs_state *s, const CdfScratch &c, const qs_pcg64 *rng, int64_t k
 }
 
 int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
+    NvtxRange nvtx_range("qsb sample");
     CdfScratch c;
     int rc = cdf_scratch(s, k, c);
     if (rc) return rc;

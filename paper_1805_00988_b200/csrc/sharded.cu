@@ -149,6 +149,7 @@ void swap_physical(qs_sharded *h, int p1, int p2) {
 // shards r (rank bit 0) and r2 = r | 1 << rank_bit trade r's half with bit
 // L-1 = 1 and r2's half with bit L-1 = 0 (sharded.py exchange_plan).
 int exchange(qs_sharded *h, int rank_bit) {
+    NvtxRange nvtx_range("qsb sharded exchange");
     const uint64_t half = 1ull << (h->L - 1);
     const int bit = 1 << rank_bit;
     if (h->exchange == QS_EXCHANGE_NCCL) {

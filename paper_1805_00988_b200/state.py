@@ -366,6 +366,35 @@ class State:
         N.consume_draws(seed, 1)
         return int(out.value)
 
+    # ---- checkpoint / resume: the amplitudes as a .npy file -----
+    _CHUNK = 1 << 26  # amplitudes per host transfer (512 MiB of complex64)
+
+    def save(self, path) -> None:
+        """Write the register to `path` as a .npy array (complex64 or
+        complex128), streamed in chunks (no full host copy)."""
+        mm = np.lib.format.open_memmap(str(path), mode="w+", dtype=self.dtype, shape=(self.dim,))
+        try:
+            for off in range(0, self.dim, self._CHUNK):
+                cnt = min(self._CHUNK, self.dim - off)
+                mm[off: off + cnt] = self.amplitudes(off, cnt)
+            mm.flush()
+        finally:
+            del mm
+
+    @classmethod
+    def load(cls, path, device: int = 0, memory_budget: int | None = None) -> "State":
+        """A new register holding the amplitudes saved by `save` (or any 1-D
+        complex64 / complex128 .npy array of length 2^n)."""
+        arr = np.load(str(path), mmap_mode="r")
+        n = int(arr.shape[0]).bit_length() - 1
+        if arr.ndim != 1 or arr.shape[0] != 1 << n or arr.dtype not in (np.complex64, np.complex128):
+            raise ValueError("expected a 1-D complex64/complex128 array of length 2^n")
+        st = cls(n, device=device, memory_budget=memory_budget, precision=arr.dtype)
+        for off in range(0, arr.shape[0], cls._CHUNK):
+            cnt = min(cls._CHUNK, arr.shape[0] - off)
+            st.set_amplitudes(np.ascontiguousarray(arr[off: off + cnt]), offset=off)
+        return st
+
     def __repr__(self) -> str:
         prec = ", precision='double'" if self.is_double else ""
         return f"State(num_qubits={self.num_qubits}, device={self.device}{prec})"

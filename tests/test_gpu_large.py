@@ -380,3 +380,23 @@ class TestReadout:
         with pytest.raises(ValueError):
             st.probabilities(out=np.empty(10))
         st.close()
+
+
+class TestCheckpoint:
+    @pytest.mark.parametrize("precision", ["single", "double"])
+    def test_save_load_round_trip(self, tmp_path, precision):
+        from paper_1805_00988_b200 import fusion
+
+        n = 18
+        st = State(n, precision=precision)
+        execute(build_qft(n), st, fuse=False)
+        st.t(3)
+        st.cx(17, 2)
+        path = tmp_path / "reg.npy"
+        st.save(path)
+        back = State.load(path)
+        assert back.num_qubits == n and back.dtype == st.dtype
+        assert back.amplitudes().tobytes() == st.amplitudes().tobytes()
+        assert np.load(path).tobytes() == st.amplitudes().tobytes()
+        st.close()
+        back.close()
