@@ -337,6 +337,33 @@ def run_ours(args):
                          "two registers in flight, synchronized at the end"}
         st2.close()
         del inp, outs
+        # the circuit workflow a pairsim user runs (cli `run`: a circuit in,
+        # a histogram out): per step the op list goes H2D with the fused
+        # passes (kernel parameter blocks), the register starts from |0> on
+        # the device (pairsim's new_state), 1000 shots are drawn and the
+        # outcomes read back — reported beside e2e, which moves the whole
+        # 8 GiB register both ways every step
+        try:
+            from paper_1805_00988_b200 import _native as _Nw
+
+            st.reset(0)
+            fusion.run(st, layer_passes)
+            st.sample_outcomes(1000, 0)
+            st.flush()
+            reps = 10
+            t0 = time.perf_counter()
+            for k in range(reps):
+                st.reset(0)
+                fusion.run(st, layer_passes)
+                shots = st.sample_outcomes(1000, k)
+            dt_w = time.perf_counter() - t0
+            e2e["circuit_workflow"] = {
+                "value": reps * n / dt_w, "unit": UNIT, "steps": reps, "d2h_bytes_per_step": shots.nbytes,
+                "timing": "host wall clock: State.reset + the H layer as fused passes + 1000 exact shots "
+                          "(sample_outcomes, int64 outcomes to the host) per step"}
+            del _Nw
+        except Exception as exc:  # noqa: BLE001
+            e2e["circuit_workflow"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
