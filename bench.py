@@ -344,8 +344,6 @@ def run_ours(args):
         # outcomes read back — reported beside e2e, which moves the whole
         # 8 GiB register both ways every step
         try:
-            from paper_1805_00988_b200 import _native as _Nw
-
             st.reset(0)
             fusion.run(st, layer_passes)
             st.sample_outcomes(1000, 0)
@@ -361,7 +359,6 @@ def run_ours(args):
                 "value": reps * n / dt_w, "unit": UNIT, "steps": reps, "d2h_bytes_per_step": shots.nbytes,
                 "timing": "host wall clock: State.reset + the H layer as fused passes + 1000 exact shots "
                           "(sample_outcomes, int64 outcomes to the host) per step"}
-            del _Nw
         except Exception as exc:  # noqa: BLE001
             e2e["circuit_workflow"] = {"error": f"{type(exc).__name__}: {exc}"}
 
