@@ -69,4 +69,22 @@ if part in ("all", "peer"):
         vs.cx(n - 1, 0)
         vs.amplitudes()
         vs.close()
+if part in ("all", "multidev"):
+    from paper_1805_00988_b200 import build_qft
+    from paper_1805_00988_b200.multigpu import MultiDeviceState
+    from paper_1805_00988_b200.sharded import ShardedState
+
+    for peer in (False, True):
+        with MultiDeviceState(n, [0, 0, 0, 0], peer_gates=peer) as md:
+            for q in range(n):
+                md.h(q)
+            md.cx(n - 1, 0)
+            md.run(build_qft(n), fuse=True)
+            md.sample_outcomes(1000, 1)
+            md.probabilities()
+    vs = ShardedState.virtual(n, 2, peer_gates=True, exchange="peer", precision="double")
+    for q in range(n):
+        vs.h(q)
+    vs.amplitudes()
+    vs.close()
 print("sanitize driver done:", part)
