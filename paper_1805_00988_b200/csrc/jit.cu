@@ -570,6 +570,7 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
 // caller asks for it (QSB_FUSED_JIT=2, qs_jit_sync).
 struct Job;
 bool compile_nvrtc(Job &job);
+const char *const kNvrtcOpts[4] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DQSB_JIT=1"};
 
 struct Job {
     int device = 0;
@@ -616,7 +617,7 @@ std::string cache_path(const std::string &src) {
         return "";
     }
     uint64_t hsh = 1469598103934665603ull;  // FNV-1a over the source + the target
-    for (unsigned char c : src + "|sm_100a|v1") hsh = (hsh ^ c) * 1099511628211ull;
+    for (unsigned char c : src) hsh = (hsh ^ c) * 1099511628211ull;
     char name[40];
     std::snprintf(name, sizeof name, "/%016llx.bin", (unsigned long long)hsh);
     return dir + name;
@@ -665,14 +666,15 @@ void cache_store(const std::string &path, const std::string &src, const std::vec
 }
 
 // the cache key: the generated source plus the device headers it includes
-// (a rebuilt library with changed headers must not load stale programs)
+// and the NVRTC options (a rebuilt library with changed headers or options
+// must not load stale programs)
 std::string cache_key(const std::string &src) {
     static const std::string tag = [] {
         uint64_t h = 1469598103934665603ull;
-        for (const char *t : {kJitCommon, kJitFusedDev})
+        for (const char *t : {kJitCommon, kJitFusedDev, kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3]})
             for (const char *c = t; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;
         char b[40];
-        std::snprintf(b, sizeof b, "\n// headers %016llx\n", (unsigned long long)h);
+        std::snprintf(b, sizeof b, "\n// headers+options %016llx\n", (unsigned long long)h);
         return std::string(b);
     }();
     return src + tag;
@@ -706,7 +708,7 @@ bool compile_nvrtc(Job &job) {
         job.err = "nvrtcCreateProgram failed";
         return false;
     }
-    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DQSB_JIT=1"};
+    const char *opts[] = {kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3]};
     if (nv.compile(prog, 4, opts) != 0) {
         size_t n = 0;
         nv.log_size(prog, &n);
