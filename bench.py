@@ -730,6 +730,9 @@ def run_single_process(n, world, rank):
                 md.close()
             if world >= 4:  # config 5 through the single-process C ABI
                 out["config5_hlayer_qft36"] = _config5_single_process(world)
+            from paper_1805_00988_b200 import _native as N
+
+            N.lib().qs_release_cached(-1)  # hand the other ranks' devices their memory back
         except Exception as exc:  # noqa: BLE001
             out = {"error": f"{type(exc).__name__}: {exc}"}
     dist.barrier()
