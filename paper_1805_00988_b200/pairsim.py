@@ -120,9 +120,12 @@ def _device() -> int:
 class _Mirror(np.ndarray):
     """Host copy of a register handed out as `StateVector.amps`.  Every write
     through it — item / slice assignment, in-place operators and ufuncs with
-    `out=`, ndarray's mutating methods, np.copyto / np.put / np.place /
-    np.putmask — marks it dirty (views share the flag), so the next device
-    operation uploads it; an untouched mirror is not re-uploaded."""
+    `out=`, numpy functions with `out=`, ndarray's mutating methods,
+    np.copyto / np.put / np.place / np.putmask — marks it dirty (views share
+    the flag), so the next device operation uploads it; an untouched mirror
+    is not re-uploaded.  (Writes through a plain-ndarray view of it, e.g.
+    `amps.view(np.ndarray)`, or through raw pointers are not seen: assign
+    `state.amps = array` after such edits.)"""
 
     _MUTATORS = ("fill", "put", "sort", "partition", "resize", "setfield", "byteswap")
 
@@ -153,6 +156,10 @@ class _Mirror(np.ndarray):
         if func in (np.copyto, np.put, np.place, np.putmask, np.fill_diagonal) and args and \
                 isinstance(args[0], _Mirror):
             args[0]._touch()
+        out = kwargs.get("out")  # np.dot(..., out=amps), np.matmul(..., out=amps), ...
+        for o in (out if isinstance(out, tuple) else (out,)):
+            if isinstance(o, _Mirror):
+                o._touch()
         return super().__array_function__(func, types, args, kwargs)
 
     def __reduce__(self):  # pickles as a plain array
