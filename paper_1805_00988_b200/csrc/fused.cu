@@ -286,13 +286,18 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         std::vector<int> rb;    // register f-bits
         int begin, end, first;  // op range; first pair op with a register target
     };
+    // An LDS/STS.128 quarter-warp (lanes 0..7) is bank-conflict-free iff the
+    // 8 padded unit addresses differ mod 8.  With 33-unit padded rows, f-bit
+    // i adds 1, 2, 4 mod 8 for i = 0, 1, 2 and for i = 5, 6, 7 (the row
+    // strides 33, 66, 132) and 0 mod 8 otherwise: lanes 0..2 must take one
+    // f-bit from each class {0,5}, {1,6}, {2,7} (8 conflict-free triples).
     auto triple_ok = [&](const std::vector<int> &rb) {
-        bool low_free = true, high_free = FB > 7;
-        for (int f : rb) {
-            if (f <= 2) low_free = false;
-            if (f >= 5 && f <= 7) high_free = false;
+        for (int c = 0; c < 3; ++c) {
+            const bool lo_free = std::find(rb.begin(), rb.end(), c) == rb.end();
+            const bool hi_free = FB > c + 5 && std::find(rb.begin(), rb.end(), c + 5) == rb.end();
+            if (!lo_free && !hi_free) return false;
         }
-        return low_free || high_free;
+        return true;
     };
     auto fits = [&](const std::vector<int> &rb, int f) {
         if (std::find(rb.begin(), rb.end(), f) != rb.end()) return true;
@@ -393,20 +398,16 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         std::memset(&st, 0, sizeof st);
         for (int r = 0; r < RB; ++r) st.rf[r] = pl.rb[r];
         {
-            // lanes 0..2 must vary f0..f2 or f5..f7 (bank-conflict-free on the
-            // padded layout): a triple free of register bits, the one the
-            // stage's ops test less when both are
-            const int tri_lo[3] = {0, 1, 2}, tri_hi[3] = {5, 6, 7};
+            // lanes 0..2: one f-bit of each class {0,5}, {1,6}, {2,7} (bank-
+            // conflict-free, triple_ok), the one the stage's ops test less
+            // when both are free of register bits
             bool used[32] = {false};
             for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
-            const bool lo_free = !used[0] && !used[1] && !used[2];
-            const bool hi_free = FB > 7 && !used[5] && !used[6] && !used[7];
-            const int *first3 = tri_lo;
-            if (!lo_free || (hi_free && uses[5] + uses[6] + uses[7] < uses[0] + uses[1] + uses[2]))
-                first3 = tri_hi;
-            for (int l = 0; l < 3; ++l) {
-                st.lf[l] = first3[l];
-                used[first3[l]] = true;
+            for (int c = 0; c < 3; ++c) {
+                const bool lo_free = !used[c], hi_free = FB > c + 5 && !used[c + 5];
+                const int f = (!lo_free || (hi_free && uses[c + 5] < uses[c])) ? c + 5 : c;
+                st.lf[c] = f;
+                used[f] = true;
             }
             std::vector<int> fr;
             for (int f = 0; f < FB; ++f)

@@ -189,7 +189,7 @@ def _order_for_stages(pops, tile) -> list:
     """Reorder a reordered pass's ops (DAG order kept: ops sharing a qubit
     stay in order) so that the kernel's stage planner (csrc/fused.cu
     plan_pass: a stage holds its pair targets in RB register bits and
-    leaves one of the f-bit triples {0,1,2} / {5,6,7} to the lanes) needs as
+    leaves one f-bit of each class {0,5} / {1,6} / {2,7} to the lanes) needs as
     few stages as possible: every stage is a shared-memory round trip of
     the whole tile (~3 ms per extra stage at 32 qubits).  Greedy: absorb
     every ready op whose target bit is in the current register set; grow the
@@ -208,8 +208,10 @@ def _order_for_stages(pops, tile) -> list:
         lb = local.get(t)
         return None if lb is None or lb == 0 else lb - 1
 
-    def triple_ok(rs):
-        return not (rs & {0, 1, 2}) or (len(tile) - 1 > 7 and not (rs & {5, 6, 7}))
+    nf = len(tile) - 1
+
+    def triple_ok(rs):  # one free f-bit in each class {0,5}, {1,6}, {2,7} (csrc/fused.cu)
+        return all(c not in rs or (c + 5 < nf and c + 5 not in rs) for c in range(3))
 
     masks = [_qubits(op) for op in pops]
     preds = [0] * m
