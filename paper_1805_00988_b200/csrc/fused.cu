@@ -165,13 +165,13 @@ int gate_class(const float m[8]) {
 }
 
 // Register layouts (f = local bit - 1; f has K-1 bits; RB register bits).
-// An LDS/STS.128 phase serves 8 lanes; with the padded address f + (f >> 5)
-// those 8 lanes hit 8 distinct bank quads iff lanes 0..2 vary f0..f2 (same
-// padded row) or f5..f7 (distinct padding offsets); lanes 3 and 4 are free.
-//   LOW : regs f0..f(RB-1), lanes (f5, f6, f7, two free bits), warps = the rest
-//   HIGH: regs = RB chosen f-bits >= RB, lanes (f0, f1, f2, two free bits),
-//         warps = the rest
-// (run_fused picks the two free lane bits per stage.)
+// An LDS/STS.128 phase serves 8 lanes; in the padded tile (33-unit rows) f-bit
+// i moves the unit address by 1, 2, 4 mod 8 for i = 0, 1, 2 and for i = 5,
+// 6, 7 (row strides 33, 66, 132) and by 0 mod 8 otherwise, so the 8 lanes hit
+// 8 distinct bank quads iff lanes 0..2 take one f-bit of each class {0,5},
+// {1,6}, {2,7}; lanes 3 and 4 are free.  Per stage plan_pass picks RB
+// register bits (the stage's targets, then its most-tested bits), lanes 0..2
+// from the classes, lanes 3-4 the least-tested free bits, warps the rest.
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
 // link dependency, so the library still loads on a GPU-less build host).
