@@ -176,7 +176,10 @@ __device__ __forceinline__ double binade_lo(double g) {
     return __longlong_as_double((long long)(E << 52));
 }
 
-enum : int { kFlagOk = 1, kFlagExact0 = 2, kFlagWalked = 4 };
+enum : int { kFlagOk = 1, kFlagExact0 = 2, kFlagWalked = 4, kFlagFineAbs = 8 };
+// kFlagWalked: the chunk was re-summed sequentially (binade crossing);
+// kFlagFineAbs: its fine starts (fine0) hold the exact running values
+// themselves (recorded by that walk), not trajectory offsets
 // Fine starts: M3 also keeps both trajectories (minus their guesses) at every
 // 256th amplitude of a 4096-amplitude chunk, so a draw can start its exact
 // walk at the last of the chunk's 16 sub-blocks whose running value is still
@@ -374,15 +377,49 @@ __global__ void __launch_bounds__(kMapBlock)
     }
 }
 
+// One warp re-sums a chunk exactly (a binade crossing): the lanes load and
+// square its amplitudes into shared memory (coalesced, in parallel — each
+// |a|^2 is one rounding either way), lane 0 adds them in order (the
+// sequential cumsum) and keeps the exact running value every 2^kFineLog
+// amplitudes as the chunk's fine starts, so draws landing in it walk at most
+// 2^kFineLog amplitudes.  Returns the end value in every lane.
+template <class A>
+__device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, int clog, double s, double *sp,
+                                  double *fine_abs) {
+    const int lane = threadIdx.x & 31;
+    const int C = 1 << clog;
+    const A *p = amps + ((uint64_t)chunk << clog);
+    for (int j = lane; j < C; j += 32) sp[j] = prob(p[j]);
+    __syncwarp();
+    if (lane == 0) {
+        for (int j = 0; j < C; j += 8) {
+            double pr[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pr[q] = j + q < C ? sp[j + q] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (j + q < C) {
+                    if (fine_abs && ((j + q) & ((1 << kFineLog) - 1)) == 0) fine_abs[(j + q) >> kFineLog] = s;
+                    s = __dadd_rn(s, pr[q]);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, s, 0);
+}
+
 template <class A>
 __global__ void __launch_bounds__(32)
     k_block_walk(const A *__restrict__ amps, uint64_t nch, int clog, double s_start,
                  const double *__restrict__ g0, const double *__restrict__ d0, const double *__restrict__ d1,
                  const double *__restrict__ hi, int *__restrict__ flags,
                  const long long *__restrict__ bmap, uint64_t nblk, double *__restrict__ sblock,
-                 double *__restrict__ start, double *__restrict__ total, unsigned long long *__restrict__ nslow) {
+                 double *__restrict__ start, double *__restrict__ total, unsigned long long *__restrict__ nslow,
+                 double *__restrict__ fine0, double *__restrict__ fine1) {
     __shared__ double sd0[kMapBlock], sd1[kMapBlock], shi[kMapBlock], slo[kMapBlock];
     __shared__ int sfl[kMapBlock];
+    __shared__ double sprob[1 << kChunkLog];
     const int lane = threadIdx.x;
     double s = s_start;  // identical in every lane
     unsigned long long slow = 0;
@@ -421,12 +458,12 @@ __global__ void __launch_bounds__(32)
                 sfl[j] = flags[k0 + j];
             }
             __syncwarp();
-            if (lane == 0) {
-                for (int j = 0; j < m; ++j) {
+            for (int j = 0; j < m; ++j) {  // warp-uniform: lane 0 decides, the warp walks
+                double en = 0.0;
+                int valid = 0;
+                if (lane == 0) {
                     start[k0 + j] = s;
                     const int f = sfl[j];
-                    double en;
-                    bool valid;
                     if (f & kFlagExact0) {
                         valid = (s == s_start);
                         en = sd0[j];
@@ -436,13 +473,18 @@ __global__ void __launch_bounds__(32)
                         const double h = shi[j];
                         valid = (f & kFlagOk) && s >= slo[j] && s < h && en < h;
                     }
-                    if (!valid) {
-                        en = walk_chunk(amps, k0 + j, clog, s);
-                        ++slow;
-                        flags[k0 + j] = f | kFlagWalked;  // no fine starts for this chunk
-                    }
-                    s = en;
                 }
+                valid = __shfl_sync(0xffffffffu, valid, 0);
+                if (!valid) {
+                    const bool record = fine0 && clog == kChunkLog;
+                    en = warp_walk_chunk(amps, k0 + j, clog, s, sprob, record ? fine0 + (k0 + j) * kFinePer : nullptr);
+                    if (lane == 0) {
+                        ++slow;
+                        flags[k0 + j] = sfl[j] | kFlagWalked | (record ? kFlagFineAbs : 0);
+                    }
+                    __syncwarp();
+                }
+                s = __shfl_sync(0xffffffffu, en, 0);
             }
             __syncwarp();
             s = __shfl_sync(0xffffffffu, s, 0);
@@ -549,7 +591,18 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
             uint64_t j = 0, hit = C;
             if (fine0 && clog == kChunkLog) {
                 const int f = flags[lo];
-                if ((f & kFlagOk) && !(f & (kFlagExact0 | kFlagWalked))) {
+                if (f & kFlagFineAbs) {
+                    // a walked chunk: exact running values before amplitude 256 q
+                    const double *fa = fine0 + lo * kFinePer;
+                    int sb = 0;
+                    for (int q = 1; q < kFinePer; ++q) {
+                        const double v = fa[q];
+                        if (v >= thr && __ddiv_rn(v, t) > u) break;
+                        sb = q;
+                    }
+                    j = (uint64_t)sb << kFineLog;
+                    s = fa[sb];
+                } else if ((f & kFlagOk) && !(f & (kFlagExact0 | kFlagWalked))) {
                     // exact running values after 256, 512, ... amplitudes: the
                     // chunk start plus the trajectory of its parity (M3, M4)
                     const double *fd = ((__double_as_longlong(s) & 1ll) ? fine1 : fine0) + lo * kFinePer;
@@ -786,7 +839,7 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
     k_block_maps<<<(unsigned)c.nblk, kMapBlock, 0, s->stream>>>(c.nch, c.g0, c.d0, c.d1, c.flags, c.pmap,
                                                                  c.bmap);
     k_block_walk<<<1, 32, 0, s->stream>>>(amps, c.nch, c.clog, s_start, c.g0, c.d0, c.d1, c.hi, c.flags,
-                                          c.bmap, c.nblk, c.sblock, c.start, c.end, c.nslow);
+                                          c.bmap, c.nblk, c.sblock, c.start, c.end, c.nslow, c.fine0, c.fine1);
     k_block_fill<<<(unsigned)c.nblk, kMapBlock, 0, s->stream>>>(c.nch, c.sblock, c.pmap, c.start);
     QS_CUDA(cudaGetLastError());
     return QS_OK;
