@@ -223,6 +223,9 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
         g1 = start;
     }
     double t0 = g0, t1 = g1;
+    // an exact0 chunk's running values ARE the CDF (its true start is
+    // `start`): record them absolutely (kFlagFineAbs), position 0 included
+    if (fine0 && active && exact0) fine0[my * kFinePer] = g0;
     const int rows = (int)((nch - first) < 32 ? (nch - first) : 32);
     for (uint64_t j0 = 0; j0 < C; j0 += 32) {
         const int width = (int)((C - j0) < 32 ? (C - j0) : 32);
@@ -240,8 +243,12 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
             }
             const uint64_t pos = j0 + 32;  // elements summed so far
             if (fine0 && (pos & ((1u << kFineLog) - 1)) == 0 && pos < C) {
-                fine0[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t0, g0);  // exact while in the binade
-                fine1[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t1, g1);
+                if (exact0) {
+                    fine0[my * kFinePer + (pos >> kFineLog)] = t0;
+                } else {
+                    fine0[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t0, g0);  // exact while in the binade
+                    fine1[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t1, g1);
+                }
             }
         }
         __syncwarp();
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
         d0[my] = t0;  // exact end when the true start is 0
         d1[my] = t0;
         hiout[my] = 0.0;
-        flags[my] = kFlagExact0;
+        flags[my] = kFlagExact0 | (fine0 ? kFlagFineAbs : 0);
     } else {
         d0[my] = __dsub_rn(t0, g0);  // exact: same grid, same binade
         d1[my] = __dsub_rn(t1, g1);
@@ -338,6 +345,22 @@ __global__ void __launch_bounds__(kMapBlock)
             m.a0 = __double_as_longlong(__dadd_rn(g, d0[k])) - gb;
             m.a1 = __double_as_longlong(__dadd_rn(__longlong_as_double(gb + 1), d1[k])) - (gb + 1);
         }
+    }
+    // a block of exact0 chunks (every earlier probability zero: only its last
+    // chunk can hold a nonzero sum): every chunk starts at the carried-in
+    // start, the block ends at the last chunk's exact end (bmap kind 2)
+    if (__syncthreads_and(!in || (flags[k] & kFlagExact0))) {
+        if (in) {
+            pmap[2 * k] = 0;
+            pmap[2 * k + 1] = 0;
+        }
+        const uint64_t last = (blockIdx.x + 1) * (uint64_t)kMapBlock < nch ? (blockIdx.x + 1) * (uint64_t)kMapBlock - 1
+                                                                        : nch - 1;
+        if (k == last) {
+            bmap[4 * blockIdx.x + 0] = __double_as_longlong(d0[k]);
+            bmap[4 * blockIdx.x + 3] = 2;
+        }
+        return;
     }
     if (threadIdx.x == 0) sE = E;
     __syncthreads();
@@ -441,7 +464,12 @@ __global__ void __launch_bounds__(32)
             const uint64_t b = b0 + i;
             const long long sb = __double_as_longlong(s);
             const long long eb = sb + ((sb & 1) ? f1 : f0);
-            if (r && (sb >> 52) == e && (eb >> 52) == e) {  // start and end inside the block's binade
+            if (r == 2 && s == s_start) {  // exact0 block: its chunks start at s_start
+                if (lane == 0) sblock[b] = s;
+                s = __longlong_as_double(f0);
+                continue;
+            }
+            if (r == 1 && (sb >> 52) == e && (eb >> 52) == e) {  // start and end inside the block's binade
                 if (lane == 0) sblock[b] = s;
                 s = __longlong_as_double(eb);
                 continue;
