@@ -229,10 +229,16 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
     const int rows = (int)((nch - first) < 32 ? (nch - first) : 32);
     for (uint64_t j0 = 0; j0 < C; j0 += 32) {
         const int width = (int)((C - j0) < 32 ? (C - j0) : 32);
-        for (int r = 0; r < rows; ++r) {
-            double v = 0.0;
-            if (lane < width) v = prob(amps[((first + r) << clog) + j0 + lane]);
-            tile[w][r][lane] = v;
+        // eight rows' loads in flight before their squares are stored (a
+        // load-then-store per row waited a full memory latency per row)
+        for (int r0 = 0; r0 < rows; r0 += 8) {
+            A a[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (r0 + q < rows && lane < width) a[q] = amps[((first + r0 + q) << clog) + j0 + lane];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (r0 + q < rows) tile[w][r0 + q][lane] = lane < width ? prob(a[q]) : 0.0;
         }
         __syncwarp();
         if (active) {
