@@ -1040,7 +1040,7 @@ def run_extras(st, stream, n, cpu=True, harness=True):
                 st.h(q)
         elif kind == "basis":
             st.reset(123456789)
-        st.sample_outcomes(1000, 1)
+        st.sample_outcomes(1_000_000, 1)  # warm: scratch and pinned result buffers sized for 10^6 draws
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)

@@ -16,7 +16,7 @@ for kind in ("generic", "uniform", "basis"):
             st.h(q)
         if kind == "generic":
             st.t(3); st.cx(3, 29); st.h(2)
-    st.sample_outcomes(1000, 1)
+    st.sample_outcomes(1_000_000, 1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s); st.sample_outcomes(1_000_000, 2); b.record(s); st.flush()
     out[kind] = round(a.elapsed_time(b), 3)
