@@ -492,33 +492,43 @@ __global__ void __launch_bounds__(32)
                 sfl[j] = flags[k0 + j];
             }
             __syncwarp();
-            for (int j = 0; j < m; ++j) {  // warp-uniform: lane 0 decides, the warp walks
-                double en = 0.0;
-                int valid = 0;
+            // lane 0 runs through the valid chunks alone; the warp joins only
+            // for a chunk that must be re-summed (a binade crossing)
+            for (int j = 0; j < m;) {
+                int bad = m;
                 if (lane == 0) {
-                    start[k0 + j] = s;
-                    const int f = sfl[j];
-                    if (f & kFlagExact0) {
-                        valid = (s == s_start);
-                        en = sd0[j];
-                    } else {
-                        const bool odd = (__double_as_longlong(s) & 1ll) != 0;
-                        en = __dadd_rn(s, odd ? sd1[j] : sd0[j]);
-                        const double h = shi[j];
-                        valid = (f & kFlagOk) && s >= slo[j] && s < h && en < h;
+                    for (; j < m; ++j) {
+                        start[k0 + j] = s;
+                        const int f = sfl[j];
+                        double en;
+                        bool valid;
+                        if (f & kFlagExact0) {
+                            valid = (s == s_start);
+                            en = sd0[j];
+                        } else {
+                            const bool odd = (__double_as_longlong(s) & 1ll) != 0;
+                            en = __dadd_rn(s, odd ? sd1[j] : sd0[j]);
+                            const double h = shi[j];
+                            valid = (f & kFlagOk) && s >= slo[j] && s < h && en < h;
+                        }
+                        if (!valid) {
+                            bad = j;
+                            break;
+                        }
+                        s = en;
                     }
                 }
-                valid = __shfl_sync(0xffffffffu, valid, 0);
-                if (!valid) {
-                    const bool record = fine0 && clog == kChunkLog;
-                    en = warp_walk_chunk(amps, k0 + j, clog, s, sprob, record ? fine0 + (k0 + j) * kFinePer : nullptr);
-                    if (lane == 0) {
-                        ++slow;
-                        flags[k0 + j] = sfl[j] | kFlagWalked | (record ? kFlagFineAbs : 0);
-                    }
-                    __syncwarp();
+                bad = __shfl_sync(0xffffffffu, bad, 0);
+                s = __shfl_sync(0xffffffffu, s, 0);
+                if (bad >= m) break;
+                const bool record = fine0 && clog == kChunkLog;
+                s = warp_walk_chunk(amps, k0 + bad, clog, s, sprob, record ? fine0 + (k0 + bad) * kFinePer : nullptr);
+                if (lane == 0) {
+                    ++slow;
+                    flags[k0 + bad] = sfl[bad] | kFlagWalked | (record ? kFlagFineAbs : 0);
                 }
-                s = __shfl_sync(0xffffffffu, en, 0);
+                __syncwarp();
+                j = bad + 1;
             }
             __syncwarp();
             s = __shfl_sync(0xffffffffu, s, 0);
