@@ -420,22 +420,74 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
     const A *p = amps + ((uint64_t)chunk << clog);
     for (int j = lane; j < C; j += 32) sp[j] = prob(p[j]);
     __syncwarp();
-    if (lane == 0) {
-        for (int j = 0; j < C; j += 8) {
-            double pr[8];
+    constexpr int S = 1 << kFineLog;  // sub-block: the fine-start spacing
+    const int nsb = C / S;
+    double res = s;
+    if (nsb < 2) {  // short chunk: plain sequential sum
+        if (lane == 0) {
+            if (fine_abs) fine_abs[0] = res;
+            for (int j = 0; j < C; ++j) res = __dadd_rn(res, sp[j]);
+        }
+        __syncwarp();
+        return __shfl_sync(0xffffffffu, res, 0);
+    }
+    // The M3/M4 argument one level down: sub-block L's sequential sum from an
+    // even / odd start g0, g1 = g0 + ulp near its guessed start (the chunk
+    // start plus a plain sum of the earlier sub-blocks) is, while both
+    // trajectories stay in g0's binade, the true sum's offset for a true
+    // start of that parity in that binade; lane 0 then chains the sub-blocks
+    // exactly and re-sums in order only those that leave their binade.
+    const double *q = sp + (lane < nsb ? lane : 0) * S;
+    double bs = 0.0;  // this sub-block's plain sum (for the guess only)
+    if (lane < nsb)
+        for (int j = 0; j < S; ++j) bs += q[j];
+    double pre = bs;  // inclusive warp scan -> exclusive prefix (guess)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) pr[q] = j + q < C ? sp[j + q] : 0.0;
+    for (int o = 1; o < 32; o <<= 1) {
+        const double x = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += x;
+    }
+    pre -= bs;
+    double g0 = 0.0, d0 = 0.0, d1 = 0.0, hi = 0.0;
+    int ok = 0;
+    if (lane < nsb) {
+        const double gg = __dadd_rn(s, pre);
+        g0 = __longlong_as_double(__double_as_longlong(gg) & ~1ll);
+        const double g1 = __longlong_as_double(__double_as_longlong(g0) + 1ll);
+        hi = binade_hi(g0);
+        double t0 = g0, t1 = g1;
+        for (int j = 0; j < S; ++j) {
+            t0 = __dadd_rn(t0, q[j]);
+            t1 = __dadd_rn(t1, q[j]);
+        }
+        d0 = __dsub_rn(t0, g0);
+        d1 = __dsub_rn(t1, g1);
+        ok = t0 < hi && t1 < hi;
+    }
+    for (int L = 0; L < nsb; ++L) {
+        const double lg0 = __shfl_sync(0xffffffffu, g0, L), ld0 = __shfl_sync(0xffffffffu, d0, L);
+        const double ld1 = __shfl_sync(0xffffffffu, d1, L), lhi = __shfl_sync(0xffffffffu, hi, L);
+        const int lok = __shfl_sync(0xffffffffu, ok, L);
+        if (lane == 0) {
+            if (fine_abs) fine_abs[L] = res;
+            const bool odd = (__double_as_longlong(res) & 1ll) != 0;
+            const double en = __dadd_rn(res, odd ? ld1 : ld0);
+            if (lok && res >= binade_lo(lg0) && res < lhi && en < lhi) {
+                res = en;
+            } else {  // the sub-block leaves its binade (or the guess missed): sum it in order
+                const double *r = sp + L * S;
+                for (int j = 0; j < S; j += 8) {
+                    double pr[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (j + q < C) {
-                    if (fine_abs && ((j + q) & ((1 << kFineLog) - 1)) == 0) fine_abs[(j + q) >> kFineLog] = s;
-                    s = __dadd_rn(s, pr[q]);
+                    for (int u = 0; u < 8; ++u) pr[u] = r[j + u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) res = __dadd_rn(res, pr[u]);
                 }
             }
         }
     }
     __syncwarp();
-    return __shfl_sync(0xffffffffu, s, 0);
+    return __shfl_sync(0xffffffffu, res, 0);
 }
 
 template <class A>
