@@ -61,6 +61,12 @@ def device_equal(a: torch.Tensor, b: torch.Tensor, chunk: int = 1 << 28) -> bool
     return True
 
 
+def load(n: int, amps) -> State:
+    st = State(n)
+    st.set_amplitudes(amps)
+    return st
+
+
 def free_gib() -> float:
     return torch.cuda.mem_get_info()[0] / 2**30
 
@@ -400,3 +406,35 @@ class TestCheckpoint:
         assert np.load(path).tobytes() == st.amplitudes().tobytes()
         st.close()
         back.close()
+
+
+class TestSamplingChainPaths:
+    """Per-draw parity of the exact sampling chain on states that force each
+    of its paths at 2^22 amplitudes (4 blocks of 256 chunks): binade
+    crossings inside chunks and sub-blocks (log-uniform magnitudes), an
+    all-zero prefix (all-exact0 blocks), a basis state (exact0 chunk with
+    absolute fine starts), a uniform state (30 crossings)."""
+
+    @pytest.mark.parametrize("kind", ["loguniform", "zero_prefix", "basis", "uniform", "spiky"])
+    def test_per_draw_vs_oracle(self, kind):
+        n = 22
+        rng = np.random.default_rng(hash(kind) % 1000)
+        if kind == "loguniform":
+            mag = np.exp(rng.uniform(np.log(1e-30), 0.0, size=1 << n))
+            amps = (mag * np.exp(2j * np.pi * rng.random(1 << n))).astype(np.complex64)
+        elif kind == "zero_prefix":
+            amps = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)).astype(np.complex64)
+            amps[: (3 << n) // 4] = 0
+        elif kind == "basis":
+            amps = np.zeros(1 << n, np.complex64)
+            amps[3_000_001] = 1
+        elif kind == "uniform":
+            amps = np.full(1 << n, np.float32(2.0 ** (-n / 2)), np.complex64)
+        else:  # a few large spikes on a tiny floor
+            amps = np.full(1 << n, np.float32(1e-20), np.complex64)
+            amps[rng.integers(0, 1 << n, 40)] = rng.normal(size=40).astype(np.float32)
+        st = load(n, amps)
+        for seed in (1, 77):
+            got = st.sample_outcomes(20000, seed)
+            assert np.array_equal(got, oc.sample_outcomes(amps, 20000, seed)), (kind, seed)
+        st.close()
