@@ -21,7 +21,7 @@
 //
 // Pipeline (C = 4096 amplitudes per chunk):
 //   M1 k_chunk_sums   parallel fp64 chunk sums (any order: guesses only)
-//   M2 k_scan_guess   exclusive scan of the sums -> guessed chunk starts
+//   M2 scan_guess     two-level exclusive scan of the sums -> guessed chunk starts
 //   M3 k_trajectories both guessed trajectories per chunk (warp-transposed
 //                     through shared memory so HBM reads stay coalesced)
 //   M4 true chunk starts: the parity of s's mantissa selects the
@@ -136,30 +136,105 @@ __global__ void __launch_bounds__(256) k_chunk_sums_f4(const float4 *__restrict_
     if (threadIdx.x == 0) csum[blockIdx.x] = acc;
 }
 
-// ---- M2: exclusive scan of chunk sums (single block) -------------------------
-__global__ void k_scan_guess(const double *__restrict__ csum, uint64_t nch, double *__restrict__ g) {
-    __shared__ double part[1024];
-    const uint64_t per = (nch + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = threadIdx.x * per;
-    const uint64_t hi = lo + per < nch ? lo + per : nch;
+// ---- M2: exclusive scan of chunk sums -> guessed chunk starts ----------------
+// Only a GUESS of every chunk's start is needed (M3-M5 resolve the exact
+// sequential values), so any summation order will do; a sum of non-negative
+// terms is 0 exactly when every term is 0, which is all M3 relies on.  Two
+// levels: per-segment sums (coalesced), one block scanning the segment sums,
+// then each segment's in-block scan plus its offset.
+constexpr int kScanThreads = 256, kScanPer = 8, kScanSeg = kScanThreads * kScanPer;
+
+__device__ __forceinline__ double block_excl_scan(double v, double *warp_tot, double &total) {
+    const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (unsigned)o) inc += t;
+    }
+    if (lane == 31) warp_tot[w] = inc;
+    __syncthreads();
+    double base = 0.0, all = 0.0;
+    const unsigned nw = blockDim.x >> 5;
+    for (unsigned i = 0; i < nw; ++i) {
+        if (i == w) base = all;
+        all += warp_tot[i];
+    }
+    __syncthreads();
+    total = all;
+    return base + inc - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_seg_sums(const double *__restrict__ csum, uint64_t nch,
+                                                                double *__restrict__ ssum) {
+    __shared__ double wt[kScanThreads / 32];
+    const uint64_t lo = (uint64_t)blockIdx.x * kScanSeg;
     double acc = 0.0;
-    for (uint64_t i = lo; i < hi; ++i) acc += csum[i];
-    part[threadIdx.x] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double run = 0.0;
-        for (unsigned i = 0; i < blockDim.x; ++i) {
-            double t = part[i];
-            part[i] = run;
-            run += t;
-        }
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+        const uint64_t i = lo + (uint64_t)j * kScanThreads + threadIdx.x;
+        if (i < nch) acc += csum[i];
     }
-    __syncthreads();
-    double run = part[threadIdx.x];
+    double total;
+    block_excl_scan(acc, wt, total);
+    if (threadIdx.x == 0) ssum[blockIdx.x] = total;
+}
+
+// one block: in-place exclusive scan of the nseg segment sums
+__global__ void __launch_bounds__(1024) k_scan_seg_top(double *__restrict__ ssum, uint64_t nseg) {
+    __shared__ double wt[32];
+    const uint64_t per = (nseg + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * per;
+    const uint64_t hi = lo + per < nseg ? lo + per : nseg;
+    double acc = 0.0;
+    for (uint64_t i = lo; i < hi; ++i) acc += ssum[i];
+    double total;
+    double run = block_excl_scan(acc, wt, total);
     for (uint64_t i = lo; i < hi; ++i) {
-        g[i] = run;
-        run += csum[i];
+        const double t = ssum[i];
+        ssum[i] = run;
+        run += t;
     }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_seg_apply(const double *__restrict__ csum, uint64_t nch,
+                                                                 const double *__restrict__ soff,
+                                                                 double *__restrict__ g) {
+    __shared__ double tile[kScanSeg];
+    __shared__ double wt[kScanThreads / 32];
+    const uint64_t lo = (uint64_t)blockIdx.x * kScanSeg;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {  // coalesced load, then each thread owns 8 consecutive chunks
+        const uint64_t i = lo + (uint64_t)j * kScanThreads + threadIdx.x;
+        tile[j * kScanThreads + threadIdx.x] = i < nch ? csum[i] : 0.0;
+    }
+    __syncthreads();
+    double v[kScanPer], acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+        v[j] = tile[threadIdx.x * kScanPer + j];
+        acc += v[j];
+    }
+    double total;
+    double run = soff[blockIdx.x] + block_excl_scan(acc, wt, total);
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+        tile[threadIdx.x * kScanPer + j] = run;
+        run += v[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+        const uint64_t i = lo + (uint64_t)j * kScanThreads + threadIdx.x;
+        if (i < nch) g[i] = tile[j * kScanThreads + threadIdx.x];
+    }
+}
+
+static void scan_guess(const double *csum, uint64_t nch, double *seg_tmp, double *g, cudaStream_t st) {
+    const uint64_t nseg = (nch + kScanSeg - 1) / kScanSeg;
+    k_scan_seg_sums<<<(unsigned)nseg, kScanThreads, 0, st>>>(csum, nch, seg_tmp);
+    k_scan_seg_top<<<1, 1024, 0, st>>>(seg_tmp, nseg);
+    k_scan_seg_apply<<<(unsigned)nseg, kScanThreads, 0, st>>>(csum, nch, seg_tmp, g);
 }
 
 // binade helpers on the bit pattern of a non-negative double
@@ -925,7 +1000,7 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
         k_chunk_sums_f4<<<(unsigned)c.nch, 256, 0, s->stream>>>((const float4 *)amps, c.csum);
     else
         k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(amps, c.clog, c.csum);
-    k_scan_guess<<<1, 1024, 0, s->stream>>>(c.csum, c.nch, c.start);  // prefixes -> start[]
+    scan_guess(c.csum, c.nch, c.d0, c.start, s->stream);  // guessed prefixes -> start[] (d0: segment sums)
     {
         const uint64_t warps = (c.nch + 31) / 32;
         const unsigned blocks = (unsigned)((warps + kTrajWarps - 1) / kTrajWarps);
