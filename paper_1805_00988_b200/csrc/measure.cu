@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -343,6 +344,120 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
         flags[my] = kFlagExact0 | (fine0 ? kFlagFineAbs : 0);
     } else {
         d0[my] = __dsub_rn(t0, g0);  // exact: same grid, same binade
+        d1[my] = __dsub_rn(t1, g1);
+        hiout[my] = hi;
+        flags[my] = (t0 < hi && t1 < hi) ? kFlagOk : 0;
+    }
+}
+
+// M3 for complex64 registers of >= 2^17 amplitudes (whole warps of 4096-
+// amplitude chunks): the same trajectories, but each warp streams its 32
+// chunks through a two-stage shared-memory ring with 1-D bulk copies (one
+// 512-B row per lane and stage, completion on an mbarrier), so a row block is
+// in flight while the previous one is summed.  The register-staged form above
+// kept only eight rows of loads in flight per warp and was memory-latency
+// bound (ncu: long_scoreboard 50% of stalls, 2.1 ms at n = 30).
+constexpr int kTbCols = 64;                  // amplitudes per row and stage (512 B)
+constexpr int kTbPitch4 = kTbCols / 2 + 1;   // padded row pitch in float4 (528 B)
+constexpr int kTbStage4 = 32 * kTbPitch4;
+
+__device__ __forceinline__ uint32_t tb_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tb_wait(uint64_t *bar, uint32_t parity) {
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\nselp.u32 %0, 1, 0, P;\n}\n"
+            : "=r"(ok)
+            : "r"(tb_smem(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (spins > (1u << 22)) __trap();
+    }
+}
+// stage the row block `col` (kTbCols amplitudes of each of the warp's 32 chunks)
+__device__ __forceinline__ void tb_issue(const float2 *__restrict__ rows, uint64_t *bar, float4 *stage, int col,
+                                         int lane) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the stage
+    __syncwarp();
+    if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_smem(bar)),
+                     "r"(32u * kTbCols * 8u)
+                     : "memory");
+    __syncwarp();
+    const float2 *src = rows + ((uint64_t)lane << kChunkLog) + (uint64_t)col * kTbCols;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            tb_smem(stage + lane * kTbPitch4)),
+        "l"(src), "r"((uint32_t)(kTbCols * 8)), "r"(tb_smem(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(32)
+    k_trajectories_bulk(const float2 *__restrict__ amps, double start, const double *__restrict__ g,
+                        double *__restrict__ g0out, double *__restrict__ d0, double *__restrict__ d1,
+                        double *__restrict__ hiout, int *__restrict__ flags, double *__restrict__ fine0,
+                        double *__restrict__ fine1) {
+    __shared__ __align__(128) float4 ring[2][kTbStage4];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int lane = threadIdx.x;
+    const uint64_t first = (uint64_t)blockIdx.x * 32;
+    const uint64_t my = first + lane;
+    const float2 *rows = amps + (first << kChunkLog);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    tb_issue(rows, &bar[0], ring[0], 0, lane);
+    tb_issue(rows, &bar[1], ring[1], 1, lane);
+
+    // prologue and epilogue as in k_trajectories
+    const double prefix = g[my];
+    const bool exact0 = (my == 0) || prefix == 0.0;
+    const double gg = __dadd_rn(start, prefix);
+    double g0 = start, g1 = start, hi = 0.0;
+    if (!exact0) {
+        g0 = __longlong_as_double(__double_as_longlong(gg) & ~1ll);
+        g1 = __longlong_as_double(__double_as_longlong(g0) + 1ll);
+        hi = binade_hi(g0);
+    }
+    double t0 = g0, t1 = g1;
+    if (fine0 && exact0) fine0[my * kFinePer] = g0;
+    constexpr int kCols = (1 << kChunkLog) / kTbCols;
+    constexpr int kFineEvery = (1 << kFineLog) / kTbCols;
+    for (int c = 0; c < kCols; ++c) {
+        const int st = c & 1;
+        tb_wait(&bar[st], (uint32_t)(c >> 1) & 1u);
+        const float4 *row = ring[st] + lane * kTbPitch4;
+#pragma unroll 8
+        for (int j = 0; j < kTbCols / 2; ++j) {
+            const float4 q = row[j];
+            const double p0 = prob(make_float2(q.x, q.y)), p1 = prob(make_float2(q.z, q.w));
+            t0 = __dadd_rn(t0, p0);
+            t1 = __dadd_rn(t1, p0);
+            t0 = __dadd_rn(t0, p1);
+            t1 = __dadd_rn(t1, p1);
+        }
+        if (c + 2 < kCols) tb_issue(rows, &bar[st], ring[st], c + 2, lane);
+        if (fine0 && (c + 1) % kFineEvery == 0 && c + 1 < kCols) {
+            const int f = (c + 1) / kFineEvery;
+            if (exact0) {
+                fine0[my * kFinePer + f] = t0;
+            } else {
+                fine0[my * kFinePer + f] = __dsub_rn(t0, g0);  // exact while in the binade
+                fine1[my * kFinePer + f] = __dsub_rn(t1, g1);
+            }
+        }
+    }
+    g0out[my] = g0;
+    if (exact0) {
+        d0[my] = t0;
+        d1[my] = t0;
+        hiout[my] = 0.0;
+        flags[my] = kFlagExact0 | (fine0 ? kFlagFineAbs : 0);
+    } else {
+        d0[my] = __dsub_rn(t0, g0);
         d1[my] = __dsub_rn(t1, g1);
         hiout[my] = hi;
         flags[my] = (t0 < hi && t1 < hi) ? kFlagOk : 0;
@@ -994,6 +1109,14 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
 
 // M1..M4: exact sequential running sum over the register, continuing from
 // `s_start`; leaves chunk starts in c.start and the final value in *c.end.
+static bool traj_regs() {
+    static const bool on = [] {
+        const char *e = std::getenv("QSB_TRAJ_REGS");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
 template <class A>
 static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s_start) {
     if (sizeof(A) == sizeof(float2) && c.clog == kChunkLog)
@@ -1004,8 +1127,17 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
     {
         const uint64_t warps = (c.nch + 31) / 32;
         const unsigned blocks = (unsigned)((warps + kTrajWarps - 1) / kTrajWarps);
-        k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
-            amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
+        bool bulk = false;
+        if constexpr (std::is_same<A, float2>::value)  // QSB_TRAJ_REGS=1: the register-staged form (probes)
+            bulk = c.clog == kChunkLog && c.nch % 32 == 0 && !traj_regs();
+        if constexpr (std::is_same<A, float2>::value) {
+            if (bulk)
+                k_trajectories_bulk<<<(unsigned)(c.nch / 32), 32, 0, s->stream>>>(
+                    amps, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
+        }
+        if (!bulk)
+            k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
+                amps, c.nch, c.clog, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
     }
     k_block_maps<<<(unsigned)c.nblk, kMapBlock, 0, s->stream>>>(c.nch, c.g0, c.d0, c.d1, c.flags, c.pmap,
                                                                  c.bmap);
