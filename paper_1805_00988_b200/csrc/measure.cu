@@ -604,11 +604,37 @@ __global__ void __launch_bounds__(kMapBlock)
 // 2^kFineLog amplitudes.  Returns the end value in every lane.
 template <class A>
 __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, int clog, double s, double *sp,
-                                  double *fine_abs) {
+                                  double *fine_abs, uint64_t *bar, uint32_t &phase) {
     const int lane = threadIdx.x & 31;
     const int C = 1 << clog;
     const A *p = amps + ((uint64_t)chunk << clog);
-    for (int j = lane; j < C; j += 32) sp[j] = prob(p[j]);
+    if (sizeof(A) == sizeof(double) && clog == kChunkLog) {
+        // one 32-KB bulk copy of the chunk into sp (a complex64 amplitude and
+        // its fp64 probability are both 8 B), then each lane squares its own
+        // slots in place: one memory latency instead of C/32 dependent loads
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tb_smem(bar)),
+                         "r"((uint32_t)(C * 8))
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    tb_smem(sp)),
+                "l"(p), "r"((uint32_t)(C * 8)), "r"(tb_smem(bar))
+                : "memory");
+        }
+        tb_wait(bar, phase);
+        phase ^= 1u;
+        const A *raw = reinterpret_cast<const A *>(sp);
+#pragma unroll 8
+        for (int j = lane; j < (1 << kChunkLog); j += 32) {
+            const A a = raw[j];
+            sp[j] = prob(a);
+        }
+    } else {
+        for (int j = lane; j < C; j += 32) sp[j] = prob(p[j]);
+    }
     __syncwarp();
     constexpr int S = 1 << kFineLog;  // sub-block: the fine-start spacing
     const int nsb = C / S;
@@ -690,8 +716,15 @@ __global__ void __launch_bounds__(32)
                  double *__restrict__ fine0, double *__restrict__ fine1) {
     __shared__ double sd0[kMapBlock], sd1[kMapBlock], shi[kMapBlock], slo[kMapBlock];
     __shared__ int sfl[kMapBlock];
-    __shared__ double sprob[1 << kChunkLog];
+    __shared__ __align__(16) double sprob[1 << kChunkLog];
+    __shared__ __align__(8) uint64_t wbar;
+    uint32_t wphase = 0;
     const int lane = threadIdx.x;
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&wbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     double s = s_start;  // identical in every lane
     unsigned long long slow = 0;
     for (uint64_t b0 = 0; b0 < nblk; b0 += 32) {
@@ -739,19 +772,31 @@ __global__ void __launch_bounds__(32)
             for (int j = 0; j < m;) {
                 int bad = m;
                 if (lane == 0) {
+                    // software-pipelined: chunk j+1's shared-memory values are
+                    // loaded while chunk j's add / compares (the only work that
+                    // waits for s) run
+                    double na0 = sd0[j], na1 = sd1[j], nh = shi[j], nl = slo[j];
+                    int nf = sfl[j];
                     for (; j < m; ++j) {
+                        const double a0 = na0, a1 = na1, h = nh, l = nl;
+                        const int f = nf;
+                        if (j + 1 < m) {
+                            na0 = sd0[j + 1];
+                            na1 = sd1[j + 1];
+                            nh = shi[j + 1];
+                            nl = slo[j + 1];
+                            nf = sfl[j + 1];
+                        }
                         start[k0 + j] = s;
-                        const int f = sfl[j];
                         double en;
                         bool valid;
                         if (f & kFlagExact0) {
                             valid = (s == s_start);
-                            en = sd0[j];
+                            en = a0;
                         } else {
                             const bool odd = (__double_as_longlong(s) & 1ll) != 0;
-                            en = __dadd_rn(s, odd ? sd1[j] : sd0[j]);
-                            const double h = shi[j];
-                            valid = (f & kFlagOk) && s >= slo[j] && s < h && en < h;
+                            en = __dadd_rn(s, odd ? a1 : a0);
+                            valid = (f & kFlagOk) && s >= l && s < h && en < h;
                         }
                         if (!valid) {
                             bad = j;
@@ -764,7 +809,8 @@ __global__ void __launch_bounds__(32)
                 s = __shfl_sync(0xffffffffu, s, 0);
                 if (bad >= m) break;
                 const bool record = fine0 && clog == kChunkLog;
-                s = warp_walk_chunk(amps, k0 + bad, clog, s, sprob, record ? fine0 + (k0 + bad) * kFinePer : nullptr);
+                s = warp_walk_chunk(amps, k0 + bad, clog, s, sprob, record ? fine0 + (k0 + bad) * kFinePer : nullptr,
+                                    &wbar, wphase);
                 if (lane == 0) {
                     ++slow;
                     flags[k0 + bad] = sfl[bad] | kFlagWalked | (record ? kFlagFineAbs : 0);
@@ -831,6 +877,52 @@ __device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
     return acc_mult * state + acc_plus;
 }
 
+// Smallest non-negative double S with fl(S / t) > u, as the condition the
+// reference's searchsorted applies to each normalised CDF value (measure.py:
+// 80-83: cdf /= total, then the first value > u).  fl(s / t) is monotone in
+// s (t > 0) and the bit patterns of non-negative doubles are ordered like
+// their values, so S is found by galloping from fl(u t) and bisecting bit
+// patterns — a few divisions per draw instead of one per amplitude walked;
+// `fl(s / t) > u` is then exactly `s >= S`.  u < 1, so fl(t / t) = 1 > u
+// bounds the search.
+__device__ double cdf_cut(double u, double t) {
+    const long long top = __double_as_longlong(t);
+    auto pred = [&](long long b) { return __ddiv_rn(__longlong_as_double(b), t) > u; };
+    const double g0 = __dmul_rn(u, t);
+    long long g = g0 > 0.0 ? __double_as_longlong(g0) : 0ll;
+    if (g > top) g = top;
+    long long lo, hi;  // pred(hi) holds; pred(lo) fails (lo = -1: below every s)
+    if (pred(g)) {
+        hi = g;
+        long long step = 1;
+        lo = g - 1;
+        while (lo >= 0 && pred(lo)) {
+            hi = lo;
+            step <<= 1;
+            lo = hi - step;
+        }
+        if (lo < 0) lo = -1;
+    } else {
+        lo = g;
+        long long step = 1;
+        hi = g + 1;
+        while (hi < top && !pred(hi)) {
+            lo = hi;
+            step <<= 1;
+            hi = lo + step;
+        }
+        if (hi > top) hi = top;
+    }
+    while (hi - lo > 1) {
+        const long long mid = lo + (hi - lo) / 2;
+        if (pred(mid))
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return __longlong_as_double(hi);
+}
+
 // ---- M6: draws ---------------------------------------------------------------------
 // Draw i resolves in this register iff fl(s_start / t) <= u (no earlier
 // register holds a value above u) and u < last[nch-1] (or this is the last
@@ -869,8 +961,7 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
             const uint64_t C = 1ull << clog;
             const A *p = amps + (lo << clog);
             double s = start[lo];
-            // s below `thr` cannot satisfy fl(s / t) > u; skip the division there
-            const double thr = __dmul_rn(__dmul_rn(u, t), 1.0 - 0x1p-50);
+            const double cut = cdf_cut(u, t);  // fl(s / t) > u  <=>  s >= cut
             // the same sequential sum, 8 probabilities loaded ahead of the
             // chain (the loads do not depend on s; a one-at-a-time loop
             // waits a memory latency per amplitude)
@@ -883,7 +974,7 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
                     int sb = 0;
                     for (int q = 1; q < kFinePer; ++q) {
                         const double v = fa[q];
-                        if (v >= thr && __ddiv_rn(v, t) > u) break;
+                        if (v >= cut) break;
                         sb = q;
                     }
                     j = (uint64_t)sb << kFineLog;
@@ -896,7 +987,7 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
                     int sb = 0;
                     for (int q = 1; q < kFinePer; ++q) {
                         const double v = __dadd_rn(s, fd[q]);
-                        if (v >= thr && __ddiv_rn(v, t) > u) break;
+                        if (v >= cut) break;
                         sb = q;
                         fs = v;
                     }
@@ -912,13 +1003,13 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
                 for (int q = 0; q < 8; ++q) {
                     if (hit == C) {
                         s = __dadd_rn(s, pr[q]);
-                        if (s >= thr && __ddiv_rn(s, t) > u) hit = j + q;
+                        if (s >= cut) hit = j + q;
                     }
                 }
             }
             for (; j < C && hit == C; ++j) {
                 s = __dadd_rn(s, prob(p[j]));
-                if (s >= thr && __ddiv_rn(s, t) > u) hit = j;
+                if (s >= cut) hit = j;
             }
             idx = (lo << clog) + hit;
         }

@@ -415,7 +415,8 @@ class TestSamplingChainPaths:
     all-zero prefix (all-exact0 blocks), a basis state (exact0 chunk with
     absolute fine starts), a uniform state (30 crossings)."""
 
-    @pytest.mark.parametrize("kind", ["loguniform", "zero_prefix", "basis", "uniform", "spiky"])
+    @pytest.mark.parametrize("kind", ["loguniform", "zero_prefix", "basis", "uniform", "spiky", "scaled_up",
+                                      "scaled_down"])
     def test_per_draw_vs_oracle(self, kind):
         n = 22
         rng = np.random.default_rng(hash(kind) % 1000)
@@ -430,6 +431,9 @@ class TestSamplingChainPaths:
             amps[3_000_001] = 1
         elif kind == "uniform":
             amps = np.full(1 << n, np.float32(2.0 ** (-n / 2)), np.complex64)
+        elif kind in ("scaled_up", "scaled_down"):  # unnormalised: total 2^22 * 1e12 or * 1e-34
+            scale = 1e6 if kind == "scaled_up" else 1e-17
+            amps = ((rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)) * scale).astype(np.complex64)
         else:  # a few large spikes on a tiny floor
             amps = np.full(1 << n, np.float32(1e-20), np.complex64)
             amps[rng.integers(0, 1 << n, 40)] = rng.normal(size=40).astype(np.float32)
