@@ -186,20 +186,44 @@ int encode_tile_map(qs_state *s, FParams &p) {
         encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
     }
     // complex64: 64 amplitudes (8 B) per 512-B row; complex128: 32 (16 B);
-    // either way 64 eight-byte elements per row
+    // either way 64 eight-byte elements per row, padded to 66 in shared
+    // memory (box dim 0 runs 2 elements past the tensor's 64: zero-filled on
+    // load, skipped on store).  Box dims 1-3 take the first three runs of
+    // consecutive qubits among the tile's row bits (<= 8 bits each), so a
+    // tile whose row qubits are one run (every H-layer pass) moves in ONE
+    // copy; the row bits left over are enumerated by copies (ncopies, crow).
     const int low = s->prec == QS_DOUBLE ? 5 : kLow;
     const uint64_t ab = s->prec == QS_DOUBLE ? 16ull : 8ull;
-    const cuuint64_t dims[5] = {64, 2, 2, 2, 1ull << (p.n - low)};
-    const cuuint64_t strides[4] = {ab << p.qpos[low], ab << p.qpos[low + 1], ab << p.qpos[low + 2], 512ull};
-    const cuuint32_t box[5] = {66, 2, 2, 2, 1};
+    cuuint64_t dims[5] = {64, 1, 1, 1, 1ull << (p.n - low)};
+    cuuint64_t strides[4] = {512ull, 512ull, 512ull, 512ull};
+    cuuint32_t box[5] = {66, 1, 1, 1, 1};
+    // QSB_FUSED_RUN_BOXES=0: one row bit per box dim (the round-1 form; probes)
+    static const bool run_boxes = [] {
+        const char *e = std::getenv("QSB_FUSED_RUN_BOXES");
+        return !(e && e[0] == '0');
+    }();
+    int cov = 0;  // row bits covered by box dims 1-3
+    for (int d = 1; d <= 3 && low + cov < p.K; ++d) {
+        const int q0 = p.qpos[low + cov];
+        int len = 1;
+        while (run_boxes && len < 8 && low + cov + len < p.K && p.qpos[low + cov + len] == q0 + len) ++len;
+        dims[d] = 1ull << len;
+        box[d] = 1u << len;
+        strides[d - 1] = ab << q0;
+        cov += len;
+    }
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)s->amps, dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return set_error(QS_ERR_CUDA, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
-    p.ncopies = 1 << (p.K - low - 3);
-    for (int k = 0; k < 4; ++k) p.crow[k] = (low + 3 + k < p.K) ? p.qpos[low + 3 + k] - low : 0;
+    const int left = p.K - low - cov;  // row bits enumerated by copies
+    if (left > 4) return set_error(QS_ERR_VALUE, "tile row bits too fragmented for the copy table");
+    p.ncopies = 1 << left;
+    p.copy_f4 = (1 << cov) * 33;
+    p.box_bytes = (uint32_t)(1u << cov) * 66u * 8u;
+    for (int k = 0; k < 4; ++k) p.crow[k] = (k < left) ? p.qpos[low + cov + k] - low : 0;
     return QS_OK;
 }
 

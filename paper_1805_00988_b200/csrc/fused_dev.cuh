@@ -58,8 +58,10 @@ constexpr int kNB = 3;  // tile buffers in the TMA ring
 constexpr int kMaxStages = 48;
 struct FParams {
     CUtensorMap tmap;  // 64-B aligned, first member
-    int ncopies;       // TMA copies per tile (2^(K-9))
+    int ncopies;       // TMA copies per tile (2^(row bits not in box dims 1-3))
     int crow[4];       // row-index bit of copy-index bit i
+    int copy_f4;       // padded float4 per copy (2^(box row bits) * 33)
+    uint32_t box_bytes;  // bytes one copy moves into shared memory
     int n, K, nwbits, nstages, nruns, nops;
     int dry;    // probes (QSB_FUSED_DRY): 1 skip the ops, 2 also the register stages, 3 also the stores,
                 // 4 no HBM traffic at all (compute only; the register content is garbage)
@@ -322,6 +324,7 @@ __device__ __forceinline__ void apply_run(int variant, const FOp *ops, int len, 
 // Ahead-of-time program: walks the op table staged in shared memory.
 struct Interp {
     static constexpr bool kPlanar = false;
+    static constexpr bool kOwnsStages = false;  // the generic stage loop in fused_body
     template <int RB>
     static __device__ __forceinline__ void run(int, const FStage &st, const FOp *sops, uint32_t tid,
                                                uint64_t base, float, float4 (&v)[1 << RB]) {
@@ -674,8 +677,8 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         // ~0 ends the loop.
         const CUtensorMap *map = &p.tmap;
         const uint64_t pol = l2_evict_first();
-        constexpr int kCopyF4 = 8 * 33;  // one 5-D box: 8 padded segments
-        constexpr uint32_t kBoxBytes = 8u * 66u * 8u;
+        const int kCopyF4 = p.copy_f4;  // one 5-D box: 2^(box row bits) padded segments
+        const uint32_t kBoxBytes = p.box_bytes;
         uint64_t pending[kNB];
         int i = 0;
         for (;; ++i) {
@@ -740,9 +743,9 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
                 uint32_t row = row0;
                 for (int q = 0; q < 4; ++q) row |= (uint32_t)((c >> q) & 1) << p.crow[q];
                 if (p.l2hint)
-                    tma_store_5d_hint(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4, pol);
+                    tma_store_5d_hint(map, (int)row, buf0 + b * kBufF4 + c * p.copy_f4, pol);
                 else
-                    tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * kCopyF4);
+                    tma_store_5d(map, (int)row, buf0 + b * kBufF4 + c * p.copy_f4);
             }
             bulk_commit();
         }
@@ -758,7 +761,14 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         const uint64_t t = tile_id[b];
         if (t == ~0ull) break;
         const uint64_t base = tile_base(t, p);
-        for (int s = 0; s < (p.dry == 2 || p.dry == 3 ? 0 : p.nstages); ++s) {
+        bool staged = false;
+        if constexpr (Prog::kOwnsStages) {  // generated program: literal stage layouts
+            if (p.dry == 0 || p.dry == 4) {
+                Prog::template run_stages<RB, kCompute>(tile, (uint32_t)tid, base, p.one, sops);
+                staged = true;
+            }
+        }
+        for (int s = 0; s < (staged || p.dry == 2 || p.dry == 3 ? 0 : p.nstages); ++s) {
             const FStage &st = p.stages[s];
             uint32_t fb = 0;
 #pragma unroll

@@ -189,6 +189,16 @@ bool unit_turns(const FOp &op, uint32_t *turns) {
     return true;
 }
 
+// QSB_JIT_STATIC_STAGES=0: generated programs use fused_body's generic
+// stage loop (layouts from the parameter block), for measurements
+bool static_stages_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("QSB_JIT_STATIC_STAGES");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 std::string generate(const FParams &p, int K, int RB, bool param = false) {
     // diagonal ops inside a test: 1 (default) scalar phase_cs, 0 packed
     // phase_ct, 2 scalar everywhere (QSB_JIT_PHASE, for measurements)
@@ -488,8 +498,58 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
         }
         src += "    } break;\n";
     }
+    src += "    default: break;\n    }\n  }\n";
+    // The whole stage sequence with the stage layouts as literals: each
+    // thread's padded base per stage is a few shifts of its lane / warp bits
+    // (loop-invariant across tiles) and every register's shared-memory
+    // offset an immediate — the generic loop in fused_body reads the layouts
+    // from the parameter block and rebuilds the addresses per stage and tile
+    // (about as many instructions as the ops of a light pass).
+    if (!planar && static_stages_enabled()) {
+        src += "  static constexpr bool kOwnsStages = true;\n"
+               "  template <int RB_, int NC>\n"
+               "  static __device__ __forceinline__ void run_stages(float4 *tile, uint32_t tid, uint64_t base,\n"
+               "      float one, const FOp *ops) {\n"
+               "    const uint32_t lane = tid & 31u, warp = tid >> 5;\n    (void)warp;\n    const FStage st0{};\n";
+        for (int k = 0; k < p.nstages; ++k) {
+            const FStage &st = p.stages[k];
+            std::string fb = "0u";
+            for (int q = 0; q < 5; ++q) {
+                std::snprintf(buf, sizeof buf, " | (((lane >> %d) & 1u) << %d)", q, st.lf[q]);
+                fb += buf;
+            }
+            for (int q = 0; q < p.nwbits; ++q) {
+                std::snprintf(buf, sizeof buf, " | (((warp >> %d) & 1u) << %d)", q, st.wf[q]);
+                fb += buf;
+            }
+            src += "    { // stage " + std::to_string(k) + "\n      const uint32_t fb = " + fb +
+                   ";\n      const uint32_t pb = fb + (fb >> 5);\n      float4 v[1 << RB_];\n";
+            std::vector<uint32_t> off(1u << RB);
+            for (int j = 0; j < (1 << RB); ++j) {
+                uint32_t a = 0;
+                for (int r = 0; r < RB; ++r)
+                    if (j & (1 << r)) a += (1u << st.rf[r]) + ((1u << st.rf[r]) >> 5);
+                off[j] = a;
+            }
+            for (int j = 0; j < (1 << RB); ++j) {
+                std::snprintf(buf, sizeof buf, "      v[%d] = tile[pb + %uu];\n", j, off[j]);
+                src += buf;
+            }
+            std::snprintf(buf, sizeof buf, "      run<RB_>(%d, st0, ops, tid, base, one, v);\n", k);
+            src += buf;
+            for (int j = 0; j < (1 << RB); ++j) {
+                std::snprintf(buf, sizeof buf, "      tile[pb + %uu] = v[%d];\n", off[j], j);
+                src += buf;
+            }
+            if (k + 1 < p.nstages) src += "      named_sync(1, NC);\n";
+            src += "    }\n";
+        }
+        src += "  }\n";
+    } else {
+        src += "  static constexpr bool kOwnsStages = false;\n";
+    }
     std::snprintf(buf, sizeof buf,
-                  "    default: break;\n    }\n  }\n};\n"
+                  "};\n"
                   "extern \"C\" __global__ void __maxnreg__(%d) qsb_pass(float4 *__restrict__ amps,\n"
                   "    const __grid_constant__ FParams p) {\n  fused_body<%d, %d, GenProg>(amps, p);\n}\n",
                   RB == 4 ? 168 : 96, K, RB);
@@ -517,7 +577,7 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 400);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n"
-           "  static constexpr bool kPlanar = false;\n  template <int RB>\n"
+           "  static constexpr bool kPlanar = false;\n  static constexpr bool kOwnsStages = false;\n  template <int RB>\n"
            "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *, uint32_t tid,\n"
            "      uint64_t base, float, double2 (&v)[1 << RB]) {\n"
            "    const uint32_t wid = __reduce_or_sync(0xffffffffu, tid & ~31u);\n"

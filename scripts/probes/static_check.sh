@@ -1,0 +1,5 @@
+python scripts/probes/hpass_time.py
+QSB_JIT_STATIC_STAGES=0 python scripts/probes/hpass_time.py
+QSB_FUSED_DRY=4 python scripts/probes/hpass_time.py
+python scripts/fused_iter.py --big 'QSB_JIT_STATIC_STAGES=1' > gpurun_out/static_iter.jsonl 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x -k 'fused or Fused or jit or Jit or large or Large or sharded or multidevice or double' 2>&1 | tail -3
