@@ -585,6 +585,22 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const FParams &p) {
 }
 
 __device__ __forceinline__ uint32_t padded(uint32_t f) { return f + (f >> 5); }
+// 128-bit shared-memory accesses for the generated stage loops: with literal
+// offsets ptxas otherwise splits a float4 into two LDS.64 / STS.64 (to land
+// the halves in the register pairs the packed ops want), which doubles the
+// wavefronts and breaks the bank-conflict-free lane triples
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

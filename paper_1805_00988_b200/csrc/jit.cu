@@ -523,7 +523,7 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
                 fb += buf;
             }
             src += "    { // stage " + std::to_string(k) + "\n      const uint32_t fb = " + fb +
-                   ";\n      const uint32_t pb = fb + (fb >> 5);\n      float4 v[1 << RB_];\n";
+                   ";\n      const uint32_t sb = smem_u32(tile) + (fb + (fb >> 5)) * 16u;\n      float4 v[1 << RB_];\n";
             std::vector<uint32_t> off(1u << RB);
             for (int j = 0; j < (1 << RB); ++j) {
                 uint32_t a = 0;
@@ -532,13 +532,13 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
                 off[j] = a;
             }
             for (int j = 0; j < (1 << RB); ++j) {
-                std::snprintf(buf, sizeof buf, "      v[%d] = tile[pb + %uu];\n", j, off[j]);
+                std::snprintf(buf, sizeof buf, "      v[%d] = lds128(sb + %uu);\n", j, 16u * off[j]);
                 src += buf;
             }
             std::snprintf(buf, sizeof buf, "      run<RB_>(%d, st0, ops, tid, base, one, v);\n", k);
             src += buf;
             for (int j = 0; j < (1 << RB); ++j) {
-                std::snprintf(buf, sizeof buf, "      tile[pb + %uu] = v[%d];\n", off[j], j);
+                std::snprintf(buf, sizeof buf, "      sts128(sb + %uu, v[%d]);\n", 16u * off[j], j);
                 src += buf;
             }
             if (k + 1 < p.nstages) src += "      named_sync(1, NC);\n";
