@@ -69,15 +69,23 @@ struct Nvrtc {
     nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t *);
     nvrtcResult_t (*cubin)(nvrtcProgram_t, char *);
     nvrtcResult_t (*destroy)(nvrtcProgram_t *);
+    int major = 0, minor = 0;
 };
 
 Nvrtc load_nvrtc() {
     Nvrtc n;
-    const char *names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+    // The toolkit's NVRTC by absolute path first: a bare "libnvrtc.so.12"
+    // resolves to whichever copy the process already holds — under torch its
+    // bundled (older) one, whose ptxas builds every packed FFMA2 multiplier as
+    // a register pair (two MOVs each; the H-layer's first pass 2.63 -> 3.1 ms).
+    // QSB_NVRTC overrides.
+    const char *names[] = {std::getenv("QSB_NVRTC"), "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
+                           "libnvrtc.so"};
     void *h = nullptr;
     for (const char *nm : names)
-        if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+        if (nm && *nm && (h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
     if (!h) return n;
+    if (auto ver = (nvrtcResult_t(*)(int *, int *))dlsym(h, "nvrtcVersion")) ver(&n.major, &n.minor);
     n.create = (decltype(n.create))dlsym(h, "nvrtcCreateProgram");
     n.compile = (decltype(n.compile))dlsym(h, "nvrtcCompileProgram");
     n.log_size = (decltype(n.log_size))dlsym(h, "nvrtcGetProgramLogSize");
@@ -733,8 +741,9 @@ std::string cache_key(const std::string &src) {
         uint64_t h = 1469598103934665603ull;
         for (const char *t : {kJitCommon, kJitFusedDev, kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3]})
             for (const char *c = t; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;
-        char b[40];
-        std::snprintf(b, sizeof b, "\n// headers+options %016llx\n", (unsigned long long)h);
+        char b[80];  // the compiler version too: programs differ between NVRTC releases
+        std::snprintf(b, sizeof b, "\n// headers+options %016llx nvrtc %d.%d\n", (unsigned long long)h,
+                      nvrtc().major, nvrtc().minor);
         return std::string(b);
     }();
     return src + tag;
@@ -761,6 +770,17 @@ bool compile_cubin(Job &job) {
 
 bool compile_nvrtc(Job &job) {
     const Nvrtc &nv = nvrtc();
+    if (const char *dir = std::getenv("QSB_JIT_DUMP")) {  // generated sources, for offline SASS study
+        uint64_t h = 1469598103934665603ull;
+        for (char c : job.src) h = (h ^ (unsigned char)c) * 1099511628211ull;
+        char name[48];
+        std::snprintf(name, sizeof name, "/qsb_pass_%016llx.cu", (unsigned long long)h);
+        const std::string path = std::string(dir) + name;
+        if (FILE *f = std::fopen(path.c_str(), "w")) {
+            std::fwrite(job.src.data(), 1, job.src.size(), f);
+            std::fclose(f);
+        }
+    }
     const char *hdrs[2] = {kJitCommon, kJitFusedDev};
     const char *names[2] = {"common.cuh", "fused_dev.cuh"};
     nvrtcProgram_t prog = nullptr;
