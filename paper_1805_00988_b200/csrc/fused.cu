@@ -315,7 +315,14 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     // i adds 1, 2, 4 mod 8 for i = 0, 1, 2 and for i = 5, 6, 7 (the row
     // strides 33, 66, 132) and 0 mod 8 otherwise: lanes 0..2 must take one
     // f-bit from each class {0,5}, {1,6}, {2,7} (8 conflict-free triples).
+    // QSB_FUSED_NOBANK=1 (probe): ignore the bank classes — lanes take the
+    // least-tested free bits, shared-memory accesses may conflict
+    static const bool nobank = [] {
+        const char *e = std::getenv("QSB_FUSED_NOBANK");
+        return e && e[0] == '1';
+    }();
     auto triple_ok = [&](const std::vector<int> &rb) {
+        if (nobank) return true;
         for (int c = 0; c < 3; ++c) {
             const bool lo_free = std::find(rb.begin(), rb.end(), c) == rb.end();
             const bool hi_free = FB > c + 5 && std::find(rb.begin(), rb.end(), c + 5) == rb.end();
@@ -427,7 +434,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
             // when both are free of register bits
             bool used[32] = {false};
             for (int r = 0; r < RB; ++r) used[st.rf[r]] = true;
-            for (int c = 0; c < 3; ++c) {
+            for (int c = 0; c < (nobank ? 0 : 3); ++c) {
                 const bool lo_free = !used[c], hi_free = FB > c + 5 && !used[c + 5];
                 const int f = (!lo_free || (hi_free && uses[c + 5] < uses[c])) ? c + 5 : c;
                 st.lf[c] = f;
@@ -437,9 +444,9 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
             for (int f = 0; f < FB; ++f)
                 if (!used[f]) fr.push_back(f);
             std::stable_sort(fr.begin(), fr.end(), [&](int x, int y) { return uses[x] < uses[y]; });
-            st.lf[3] = fr[0];
-            st.lf[4] = fr[1];
-            std::vector<int> wb(fr.begin() + 2, fr.end());
+            const int nl = nobank ? 5 : 2;  // lanes still to assign
+            for (int l = 0; l < nl; ++l) st.lf[5 - nl + l] = fr[l];
+            std::vector<int> wb(fr.begin() + nl, fr.end());
             std::sort(wb.begin(), wb.end());
             for (int w = 0; w < (int)wb.size(); ++w) st.wf[w] = wb[w];
         }

@@ -469,6 +469,22 @@ __device__ __forceinline__ void pphase_sel(bool on, float2 d, float4 (&v)[1 << R
 // Combined diagonal run (opt-in, not bit-exact): multiply by e^{2 pi i t / 2^32}
 // for an accumulated phase t in fixed-point turns (exact modular sum of the
 // run's angles); one complex product per amplitude instead of one per op.
+// (cos, sin) of an angle in fixed-point turns, and the product with it
+__device__ __forceinline__ float2 turns_sincos(uint32_t t) {
+    const float ang = (float)(int)t * 1.46291807926715968e-9f;  // 2 pi / 2^32
+    float sn, cs;
+    __sincosf(ang, &sn, &cs);
+    return make_float2(cs, sn);
+}
+// product of two unit factors, rounding unconstrained (combined mode only)
+__device__ __forceinline__ float2 cmul_any(float2 x, float2 y) {
+    return make_float2(x.x * y.x - x.y * y.y, x.x * y.y + x.y * y.x);
+}
+__device__ __forceinline__ void turns_apply(float2 e, float &re, float &im) {
+    const float nr = __fmaf_rn(re, e.x, -__fmul_rn(im, e.y));
+    im = __fmaf_rn(re, e.y, __fmul_rn(im, e.x));
+    re = nr;
+}
 __device__ __forceinline__ void turns_mul(uint32_t t, float &re, float &im) {
     const float ang = (float)(int)t * 1.46291807926715968e-9f;  // 2 pi / 2^32
     float sn, cs;

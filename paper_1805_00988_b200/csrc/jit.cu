@@ -377,17 +377,47 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
                     src += adds;
                     const char *re[2] = {planar ? "x" : "x", planar ? "y" : "z"};
                     const char *im[2] = {planar ? "z" : "y", planar ? "w" : "w"};
+                    // e^{i a} for each accumulator once per thread (one
+                    // __sincosf each), and per distinct set of matching
+                    // patterns the product of those factors (built from the
+                    // set minus its last member, memoised): the SFU pipe
+                    // (16 lanes / clk / SM) bounded QFT pass 0 when every
+                    // amplitude took its own __sincosf.  Each factor is
+                    // within ~4e-7 of e^{i a}; a product of m factors within
+                    // ~m times that (the mode's bar is rtol 1e-5).
+                    std::vector<std::vector<int>> sets;  // index = factor f<k>
+                    std::string facs, muls;
+                    auto factor = [&](auto &&self, const std::vector<int> &set) -> size_t {
+                        size_t k = std::find(sets.begin(), sets.end(), set) - sets.begin();
+                        if (k < sets.size()) return k;
+                        if (set.size() == 1) {
+                            std::snprintf(buf, sizeof buf, "        const float2 f%zu = turns_sincos(a%d);\n", sets.size(),
+                                          set[0]);
+                        } else {
+                            const std::vector<int> head(set.begin(), set.end() - 1);
+                            const size_t h = self(self, head), t = self(self, std::vector<int>{set.back()});
+                            std::snprintf(buf, sizeof buf, "        const float2 f%zu = cmul_any(f%zu, f%zu);\n",
+                                          sets.size(), h, t);
+                        }
+                        facs += buf;
+                        sets.push_back(set);
+                        return sets.size() - 1;
+                    };
                     for (int j = 0; j < (1 << RB); ++j)
                         for (int h = 0; h < 2; ++h) {
-                            std::string sum;
+                            std::vector<int> set;
                             for (size_t a = 0; a < pats.size(); ++a)
                                 if (((uint32_t)j & pats[a].first) == pats[a].first && (!pats[a].second || h == 1))
-                                    sum += (sum.empty() ? "a" : " + a") + std::to_string(a);
-                            if (sum.empty()) continue;
-                            std::snprintf(buf, sizeof buf, "        if constexpr (%d < (1 << RB)) turns_mul(%s, v[%d].%s, v[%d].%s);\n",
-                                          j, sum.c_str(), j, re[h], j, im[h]);
-                            src += buf;
+                                    set.push_back((int)a);
+                            if (set.empty()) continue;
+                            const size_t e = factor(factor, set);
+                            std::snprintf(buf, sizeof buf,
+                                          "        if constexpr (%d < (1 << RB)) turns_apply(f%zu, v[%d].%s, v[%d].%s);\n",
+                                          j, e, j, re[h], j, im[h]);
+                            muls += buf;
                         }
+                    src += facs;
+                    src += muls;
                     src += "      }\n";
                     o = e2;
                     continue;
