@@ -296,8 +296,8 @@ def run_ours(args):
         # PCIe-bound (this box: 55-57 GB/s one way, 46 GB/s each way when
         # both directions run, scripts/probes/pcie.py): the first upload and
         # the last download are not overlapped, so a short run under-reports
-        # the steady state by (k+1)/k; 10 steps keep that under 10 %.
-        k2 = max(10, min(args.steps, 20))
+        # the steady state by (k+1)/k; 20 steps keep that near 5 %.
+        k2 = max(20, min(args.steps, 40))
 
         # the layer as a user runs it: fused passes through qs_apply_fused
         # (compiled pass programs from the second warm-up step on)
@@ -410,7 +410,7 @@ def run_sharded(args):
     import torch.distributed as dist
 
     from paper_1805_00988_b200 import _native as N
-    from paper_1805_00988_b200.gates import H
+    from paper_1805_00988_b200.gates import H, m8
     from paper_1805_00988_b200.sharded import ShardedState
 
     rank, world, local = _dist_env()
@@ -455,6 +455,32 @@ def run_sharded(args):
     swaps = (st.swaps - swaps0) // args.steps
     sweeps = args.steps * n * world
     value = sweeps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the local shard sweep): CUDA events
+    # around single local-target sweeps on the shard's stream, max over ranks
+    h = eng.state.handle
+    hm = m8(H)
+    hp = N.f32ptr(hm)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2 * L)]
+    barrier()
+    for i, (ea, eb) in enumerate(ev):
+        ea.record(stream)
+        N.check(N.lib().qs_apply_gate(h, i % L, hp))
+        eb.record(stream)
+    barrier()
+    launch_ms = statistics.mean(ea.elapsed_time(eb) for ea, eb in ev)
+    tt = torch.tensor([launch_ms], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    launch_ms = float(tt.item())
+    peak, peak_src = measured_peak_gbs()
+    bytes_per_launch = 16 * (1 << L)
+    achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic() if L == N_QUBITS else None,
+                "kernel": "k_sweep_high/k_sweep_low on each rank's shard (local targets)",
+                "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src,
+                "avg_launch_ms": launch_ms, "timing": "CUDA events per launch on the shard stream, "
+                                                      "mean over 2 x L local targets, max over ranks"}
 
     e2e = None
     if not args.no_e2e:
@@ -509,6 +535,7 @@ def run_sharded(args):
                        "value_unit": "shard sweeps (2^%d amplitudes) per second, summed over GPUs" % L,
                        "l2": "shards (8 GiB) larger than L2; no flush needed"},
             "gpu_launches": args.steps * n,
+            "roofline": roofline,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": None,

@@ -28,6 +28,8 @@ def test_two_ranks_one_gpu():
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["n_qubits"] == 23
+    roof = line["roofline"]
+    assert roof["bound"] == "hbm" and roof["achieved"] > 0 and roof["frac"] == roof["achieved"] / roof["peak"]
     ex = line["extras"]
     assert ex["global_gates"]["peer_nvlink"]["peer_gates_per_rep"] == 1
     assert ex["strong34"]["analytic_check_ok"] is True
