@@ -1059,7 +1059,7 @@ int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host
     if (rc) return rc;
     // A fresh numpy result page-faults 4-KiB pages during the host copy: ask
     // for transparent huge pages on its 2-MiB-aligned interior.
-    if (count * sizeof(double) >= (64u << 20)) {
+    if (count * sizeof(double) >= (64u << 20) && !(std::getenv("QSB_PROB_THP") && std::getenv("QSB_PROB_THP")[0] == '0')) {
         const uintptr_t a = ((uintptr_t)host + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
         const uintptr_t z = ((uintptr_t)(host + count)) & ~(uintptr_t)((2u << 20) - 1);
         if (z > a) madvise((void *)a, z - a, MADV_HUGEPAGE);
@@ -1086,7 +1086,8 @@ int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host
     };
     // copy team: worker t copies slice t of piece `ready`, then counts itself done
     unsigned hw = std::thread::hardware_concurrency();
-    const int nt = count * sizeof(double) < (16u << 20) ? 0 : (int)(hw > 16 ? 16 : (hw < 2 ? 2 : hw));
+    int nt = count * sizeof(double) < (16u << 20) ? 0 : (int)(hw > 16 ? 16 : (hw < 2 ? 2 : hw));
+    if (const char *e = std::getenv("QSB_PROB_THREADS")) nt = nt ? std::atoi(e) : 0;  // probes
     std::atomic<long long> ready{-1};
     std::atomic<int> finished{0};
     std::atomic<bool> stop{false};
