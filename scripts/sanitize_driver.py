@@ -59,6 +59,20 @@ if part in ("all", "sample"):
     st.measure_collapse(4)
     st.close()
 
+if part in ("all", "sample18"):
+    # n = 18: whole warps of 4096-amplitude chunks, so M3 takes the bulk-copy
+    # ring (k_trajectories_bulk) and M4b the bulk-copied chunk re-sums
+    m = 18
+    st = State(m)
+    for q in range(m):
+        st.h(q)
+    st.t(2)
+    st.sample_outcomes(3000, 5)
+    mag = np.exp(rng.uniform(np.log(1e-30), 0.0, size=1 << m))
+    st.set_amplitudes((mag * np.exp(2j * np.pi * rng.random(1 << m))).astype(np.complex64))
+    st.sample_outcomes(3000, 6)
+    st.close()
+
 if part in ("all", "peer"):
     from paper_1805_00988_b200.sharded import ShardedState
 
