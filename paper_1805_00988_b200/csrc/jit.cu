@@ -207,6 +207,59 @@ bool static_stages_enabled() {
     return on;
 }
 
+// The whole stage sequence of a generated program with the stage layouts as
+// literals: each thread's padded shared-memory base per stage is a few
+// shifts of its lane / warp bits (loop-invariant across tiles) and every
+// register's offset the immediate of a 128-bit ld/st.shared.  The generic
+// loop in fused_body reads the layouts from the parameter block and
+// rebuilds the addresses per stage and tile (about as many instructions as
+// the ops of a light pass).  dbl: complex128 registers (one amplitude per
+// 16-B unit).
+void emit_run_stages(std::string &src, const FParams &p, int RB, bool dbl) {
+    char buf[256];
+    const char *vt = dbl ? "double2" : "float4";
+    src += "  static constexpr bool kOwnsStages = true;\n"
+           "  template <int RB_, int NC>\n"
+           "  static __device__ __forceinline__ void run_stages(float4 *tile, uint32_t tid, uint64_t base,\n"
+           "      float one, const FOp *ops) {\n"
+           "    const uint32_t lane = tid & 31u, warp = tid >> 5;\n    (void)warp;\n    const FStage st0{};\n";
+    for (int k = 0; k < p.nstages; ++k) {
+        const FStage &st = p.stages[k];
+        std::string fb = "0u";
+        for (int q = 0; q < 5; ++q) {
+            std::snprintf(buf, sizeof buf, " | (((lane >> %d) & 1u) << %d)", q, st.lf[q]);
+            fb += buf;
+        }
+        for (int q = 0; q < p.nwbits; ++q) {
+            std::snprintf(buf, sizeof buf, " | (((warp >> %d) & 1u) << %d)", q, st.wf[q]);
+            fb += buf;
+        }
+        src += "    { // stage " + std::to_string(k) + "\n      const uint32_t fb = " + fb +
+               ";\n      const uint32_t sb = smem_u32(tile) + (fb + (fb >> 5)) * 16u;\n      " + vt +
+               " v[1 << RB_];\n";
+        std::vector<uint32_t> off(1u << RB);
+        for (int j = 0; j < (1 << RB); ++j) {
+            uint32_t a = 0;
+            for (int r = 0; r < RB; ++r)
+                if (j & (1 << r)) a += (1u << st.rf[r]) + ((1u << st.rf[r]) >> 5);
+            off[j] = a;
+        }
+        for (int j = 0; j < (1 << RB); ++j) {
+            std::snprintf(buf, sizeof buf, "      v[%d] = %s(sb + %uu);\n", j, dbl ? "lds128d" : "lds128", 16u * off[j]);
+            src += buf;
+        }
+        std::snprintf(buf, sizeof buf, "      run<RB_>(%d, st0, ops, tid, base, one, v);\n", k);
+        src += buf;
+        for (int j = 0; j < (1 << RB); ++j) {
+            std::snprintf(buf, sizeof buf, "      %s(sb + %uu, v[%d]);\n", dbl ? "sts128d" : "sts128", 16u * off[j], j);
+            src += buf;
+        }
+        if (k + 1 < p.nstages) src += "      named_sync(1, NC);\n";
+        src += "    }\n";
+    }
+    src += "  }\n";
+}
+
 std::string generate(const FParams &p, int K, int RB, bool param = false) {
     // diagonal ops inside a test: 0 (default) packed phase_ct, 1 scalar
     // phase_cs, 2 scalar everywhere (QSB_JIT_PHASE, for measurements).  The
@@ -540,55 +593,12 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
         src += "    } break;\n";
     }
     src += "    default: break;\n    }\n  }\n";
-    // The whole stage sequence with the stage layouts as literals: each
-    // thread's padded base per stage is a few shifts of its lane / warp bits
-    // (loop-invariant across tiles) and every register's shared-memory
-    // offset an immediate — the generic loop in fused_body reads the layouts
-    // from the parameter block and rebuilds the addresses per stage and tile
-    // (about as many instructions as the ops of a light pass).
-    if (!planar && static_stages_enabled()) {
-        src += "  static constexpr bool kOwnsStages = true;\n"
-               "  template <int RB_, int NC>\n"
-               "  static __device__ __forceinline__ void run_stages(float4 *tile, uint32_t tid, uint64_t base,\n"
-               "      float one, const FOp *ops) {\n"
-               "    const uint32_t lane = tid & 31u, warp = tid >> 5;\n    (void)warp;\n    const FStage st0{};\n";
-        for (int k = 0; k < p.nstages; ++k) {
-            const FStage &st = p.stages[k];
-            std::string fb = "0u";
-            for (int q = 0; q < 5; ++q) {
-                std::snprintf(buf, sizeof buf, " | (((lane >> %d) & 1u) << %d)", q, st.lf[q]);
-                fb += buf;
-            }
-            for (int q = 0; q < p.nwbits; ++q) {
-                std::snprintf(buf, sizeof buf, " | (((warp >> %d) & 1u) << %d)", q, st.wf[q]);
-                fb += buf;
-            }
-            src += "    { // stage " + std::to_string(k) + "\n      const uint32_t fb = " + fb +
-                   ";\n      const uint32_t sb = smem_u32(tile) + (fb + (fb >> 5)) * 16u;\n      float4 v[1 << RB_];\n";
-            std::vector<uint32_t> off(1u << RB);
-            for (int j = 0; j < (1 << RB); ++j) {
-                uint32_t a = 0;
-                for (int r = 0; r < RB; ++r)
-                    if (j & (1 << r)) a += (1u << st.rf[r]) + ((1u << st.rf[r]) >> 5);
-                off[j] = a;
-            }
-            for (int j = 0; j < (1 << RB); ++j) {
-                std::snprintf(buf, sizeof buf, "      v[%d] = lds128(sb + %uu);\n", j, 16u * off[j]);
-                src += buf;
-            }
-            std::snprintf(buf, sizeof buf, "      run<RB_>(%d, st0, ops, tid, base, one, v);\n", k);
-            src += buf;
-            for (int j = 0; j < (1 << RB); ++j) {
-                std::snprintf(buf, sizeof buf, "      sts128(sb + %uu, v[%d]);\n", 16u * off[j], j);
-                src += buf;
-            }
-            if (k + 1 < p.nstages) src += "      named_sync(1, NC);\n";
-            src += "    }\n";
-        }
-        src += "  }\n";
-    } else {
+    // The whole stage sequence with the stage layouts as literals (see
+    // emit_run_stages).
+    if (!planar && static_stages_enabled())
+        emit_run_stages(src, p, RB, false);
+    else
         src += "  static constexpr bool kOwnsStages = false;\n";
-    }
     std::snprintf(buf, sizeof buf,
                   "};\n"
                   "extern \"C\" __global__ void __maxnreg__(%d) qsb_pass(float4 *__restrict__ amps,\n"
@@ -618,7 +628,7 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 400);
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n"
-           "  static constexpr bool kPlanar = false;\n  static constexpr bool kOwnsStages = false;\n  template <int RB>\n"
+           "  static constexpr bool kPlanar = false;\n  template <int RB>\n"
            "  static __device__ __forceinline__ void run(int s, const FStage &, const FOp *, uint32_t tid,\n"
            "      uint64_t base, float, double2 (&v)[1 << RB]) {\n"
            "    const uint32_t wid = __reduce_or_sync(0xffffffffu, tid & ~31u);\n"
@@ -655,8 +665,13 @@ std::string generate_d(const FParams &p, int K, int RB, const qs_op64 *ops64) {
         }
         src += "    } break;\n";
     }
+    src += "    default: break;\n    }\n  }\n";
+    if (static_stages_enabled())
+        emit_run_stages(src, p, RB, true);
+    else
+        src += "  static constexpr bool kOwnsStages = false;\n";
     std::snprintf(buf, sizeof buf,
-                  "    default: break;\n    }\n  }\n};\n"
+                  "};\n"
                   "extern \"C\" __global__ void __maxnreg__(%d) qsb_pass(float4 *__restrict__ amps,\n"
                   "    const __grid_constant__ FParams p) {\n  fused_body<%d, %d, GenProg, double2>(amps, p);\n}\n",
                   RB == 4 ? 168 : 96, K, RB);
