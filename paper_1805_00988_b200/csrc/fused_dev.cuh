@@ -621,9 +621,27 @@ __device__ __forceinline__ double2 lds128d(uint32_t a) {
 __device__ __forceinline__ void sts128d(uint32_t a, double2 v) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+template <class V>
+__device__ __forceinline__ V lds_unit(uint32_t a);
+template <>
+__device__ __forceinline__ float4 lds_unit<float4>(uint32_t a);
+template <>
+__device__ __forceinline__ double2 lds_unit<double2>(uint32_t a) {
+    return lds128d(a);
+}
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
+}
+template <>
+__device__ __forceinline__ float4 lds_unit<float4>(uint32_t a) {
+    return lds128(a);
+}
+__device__ __forceinline__ void sts_unit_(uint32_t a, float4 v) { sts128(a, v); }
+__device__ __forceinline__ void sts_unit_(uint32_t a, double2 v) { sts128d(a, v); }
+template <class V>
+__device__ __forceinline__ void sts_unit(uint32_t a, V v) {
+    sts_unit_(a, v);
 }
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
@@ -794,6 +812,18 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
     }
 
     // -------------------- compute warps: register stages --------------------
+    // Generic loop (interpreter, probes): each thread's padded base per stage
+    // depends only on its lane / warp bits, so it is built once per kernel
+    // (local memory) instead of per stage and tile.
+    uint32_t stage_pb[kMaxStages];
+    for (int s = 0; s < p.nstages; ++s) {
+        const FStage &st = p.stages[s];
+        uint32_t fb = 0;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) fb |= (uint32_t)((lane >> q) & 1) << st.lf[q];
+        for (int q = 0; q < p.nwbits; ++q) fb |= (uint32_t)((warp >> q) & 1) << st.wf[q];
+        stage_pb[s] = smem_u32(buf0) + padded(fb) * 16u;
+    }
     for (int i = 0;; ++i) {
         const int b = i % kNB;
         float4 *tile = buf0 + b * kBufF4;
@@ -810,14 +840,12 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         }
         for (int s = 0; s < (staged || p.dry == 2 || p.dry == 3 ? 0 : p.nstages); ++s) {
             const FStage &st = p.stages[s];
-            uint32_t fb = 0;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) fb |= (uint32_t)((lane >> q) & 1) << st.lf[q];
-            for (int q = 0; q < p.nwbits; ++q) fb |= (uint32_t)((warp >> q) & 1) << st.wf[q];
-            const uint32_t pb = padded(fb);
+            // byte address of this thread's unit 0 in buffer b, and the
+            // register bits' byte strides
+            const uint32_t pb = stage_pb[s] + (uint32_t)b * (uint32_t)kBufF4 * 16u;
             uint32_t rs[RB];
 #pragma unroll
-            for (int r = 0; r < RB; ++r) rs[r] = padded(1u << st.rf[r]);
+            for (int r = 0; r < RB; ++r) rs[r] = padded(1u << st.rf[r]) * 16u;
             V v[1 << RB];
 #pragma unroll
             for (int j = 0; j < (1 << RB); ++j) {
@@ -825,7 +853,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
-                v[j] = *reinterpret_cast<const V *>(tile + a);
+                v[j] = lds_unit<V>(a);
             }
             if constexpr (Prog::kPlanar && UnitTraits<V>::kHalf) {
                 if (s == 0) {
@@ -846,7 +874,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
-                *reinterpret_cast<V *>(tile + a) = v[j];
+                sts_unit<V>(a, v[j]);
             }
             if (s + 1 < p.nstages) named_sync(1, kCompute);
         }
