@@ -442,3 +442,19 @@ class TestSamplingChainPaths:
             got = st.sample_outcomes(20000, seed)
             assert np.array_equal(got, oc.sample_outcomes(amps, 20000, seed)), (kind, seed)
         st.close()
+
+
+@pytest.mark.parametrize("n", [16, 17, 18, 19])
+def test_sampling_m3_forms_at_the_warp_boundary(n):
+    """M3 runs register-staged below 32 chunks (n < 17) and as the bulk-copy
+    ring from whole warps of chunks on (n >= 17): per-draw parity with the
+    oracle on both sides of the boundary, on a state with binade crossings
+    inside chunks (log-uniform magnitudes) and on a uniform one."""
+    rng = np.random.default_rng(n)
+    mag = np.exp(rng.uniform(np.log(1e-20), 0.0, size=1 << n))
+    for amps in ((mag * np.exp(2j * np.pi * rng.random(1 << n))).astype(np.complex64),
+                 np.full(1 << n, np.float32(2.0 ** (-n / 2)), np.complex64)):
+        st = load(n, amps)
+        got = st.sample_outcomes(5000, 9)
+        assert np.array_equal(got, oc.sample_outcomes(amps, 5000, 9))
+        st.close()
