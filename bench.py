@@ -1186,6 +1186,42 @@ def run_extras(st, stream, n, cpu=True, harness=True):
                     "peer_gates": vs.peer_gate_count}
         vs.close()
         _N.lib().qs_release_cached(-1)
+    # the exchange alone (data movement of one qubit swap: each of the two
+    # 30-qubit shards trades half its amplitudes, 2 x 4 GiB) against a D2D
+    # copy of the same 8 GiB (>= 0.8 of the copy rate)
+    try:
+        xs = {}
+        payload = 2 * (1 << 29) * 8
+        for mode, exch in (("copy_exchange", "nccl"), ("peer_swap_kernel", "peer")):
+            vs = ShardedState.virtual(31, 2, peer_gates=False, exchange=exch)
+            vs._exchange(0)
+            vs.synchronize()
+            reps = 4
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                vs._exchange(0)
+            vs.synchronize()
+            dt = (time.perf_counter() - t0) / reps
+            xs[mode] = {"ms": dt * 1e3, "payload_GBps": payload / dt / 1e9}
+            vs.close()
+            _N.lib().qs_release_cached(-1)
+        src_t = torch.empty(payload // 4, dtype=torch.float32, device="cuda")
+        dst_t = torch.empty_like(src_t)
+        dst_t.copy_(src_t)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(4):
+            dst_t.copy_(src_t)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / 4
+        xs["d2d_copy_same_payload"] = {"ms": dt * 1e3, "payload_GBps": payload / dt / 1e9}
+        for mode in ("copy_exchange", "peer_swap_kernel"):
+            xs[mode]["vs_d2d_copy"] = xs["d2d_copy_same_payload"]["ms"] / xs[mode]["ms"]
+        del src_t, dst_t
+        sv["exchange_alone"] = {**xs, "note": "host wall clock per exchange (synchronized), 4 reps; payload = "
+                                              "the 8 GiB that change shards"}
+    except Exception as exc:  # noqa: BLE001
+        sv["exchange_alone"] = {"error": f"{type(exc).__name__}: {exc}"}
     # the same layer through the single-process C ABI (qs_create_sharded)
     from paper_1805_00988_b200.multigpu import MultiDeviceState
 
