@@ -605,12 +605,27 @@ class ShardedState:
 
         counters = (self.peer_swaps,)
         t_peer = timed(peer_once)
-        t_swap = timed(swap_once) / 2  # one call = two (exchange + sweep)
+        # the swap's data movement both ways when the transport can move
+        # device buffers itself (NCCL send/recv with staging) and the peers
+        # are mapped (one swap kernel, no staging): the faster one becomes
+        # the register's exchange
+        modes = ["peer", "nccl"] if getattr(self.transport, "moves_device_buffers", True) else [self.exchange]
+        keep = self.exchange
+        t_modes = []
+        for mode in modes:
+            self.exchange = mode
+            t_modes.append(timed(swap_once) / 2)  # one call = two (exchange + sweep)
+        self.exchange = keep
         (self.peer_swaps,) = counters
-        t = self.transport.combine_max([np.array([t_peer, t_swap])])
-        t_peer, t_swap = float(t[0]), float(t[1])
+        t = self.transport.combine_max([np.array([t_peer] + t_modes)])
+        t_peer, t_modes = float(t[0]), [float(x) for x in t[1:]]
+        best = int(np.argmin(t_modes))
+        self.exchange = modes[best]
+        t_swap = t_modes[best]
         self.peer_gates = t_peer <= t_swap
         self.calibration = {"peer_gate_ms": t_peer * 1e3, "swap_and_sweep_ms": t_swap * 1e3,
+                            "swap_exchange": self.exchange,
+                            **{f"swap_and_sweep_{m}_ms": x * 1e3 for m, x in zip(modes, t_modes)},
                             "chosen": "peer" if self.peer_gates else "swap"}
         return self.calibration
 
