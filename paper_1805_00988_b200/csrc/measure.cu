@@ -968,31 +968,59 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
             uint64_t j = 0, hit = C;
             if (fine0 && clog == kChunkLog) {
                 const int f = flags[lo];
-                if (f & kFlagFineAbs) {
-                    // a walked chunk: exact running values before amplitude 256 q
-                    const double *fa = fine0 + lo * kFinePer;
-                    int sb = 0;
-                    for (int q = 1; q < kFinePer; ++q) {
-                        const double v = fa[q];
-                        if (v >= cut) break;
-                        sb = q;
+                // the chunk's 16 fine values in 8 16-B loads issued together
+                // (a load-compare-break loop waited a latency per value); the
+                // values are non-decreasing, so the sub-block is the count of
+                // leading values below the cut
+                const bool absf = (f & kFlagFineAbs) != 0;
+                const bool traj = !absf && (f & kFlagOk) && !(f & (kFlagExact0 | kFlagWalked));
+                if (absf || traj) {
+                    const double *fb = (absf || !(__double_as_longlong(s) & 1ll) ? fine0 : fine1) + lo * kFinePer;
+                    double fv[kFinePer];
+#pragma unroll
+                    for (int q = 0; q < kFinePer / 2; ++q) {
+                        const double2 x = reinterpret_cast<const double2 *>(fb)[q];
+                        fv[2 * q] = x.x;
+                        fv[2 * q + 1] = x.y;
                     }
-                    j = (uint64_t)sb << kFineLog;
-                    s = fa[sb];
-                } else if ((f & kFlagOk) && !(f & (kFlagExact0 | kFlagWalked))) {
-                    // exact running values after 256, 512, ... amplitudes: the
-                    // chunk start plus the trajectory of its parity (M3, M4)
-                    const double *fd = ((__double_as_longlong(s) & 1ll) ? fine1 : fine0) + lo * kFinePer;
-                    double fs = s;
+                    // absolute (a walked / exact0 chunk: running values before
+                    // amplitude 256 q) or start + trajectory offset (M3, M4)
+                    double fs = absf ? fv[0] : s;
                     int sb = 0;
+                    bool go = true;
+#pragma unroll
                     for (int q = 1; q < kFinePer; ++q) {
-                        const double v = __dadd_rn(s, fd[q]);
-                        if (v >= cut) break;
-                        sb = q;
-                        fs = v;
+                        const double v = absf ? fv[q] : __dadd_rn(s, fv[q]);
+                        go = go && v < cut;
+                        if (go) {
+                            sb = q;
+                            fs = v;
+                        }
                     }
                     j = (uint64_t)sb << kFineLog;
                     s = fs;
+                }
+            }
+            if constexpr (std::is_same<A, float2>::value) {
+                // 16 probabilities per batch from 8 float4 loads (j is a
+                // multiple of 256 here, the chunk 32-KB aligned)
+                const float4 *p4 = reinterpret_cast<const float4 *>(p);
+                for (; j + 16 <= C && hit == C; j += 16) {
+                    float4 w[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) w[q] = p4[(j >> 1) + q];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const double pa = prob(make_float2(w[q].x, w[q].y)), pb = prob(make_float2(w[q].z, w[q].w));
+                        if (hit == C) {
+                            s = __dadd_rn(s, pa);
+                            if (s >= cut) hit = j + 2 * q;
+                        }
+                        if (hit == C) {
+                            s = __dadd_rn(s, pb);
+                            if (s >= cut) hit = j + 2 * q + 1;
+                        }
+                    }
                 }
             }
             for (; j + 8 <= C && hit == C; j += 8) {
@@ -1175,7 +1203,7 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     // (2 per chunk), block maps (4 per block), block starts + flags + outcomes
     // + fine starts (two trajectories x 16 per chunk) when there are draws
     const bool fine = k > 0 && c.clog == kChunkLog;
-    const size_t nd = 7 * nch + 2 + 2 * nch + 5 * c.nblk + (fine ? 2 * kFinePer * nch : 0);
+    const size_t nd = 7 * nch + 2 + 2 * nch + 5 * c.nblk + (fine ? 2 * kFinePer * nch + 8 : 0);
     const size_t bytes = nd * sizeof(double) + nch * sizeof(int) + 64 + (size_t)k * sizeof(int64_t);
     int rc = ensure_scratch(s, bytes);
     if (rc) return rc;
@@ -1192,7 +1220,8 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     c.pmap = (long long *)(b + 7 * nch + 2);
     c.bmap = c.pmap + 2 * nch;
     c.sblock = (double *)(c.bmap + 4 * c.nblk);
-    c.fine0 = fine ? c.sblock + c.nblk : nullptr;
+    // fine values 64-B aligned (k_draws reads them as double2)
+    c.fine0 = fine ? (double *)(((uintptr_t)(c.sblock + c.nblk) + 63) & ~(uintptr_t)63) : nullptr;
     c.fine1 = fine ? c.fine0 + kFinePer * nch : nullptr;
     c.flags = (int *)(b + nd);
     c.dout = (int64_t *)((char *)c.flags + ((nch * sizeof(int) + 63) & ~(size_t)63));
