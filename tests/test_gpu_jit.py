@@ -215,3 +215,37 @@ def test_parametric_programs_reuse_structure(tmp_path):
     assert all(o["same"] for o in out)
     assert out[0]["new"] >= 1 and out[1]["new"] >= 1  # literal, then the parametric programs
     assert out[2]["new"] == 0 and out[3]["new"] == 0
+
+
+@pytest.mark.parametrize("env", [{"QSB_JIT_STATIC_STAGES": "0"}, {"QSB_JIT_PHASE": "1", "QSB_JIT_LOOP_FORM": "cs"},
+                                 {"QSB_FUSED_RUN_BOXES": "0"}])
+def test_program_variants_same_bits(tmp_path, env):
+    """Code-generation variants kept as switches (the generic stage loop
+    instead of the literal-layout one, the scalar phase forms, one-bit TMA box
+    dims) give the default programs' bits: each runs a QFT and a layered
+    circuit in a fresh process (the switches are read once per process)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    child = (
+        "import sys, json, hashlib\n"
+        f"sys.path.insert(0, {str(root)!r})\n"
+        "from paper_1805_00988_b200 import State, build_qft, layered_random_circuit, fusion\n"
+        "from paper_1805_00988_b200.circuits import lower_ops\n"
+        "st = State(18)\n"
+        "for q in range(18): st.h(q)\n"
+        "fusion.run(st, fusion.plan(18, lower_ops(build_qft(18)), 12))\n"
+        "fusion.run(st, fusion.plan(18, lower_ops(layered_random_circuit(18, 4, seed=5)), 12))\n"
+        "print(json.dumps({'d': hashlib.sha256(st.amplitudes().tobytes()).hexdigest(), **fusion.jit_stats()}))\n")
+    outs = []
+    for e in ({}, env):
+        full = dict(__import__("os").environ, QSB_JIT_CACHE_DIR=str(tmp_path / str(len(outs))), QSB_FUSED_JIT="2",
+                    **e)
+        r = subprocess.run([sys.executable, "-c", child], env=full, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0]["failed"] == 0 and outs[1]["failed"] == 0 and outs[1]["compiled"] >= 1
+    assert outs[0]["d"] == outs[1]["d"]
