@@ -403,6 +403,11 @@ __device__ __forceinline__ void phase_sel(bool on, float2 d, float4 (&v)[1 << RB
         cmul_s(e, v[j].z, v[j].w);
     }
 }
+// the same with the packed product (FMUL, FMUL, FFMA2 per amplitude)
+template <int RNEED, bool ODD, int RB>
+__device__ __forceinline__ void phase_sel_ct(bool on, float2 d, float4 (&v)[1 << RB]) {
+    phase_ct<RNEED, ODD, RB>(make_float2(on ? d.x : 1.0f, on ? d.y : 0.0f), v);
+}
 
 template <int T, int RNEED, bool ODD_ONLY, int RB>
 __device__ __forceinline__ void swap_sel(bool on, float4 (&v)[1 << RB]) {
@@ -481,9 +486,15 @@ __device__ __forceinline__ float2 cmul_any(float2 x, float2 y) {
     return make_float2(x.x * y.x - x.y * y.y, x.x * y.y + x.y * y.x);
 }
 __device__ __forceinline__ void turns_apply(float2 e, float &re, float &im) {
+#ifdef QSB_TURNS_SCALAR
     const float nr = __fmaf_rn(re, e.x, -__fmul_rn(im, e.y));
     im = __fmaf_rn(re, e.y, __fmul_rn(im, e.x));
     re = nr;
+#else
+    const float2 r = cmul(e, make_float2(re, im));  // packed: FMUL, FMUL, FFMA2
+    re = r.x;
+    im = r.y;
+#endif
 }
 __device__ __forceinline__ void turns_mul(uint32_t t, float &re, float &im) {
     const float ang = (float)(int)t * 1.46291807926715968e-9f;  // 2 pi / 2^32

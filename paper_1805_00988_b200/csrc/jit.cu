@@ -274,6 +274,11 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
     // swap_sel: no divergent branch), 0 a branch around the body
     int sel_mode = 1;
     if (const char *e = std::getenv("QSB_JIT_SEL")) sel_mode = std::atoi(e);
+    // the selected product's form: scalar in place (phase_sel) or packed
+    // (phase_sel_ct); QSB_JIT_SEL_FORM=ct / cs
+    const char *sel_form = "phase_sel";
+    if (const char *e = std::getenv("QSB_JIT_SEL_FORM"))
+        if (!std::strcmp(e, "ct")) sel_form = "phase_sel_ct";
     // planar register layout (fused_dev.cuh: pphase / ppair): 0 (default:
     // measured slower on B200 — the packed results land in fresh register
     // pairs and ptxas copies them home around the uniform branches; QFT(30)
@@ -300,6 +305,9 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
     int nconst = 0;
     std::string src;
     src.reserve(8192 + (size_t)p.nops * 200);
+    // QSB_JIT_TURNS=cs: combined runs multiply with the scalar in-place form
+    if (const char *e = std::getenv("QSB_JIT_TURNS"))
+        if (!std::strcmp(e, "cs")) src += "#define QSB_TURNS_SCALAR 1\n";
     src += "#include \"fused_dev.cuh\"\nusing namespace qsb;\nstruct GenProg {\n";
     src += planar ? "  static constexpr bool kPlanar = true;\n" : "  static constexpr bool kPlanar = false;\n";
     src += "  template <int RB>\n"
@@ -344,7 +352,7 @@ std::string generate(const FParams &p, int K, int RB, bool param = false) {
             if (is_phase) {
                 const int R = (op.variant - kPhaseVariant) / 2, odd = (op.variant - kPhaseVariant) % 2;
                 std::snprintf(b, sizeof b, " %s<%d, %s, RB>(%s, make_float2(",
-                              planar ? (in_branch ? "pphase_sel_cs" : "pphase_sel") : "phase_sel", R,
+                              planar ? (in_branch ? "pphase_sel_cs" : "pphase_sel") : sel_form, R,
                               odd ? "true" : "false", ltest.c_str());
                 out += b;
                 ent(out, oi, 6);
