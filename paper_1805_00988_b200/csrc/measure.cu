@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(32)
                  const long long *__restrict__ bmap, uint64_t nblk, double *__restrict__ sblock,
                  double *__restrict__ start, double *__restrict__ total, unsigned long long *__restrict__ nslow,
                  double *__restrict__ fine0, double *__restrict__ fine1) {
-    __shared__ double sd0[kMapBlock], sd1[kMapBlock], shi[kMapBlock], slo[kMapBlock];
+    __shared__ double sd0[kMapBlock], sd1[kMapBlock], shi[kMapBlock], slo[kMapBlock], sg0[kMapBlock];
     __shared__ int sfl[kMapBlock];
     __shared__ __align__(16) double sprob[1 << kChunkLog];
     __shared__ __align__(8) uint64_t wbar;
@@ -755,7 +755,13 @@ __global__ void __launch_bounds__(32)
                 s = __longlong_as_double(eb);
                 continue;
             }
-            // irregular block: stage its chunk data, lane 0 walks it exactly
+            // irregular block (a binade crossing, a failed trajectory or the
+            // exact-zero prefix inside): stage its chunk data; each lane
+            // composes the parity maps of its 8 consecutive chunks when they
+            // are valid and share one binade (the M4a argument on a segment),
+            // the warp steps through the 32 segments — one step per uniform
+            // segment — and lane 0 walks only the other segments chunk by
+            // chunk (re-summing, with the whole warp, a chunk that crosses)
             if (lane == 0) sblock[b] = -1.0;
             const uint64_t k0 = b * kMapBlock;
             const int m = (int)((nch - k0) < (uint64_t)kMapBlock ? (nch - k0) : kMapBlock);
@@ -763,60 +769,107 @@ __global__ void __launch_bounds__(32)
                 sd0[j] = d0[k0 + j];
                 sd1[j] = d1[k0 + j];
                 shi[j] = hi[k0 + j];
-                slo[j] = binade_lo(g0[k0 + j]);
+                sg0[j] = g0[k0 + j];
+                slo[j] = binade_lo(sg0[j]);
                 sfl[j] = flags[k0 + j];
             }
             __syncwarp();
-            // lane 0 runs through the valid chunks alone; the warp joins only
-            // for a chunk that must be re-summed (a binade crossing)
-            for (int j = 0; j < m;) {
-                int bad = m;
-                if (lane == 0) {
-                    // software-pipelined: chunk j+1's shared-memory values are
-                    // loaded while chunk j's add / compares (the only work that
-                    // waits for s) run
-                    double na0 = sd0[j], na1 = sd1[j], nh = shi[j], nl = slo[j];
-                    int nf = sfl[j];
-                    for (; j < m; ++j) {
-                        const double a0 = na0, a1 = na1, h = nh, l = nl;
-                        const int f = nf;
-                        if (j + 1 < m) {
-                            na0 = sd0[j + 1];
-                            na1 = sd1[j + 1];
-                            nh = shi[j + 1];
-                            nl = slo[j + 1];
-                            nf = sfl[j + 1];
+            constexpr int kSeg = kMapBlock / 32;
+            const int c0 = lane * kSeg, c1 = c0 + kSeg < m ? c0 + kSeg : m;
+            PMap seg{0, 0};
+            long long segE = -1;
+            bool seg_ok = c0 < c1;
+            for (int j = c0; j < c1 && seg_ok; ++j) {
+                const long long gb = __double_as_longlong(sg0[j]);
+                const long long E = (long long)((unsigned long long)gb >> 52);
+                const int f = sfl[j];
+                if (!(f & kFlagOk) || (f & kFlagExact0) || E < 2 || (j > c0 && E != segE)) {
+                    seg_ok = false;
+                    break;
+                }
+                segE = E;
+                PMap mj;
+                mj.a0 = __double_as_longlong(__dadd_rn(sg0[j], sd0[j])) - gb;
+                mj.a1 = __double_as_longlong(__dadd_rn(__longlong_as_double(gb + 1), sd1[j])) - (gb + 1);
+                seg = pcompose(seg, mj);
+            }
+            double seg_start = -1.0;  // this lane's segment start when taken in one step
+            for (int L = 0; L * kSeg < m; ++L) {
+                const int l0 = L * kSeg, l1 = l0 + kSeg < m ? l0 + kSeg : m;
+                const long long a0 = __shfl_sync(0xffffffffu, seg.a0, L), a1 = __shfl_sync(0xffffffffu, seg.a1, L);
+                const long long e = __shfl_sync(0xffffffffu, segE, L);
+                const bool sok = __shfl_sync(0xffffffffu, (int)seg_ok, L) != 0;
+                const long long sb = __double_as_longlong(s);
+                const long long eb = sb + ((sb & 1) ? a1 : a0);
+                if (sok && (sb >> 52) == e && (eb >> 52) == e) {  // start and end inside the segment's binade
+                    if (lane == L) seg_start = s;
+                    s = __longlong_as_double(eb);
+                    continue;
+                }
+                // lane 0 runs through the segment's valid chunks alone; the
+                // warp joins only for a chunk that must be re-summed
+                for (int j = l0; j < l1;) {
+                    int bad = l1;
+                    if (lane == 0) {
+                        // software-pipelined: chunk j+1's shared-memory values
+                        // load while chunk j's add / compares (the only work
+                        // that waits for s) run
+                        double na0 = sd0[j], na1 = sd1[j], nh = shi[j], nl = slo[j];
+                        int nf = sfl[j];
+                        for (; j < l1; ++j) {
+                            const double x0 = na0, x1 = na1, h = nh, l = nl;
+                            const int f = nf;
+                            if (j + 1 < l1) {
+                                na0 = sd0[j + 1];
+                                na1 = sd1[j + 1];
+                                nh = shi[j + 1];
+                                nl = slo[j + 1];
+                                nf = sfl[j + 1];
+                            }
+                            start[k0 + j] = s;
+                            double en;
+                            bool valid;
+                            if (f & kFlagExact0) {
+                                valid = (s == s_start);
+                                en = x0;
+                            } else {
+                                const bool odd = (__double_as_longlong(s) & 1ll) != 0;
+                                en = __dadd_rn(s, odd ? x1 : x0);
+                                valid = (f & kFlagOk) && s >= l && s < h && en < h;
+                            }
+                            if (!valid) {
+                                bad = j;
+                                break;
+                            }
+                            s = en;
                         }
-                        start[k0 + j] = s;
-                        double en;
-                        bool valid;
-                        if (f & kFlagExact0) {
-                            valid = (s == s_start);
-                            en = a0;
-                        } else {
-                            const bool odd = (__double_as_longlong(s) & 1ll) != 0;
-                            en = __dadd_rn(s, odd ? a1 : a0);
-                            valid = (f & kFlagOk) && s >= l && s < h && en < h;
-                        }
-                        if (!valid) {
-                            bad = j;
-                            break;
-                        }
-                        s = en;
                     }
+                    bad = __shfl_sync(0xffffffffu, bad, 0);
+                    s = __shfl_sync(0xffffffffu, s, 0);
+                    if (bad >= l1) break;
+                    const bool record = fine0 && clog == kChunkLog;
+                    s = warp_walk_chunk(amps, k0 + bad, clog, s, sprob,
+                                        record ? fine0 + (k0 + bad) * kFinePer : nullptr, &wbar, wphase);
+                    if (lane == 0) {
+                        ++slow;
+                        flags[k0 + bad] = sfl[bad] | kFlagWalked | (record ? kFlagFineAbs : 0);
+                    }
+                    __syncwarp();
+                    j = bad + 1;
                 }
-                bad = __shfl_sync(0xffffffffu, bad, 0);
                 s = __shfl_sync(0xffffffffu, s, 0);
-                if (bad >= m) break;
-                const bool record = fine0 && clog == kChunkLog;
-                s = warp_walk_chunk(amps, k0 + bad, clog, s, sprob, record ? fine0 + (k0 + bad) * kFinePer : nullptr,
-                                    &wbar, wphase);
-                if (lane == 0) {
-                    ++slow;
-                    flags[k0 + bad] = sfl[bad] | kFlagWalked | (record ? kFlagFineAbs : 0);
+            }
+            // the chunk starts of the segments taken in one step: the segment
+            // start plus each chunk's map, in order (exact, same binade)
+            if (seg_start >= 0.0) {
+                long long cb = __double_as_longlong(seg_start);
+                for (int j = c0; j < c1; ++j) {
+                    start[k0 + j] = __longlong_as_double(cb);
+                    const long long gb = __double_as_longlong(sg0[j]);
+                    const long long inc = (cb & 1) ? __double_as_longlong(__dadd_rn(__longlong_as_double(gb + 1), sd1[j])) - (gb + 1)
+                                                   : __double_as_longlong(__dadd_rn(sg0[j], sd0[j])) - gb;
+                    cb += inc;
                 }
-                __syncwarp();
-                j = bad + 1;
             }
             __syncwarp();
             s = __shfl_sync(0xffffffffu, s, 0);
