@@ -344,21 +344,31 @@ def run_ours(args):
         # outcomes read back — reported beside e2e, which moves the whole
         # 8 GiB register both ways every step
         try:
-            st.reset(0)
-            fusion.run(st, layer_passes)
-            st.sample_outcomes(1000, 0)
-            st.flush()
-            reps = 10
-            t0 = time.perf_counter()
-            for k in range(reps):
-                st.reset(0)
-                fusion.run(st, layer_passes)
-                shots = st.sample_outcomes(1000, k)
-            dt_w = time.perf_counter() - t0
+            wf = {}
+            for mode in ("reset_then_passes", "reset_folded_into_first_pass"):
+                folded = mode == "reset_folded_into_first_pass"
+
+                def wf_step(k):
+                    if folded:  # execute(..., initial_basis=0): the first pass writes |0>'s tiles
+                        fusion.run(st, layer_passes, from_basis=0)
+                    else:
+                        st.reset(0)
+                        fusion.run(st, layer_passes)
+                    return st.sample_outcomes(1000, k)
+
+                wf_step(0)
+                st.flush()
+                reps = 10
+                t0 = time.perf_counter()
+                for k in range(reps):
+                    shots = wf_step(k)
+                wf[mode] = reps * n / (time.perf_counter() - t0)
             e2e["circuit_workflow"] = {
-                "value": reps * n / dt_w, "unit": UNIT, "steps": reps, "d2h_bytes_per_step": shots.nbytes,
-                "timing": "host wall clock: State.reset + the H layer as fused passes + 1000 exact shots "
-                          "(sample_outcomes, int64 outcomes to the host) per step"}
+                "value": wf["reset_folded_into_first_pass"], "unit": UNIT, "steps": reps,
+                "d2h_bytes_per_step": shots.nbytes, "reset_then_passes_value": wf["reset_then_passes"],
+                "timing": "host wall clock: |0> + the H layer as fused passes (the reset folded into the first "
+                          "pass: execute(..., initial_basis=0); reset_then_passes_value = State.reset first) + "
+                          "1000 exact shots (sample_outcomes, int64 outcomes to the host) per step"}
         except Exception as exc:  # noqa: BLE001
             e2e["circuit_workflow"] = {"error": f"{type(exc).__name__}: {exc}"}
 

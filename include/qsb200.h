@@ -151,6 +151,15 @@ int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile,
 enum { QS_FUSED_COMBINE_PHASES = 1 };
 int qs_apply_fused_ex(qs_state *s, const int32_t *tile_qubits, int ntile,
                       const qs_op *ops, int nops, int flags);
+/* qs_reset(s, basis) followed by qs_apply_fused_ex(...), as ONE HBM write:
+ * the pass's tiles are written as |basis> (zeros, 1 at the basis amplitude)
+ * instead of being loaded, so the register is never cleared separately.
+ * Same result bit for bit.  Falls back to the two calls when the pass has
+ * no tile kernel (small registers, unusual tile shapes) or is complex128.
+ * New entry point; pairsim's equivalent is new_state + run_circuit
+ * (pkg/src/pairsim/state.py:122-143, circuits.py:171-192). */
+int qs_apply_fused_from_basis(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops,
+                              int flags, uint64_t basis);
 /* Fused pass with fp64 gate entries (the form a complex128 register takes;
  * on a complex64 register the entries are rounded to float32 and the call
  * is qs_apply_fused). */

@@ -31,7 +31,7 @@ EXPORTS = (
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
     "qs_apply_controlled_controlled_gate", "qs_apply_gate_f64", "qs_apply_controlled_gate_f64",
-    "qs_apply_controlled_controlled_gate_f64", "qs_apply_fused", "qs_apply_fused_ex", "qs_apply_fused_f64", "qs_swap_qubits",
+    "qs_apply_controlled_controlled_gate_f64", "qs_apply_fused", "qs_apply_fused_ex", "qs_apply_fused_from_basis", "qs_apply_fused_f64", "qs_swap_qubits",
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
     "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
@@ -103,6 +103,7 @@ def _declare(L):
         "qs_apply_fused": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
         "qs_apply_fused_f64": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32], i32),
         "qs_apply_fused_ex": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32, i32], i32),
+        "qs_apply_fused_from_basis": ([vp, ctypes.POINTER(ctypes.c_int32), i32, vp, i32, i32, ctypes.c_uint64], i32),
         "qs_swap_qubits": ([vp, i32, i32], i32),
         "qs_get_amplitudes": ([vp, u64, u64, vp], i32),
         "qs_set_amplitudes": ([vp, u64, u64, vp], i32),

@@ -171,7 +171,7 @@ def lower_ops(circuit: Circuit, double: bool = False) -> list:
 
 
 def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: int | None = None,
-            reorder: bool | None = None, exact: bool = True):
+            reorder: bool | None = None, exact: bool = True, initial_basis: int | None = None):
     """Apply `circuit` to a device State in place; returns the per-draw outcomes
     of a trailing SampleMeasure (or None).
 
@@ -180,7 +180,10 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
     north_star rtol 1e-5), faster: the fused planner may exchange gates on
     disjoint qubits (reorder) and compiled passes combine runs of diagonal
     gates into one product per amplitude (QS_FUSED_COMBINE_PHASES).
-    reorder alone (default: QSB_FUSE_REORDER == "1") enables only the first."""
+    reorder alone (default: QSB_FUSE_REORDER == "1") enables only the first.
+    initial_basis=b: start from |b> (pairsim's new_state + run_circuit); with
+    fuse=True the reset is folded into the first fused pass (its tiles are
+    written as |b> instead of loaded), same bits as state.reset(b) first."""
     if circuit.num_qubits != state.num_qubits:
         raise ValueError("circuit and state widths differ")
     double = getattr(state, "is_double", False)
@@ -193,8 +196,10 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
 
             reorder = os.environ.get("QSB_FUSE_REORDER") == "1" or not exact
         fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits, reorder=reorder),
-                   combine=not exact and not double)
+                   combine=not exact and not double, from_basis=initial_basis)
     else:
+        if initial_basis is not None:
+            state.reset(int(initial_basis))
         for kind, t, cm, m in ops:
             fusion._single(state, kind, t, cm, m)
     last = circuit.instructions[-1] if circuit.instructions else None

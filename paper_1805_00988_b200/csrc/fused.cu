@@ -245,6 +245,7 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     std::unique_ptr<FParams> holder(new FParams);  // ~28 KB: off the stack
     FParams &p = *holder;
     std::memset(&p, 0, sizeof p);
+    p.synth_basis = -1;  // load the tiles (qs_apply_fused_from_basis sets it on the first group)
     p.n = n;
     p.K = K;
     p.nwbits = FB - 5 - RB;
@@ -559,7 +560,8 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
     return QS_OK;
 }
 
-int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops, int flags) {
+int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops, int flags,
+              long long basis) {
     NvtxRange nvtx_range("qsb fused pass");
     const int n = s->num_qubits;
     uint64_t tile_mask = 0;
@@ -588,6 +590,10 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
     const int K = __builtin_popcountll(tile_mask);
     const uint64_t low_mask = (1ull << kLow) - 1ull;
     const bool kernel_ok = n >= 10 && K >= 10 && K <= 13 && (tile_mask & low_mask) == low_mask;
+    if (basis >= 0 && !kernel_ok) {  // no tile kernel to write |basis> with: reset, then the ops
+        if (int rc = qs_reset(s, (uint64_t)basis)) return rc;
+        basis = -1;
+    }
     if (!kernel_ok && n <= kSmallMaxQubits) return run_small(s, ops, nops);
     if (!kernel_ok) {
         // Unsupported tile shape on a large register: one sweep per op — the
@@ -623,6 +629,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         std::vector<FParams> groups;
         if (plan_pass(s, tile_mask, ops, nops, jrb, groups) == QS_OK) {
             for (FParams &g : groups) g.combine = (flags & QS_FUSED_COMBINE_PHASES) ? 1 : 0;
+            groups[0].synth_basis = basis;  // the first launch group writes |basis> (or loads: -1)
             std::vector<void *> fns;
             for (const FParams &g : groups) {
                 void *fn = recording ? jit_lookup(s->device, g, K, jrb)
@@ -656,6 +663,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         const int rc = plan_pass(s, tile_mask, ops, nops, RB, groups);
         if (rc) return rc;
     }
+    groups[0].synth_basis = basis;
     for (const FParams &g : groups) {
         int rc;
         switch (K) {

@@ -68,6 +68,10 @@ struct FParams {
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
     int l2hint;  // TMA copies with an L2 evict_first policy
     int combine;  // generated programs: combine runs of unit-modulus diagonal ops (exact = False)
+    // >= 0: the register is |synth_basis> — the producer writes each tile's
+    // contents (zeros, 1 at the basis amplitude) instead of loading them
+    // (qs_apply_fused_from_basis: reset + first pass in one HBM write)
+    long long synth_basis;
     uint64_t ntiles;
     // Dynamic tile scheduler: the producers take tiles from this counter
     // (zero at launch; the last CTA to find it exhausted zeroes it again).
@@ -785,6 +789,36 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             }
             const uint64_t base = tile_base(t, p);
             pending[b] = base;
+            if constexpr (UnitTraits<V>::kHalf) {
+                if (p.synth_basis >= 0) {  // |basis>: write the tile, no load
+                    if (i >= kNB) bulk_wait_read0();  // this lane's stores of the buffer are read out
+                    __syncwarp();
+                    for (int u = lane; u < kBufF4; u += 32) buf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    __syncwarp();
+                    if (lane == 0) {
+                        const uint64_t bb = (uint64_t)p.synth_basis;
+                        uint64_t tmask = 0, local = 0;
+                        for (int q = 0; q < K; ++q) {
+                            tmask |= 1ull << p.qpos[q];
+                            local |= ((bb >> p.qpos[q]) & 1ull) << q;
+                        }
+                        if ((bb & ~tmask) == base) {
+                            float4 &w = buf[(local >> kLowQ) * 33u + ((local & ((1u << kLowQ) - 1u)) >> 1)];
+                            if (local & 1u)
+                                w.z = 1.f;
+                            else
+                                w.x = 1.f;
+                        }
+                    }
+                    fence_async_smem();  // the tile's bytes may reach the bulk store unchanged
+                    __syncwarp();
+                    if (lane == 0) {
+                        tile_id[b] = t;
+                        mbar_arrive(&full[b]);  // release: the compute warps see the writes
+                    }
+                    continue;
+                }
+            }
             if (lane == 0) {
                 tile_id[b] = t;
                 if (p.dry == 4)

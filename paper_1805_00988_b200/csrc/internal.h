@@ -98,7 +98,8 @@ int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
 int run_cdf_extend(qs_state *s, double start, double *end);
 int run_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
                      uint64_t base, uint64_t gdim, int is_last, int64_t *out);
-int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops, int flags = 0);
+int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops, int flags = 0,
+              long long basis = -1);
 
 }  // namespace qsb
 

@@ -377,6 +377,20 @@ int qs_apply_fused_ex(qs_state *s, const int32_t *tile_qubits, int ntile, const 
     return run_fused(s, tile_qubits, ntile, ops, nops, flags);
 }
 
+int qs_apply_fused_from_basis(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops,
+                              int flags, uint64_t basis) {
+    CHECK_HANDLE(s);
+    if (s->num_qubits < 64 && basis >= (1ull << s->num_qubits))
+        return set_error(QS_ERR_INDEX, "basis index out of range");
+    if (nops == 0 || s->prec == QS_DOUBLE) {  // nothing to fuse with / complex128: reset, then the pass
+        if (int rc = qs_reset(s, basis)) return rc;
+        return qs_apply_fused_ex(s, tile_qubits, ntile, ops, nops, flags);
+    }
+    if (!ops || !tile_qubits) return set_error(QS_ERR_NULL, "null op list or tile qubit list");
+    DeviceGuard guard(s->device);
+    return run_fused(s, tile_qubits, ntile, ops, nops, flags, (long long)basis);
+}
+
 int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *ops, int nops) {
     return qs_apply_fused_ex(s, tile_qubits, ntile, ops, nops, 0);
 }

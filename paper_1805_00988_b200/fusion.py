@@ -350,10 +350,19 @@ def jit_stats() -> dict:
     return {"compiled": c.value, "cache_hits": h.value, "failed": f.value}
 
 
-def run(state, passes: list[Pass], combine: bool = False) -> None:
+def run(state, passes: list[Pass], combine: bool = False, from_basis: int | None = None) -> None:
     """Launch the planned passes on a State (asynchronous on its stream).
     combine=True: runs of unit-modulus diagonal ops as one product per
-    amplitude (State.apply_fused; not bit-exact)."""
+    amplitude (State.apply_fused; not bit-exact).  from_basis=b: the register
+    starts as |b> (State.reset(b)), folded into the first pass when it is a
+    fused one — its tiles are written as |b> instead of loaded."""
+    if from_basis is not None:
+        if passes and len(passes[0].ops) > 1:
+            first = passes[0]
+            state.apply_fused(first.tile, first.op_array(), combine=combine, from_basis=from_basis)
+            passes = passes[1:]
+        else:
+            state.reset(int(from_basis))
     for p in passes:
         if len(p.ops) == 1:
             kind, t, cm, m = p.ops[0]

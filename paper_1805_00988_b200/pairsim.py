@@ -376,6 +376,7 @@ def run_circuit(circuit, precision: Precision = Precision.SINGLE, seed=None, exe
     from .circuits import execute
 
     state = new_state(circuit.num_qubits, precision, memory_budget)
-    outcomes = execute(circuit, state.device_state, seed=seed, fuse=fuse)
+    # the register is |0>: the first fused pass writes its tiles instead of loading them
+    outcomes = execute(circuit, state.device_state, seed=seed, fuse=fuse, initial_basis=0)
     hist = MeasurementHistogram.from_outcomes(outcomes) if outcomes is not None else None
     return state, hist

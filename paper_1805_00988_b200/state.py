@@ -209,16 +209,26 @@ class State:
         N.check(fn(self.handle, int(control1), int(control2), int(target), mp))
         return self
 
-    def apply_fused(self, tile_qubits, ops: np.ndarray, combine: bool = False) -> "State":
+    def apply_fused(self, tile_qubits, ops: np.ndarray, combine: bool = False,
+                    from_basis: int | None = None) -> "State":
         """One fused HBM pass (see fusion.py for the planner).  `ops` is an
         OP_DTYPE (float32 entries) or OP64_DTYPE (fp64 entries) record array.
         combine=True (not bit-exact, QS_FUSED_COMBINE_PHASES): runs of
-        unit-modulus diagonal ops become one product per amplitude."""
+        unit-modulus diagonal ops become one product per amplitude.
+        from_basis=b: reset to |b> first, folded into the pass (its tiles are
+        written as |b> instead of loaded: qs_apply_fused_from_basis)."""
         tq = np.ascontiguousarray(np.asarray(tile_qubits, dtype=np.int32))
         wide = np.asarray(ops).dtype == N.OP64_DTYPE
         ops = np.ascontiguousarray(ops, dtype=N.OP64_DTYPE if wide else N.OP_DTYPE)
         L = N.lib()
         tp = tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        if from_basis is not None:
+            if wide:
+                self.reset(int(from_basis))
+            else:
+                N.check(L.qs_apply_fused_from_basis(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size),
+                                                    N.QS_FUSED_COMBINE_PHASES if combine else 0, int(from_basis)))
+                return self
         if wide:
             N.check(L.qs_apply_fused_f64(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size)))
         elif combine:

@@ -249,3 +249,51 @@ def test_program_variants_same_bits(tmp_path, env):
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0]["failed"] == 0 and outs[1]["failed"] == 0 and outs[1]["compiled"] >= 1
     assert outs[0]["d"] == outs[1]["d"]
+
+
+class TestFromBasis:
+    """qs_apply_fused_from_basis / execute(..., initial_basis=b): the reset is
+    folded into the first fused pass (tiles written as |b>, not loaded).  The
+    register must equal reset(b) + the same passes bit for bit, whatever it
+    held before (filled with noise here), for bases inside every kind of tile
+    position, on the compiled programs and the interpreter, and through the
+    fallbacks (small registers, complex128)."""
+
+    @pytest.mark.parametrize("n,circ_name", [(12, "qft"), (16, "layered"), (20, "hlayer"), (20, "qft"),
+                                             (21, "random")])
+    @pytest.mark.parametrize("jit", ["2", "0"])
+    def test_equals_reset_then_passes(self, n, circ_name, jit, monkeypatch):
+        from paper_1805_00988_b200 import build_hadamard_layer, layered_random_circuit, random_circuit
+
+        monkeypatch.setenv("QSB_FUSED_JIT", jit)
+        rng = np.random.default_rng(n)
+        circ = {"qft": lambda: build_qft(n), "layered": lambda: layered_random_circuit(n, 4, seed=3),
+                "hlayer": lambda: build_hadamard_layer(n),
+                "random": lambda: random_circuit(n, 12, np.random.default_rng(5))}[circ_name]()
+        noise = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)).astype(np.complex64)
+        for b in (0, (1 << n) - 1, int(rng.integers(0, 1 << n)), 1 << (n - 1), 37):
+            ref = State(n)
+            ref.set_amplitudes(noise)
+            ref.reset(b)
+            execute(circ, ref, fuse=True)
+            got = State(n)
+            got.set_amplitudes(noise)
+            execute(circ, got, fuse=True, initial_basis=b)
+            assert got.amplitudes().tobytes() == ref.amplitudes().tobytes(), (n, circ_name, b)
+            ref.close()
+            got.close()
+
+    def test_small_double_and_errors(self):
+        for n, prec in ((8, "single"), (14, "double")):
+            circ = build_qft(n)
+            ref = State(n, precision=prec)
+            ref.reset(5)
+            execute(circ, ref, fuse=True)
+            got = State(n, precision=prec)
+            got.set_amplitudes(np.ones(1 << n))
+            execute(circ, got, fuse=True, initial_basis=5)
+            assert got.amplitudes().tobytes() == ref.amplitudes().tobytes()
+        st = State(12)
+        with pytest.raises(IndexError):
+            execute(build_qft(12), st, initial_basis=1 << 12)
+        st.close()
