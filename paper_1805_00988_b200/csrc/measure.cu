@@ -260,7 +260,19 @@ enum : int { kFlagOk = 1, kFlagExact0 = 2, kFlagWalked = 4, kFlagFineAbs = 8 };
 // 256th amplitude of a 4096-amplitude chunk, so a draw can start its exact
 // walk at the last of the chunk's 16 sub-blocks whose running value is still
 // <= u instead of at the chunk start (16x less walking per draw).
-constexpr int kFineLog = 8, kFinePer = 1 << (kChunkLog - kFineLog);
+// Fine starts: the exact running value every 2^kFineLog amplitudes of a
+// chunk, so a draw walks at most 64 amplitudes.  Stored coarse-first: the 16
+// values at multiples of 256 in slots 0..15, then per 256-block the three at
+// +64 / +128 / +192 (slots 16 + 3 q + r - 1): a draw reads the 16 coarse
+// values, then 3 fine ones.  Slot-major in memory (value (chunk, slot) at
+// slot * nch + chunk), so M3's lanes — 32 consecutive chunks — write each
+// slot as one coalesced 256-B row.
+constexpr int kFineLog = 6, kFinePer = 1 << (kChunkLog - kFineLog);
+constexpr int kCoarseStep = 4, kCoarse = kFinePer / kCoarseStep;  // 16 coarse values (every 256)
+__host__ __device__ __forceinline__ int fine_slot(int i) {  // i: position / 64
+    return (i & (kCoarseStep - 1)) == 0 ? i / kCoarseStep
+                                        : kCoarse + (kCoarseStep - 1) * (i / kCoarseStep) + (i & (kCoarseStep - 1)) - 1;
+}
 
 // ---- M3: guessed trajectories -------------------------------------------------
 // One warp owns 32 consecutive chunks; every 32-element step the warp loads a
@@ -301,7 +313,7 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
     double t0 = g0, t1 = g1;
     // an exact0 chunk's running values ARE the CDF (its true start is
     // `start`): record them absolutely (kFlagFineAbs), position 0 included
-    if (fine0 && active && exact0) fine0[my * kFinePer] = g0;
+    if (fine0 && active && exact0) fine0[my] = g0;  // slot 0
     const int rows = (int)((nch - first) < 32 ? (nch - first) : 32);
     for (uint64_t j0 = 0; j0 < C; j0 += 32) {
         const int width = (int)((C - j0) < 32 ? (C - j0) : 32);
@@ -326,10 +338,10 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
             const uint64_t pos = j0 + 32;  // elements summed so far
             if (fine0 && (pos & ((1u << kFineLog) - 1)) == 0 && pos < C) {
                 if (exact0) {
-                    fine0[my * kFinePer + (pos >> kFineLog)] = t0;
+                    fine0[(uint64_t)fine_slot((int)(pos >> kFineLog)) * nch + my] = t0;
                 } else {
-                    fine0[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t0, g0);  // exact while in the binade
-                    fine1[my * kFinePer + (pos >> kFineLog)] = __dsub_rn(t1, g1);
+                    fine0[(uint64_t)fine_slot((int)(pos >> kFineLog)) * nch + my] = __dsub_rn(t0, g0);  // exact in the binade
+                    fine1[(uint64_t)fine_slot((int)(pos >> kFineLog)) * nch + my] = __dsub_rn(t1, g1);
                 }
             }
         }
@@ -393,7 +405,7 @@ __device__ __forceinline__ void tb_issue(const float2 *__restrict__ rows, uint64
 }
 
 __global__ void __launch_bounds__(32)
-    k_trajectories_bulk(const float2 *__restrict__ amps, double start, const double *__restrict__ g,
+    k_trajectories_bulk(const float2 *__restrict__ amps, uint64_t nch, double start, const double *__restrict__ g,
                         double *__restrict__ g0out, double *__restrict__ d0, double *__restrict__ d1,
                         double *__restrict__ hiout, int *__restrict__ flags, double *__restrict__ fine0,
                         double *__restrict__ fine1) {
@@ -423,7 +435,7 @@ __global__ void __launch_bounds__(32)
         hi = binade_hi(g0);
     }
     double t0 = g0, t1 = g1;
-    if (fine0 && exact0) fine0[my * kFinePer] = g0;
+    if (fine0 && exact0) fine0[my] = g0;  // slot 0
     constexpr int kCols = (1 << kChunkLog) / kTbCols;
     constexpr int kFineEvery = (1 << kFineLog) / kTbCols;
     for (int c = 0; c < kCols; ++c) {
@@ -443,10 +455,10 @@ __global__ void __launch_bounds__(32)
         if (fine0 && (c + 1) % kFineEvery == 0 && c + 1 < kCols) {
             const int f = (c + 1) / kFineEvery;
             if (exact0) {
-                fine0[my * kFinePer + f] = t0;
+                fine0[(uint64_t)fine_slot(f) * nch + my] = t0;
             } else {
-                fine0[my * kFinePer + f] = __dsub_rn(t0, g0);  // exact while in the binade
-                fine1[my * kFinePer + f] = __dsub_rn(t1, g1);
+                fine0[(uint64_t)fine_slot(f) * nch + my] = __dsub_rn(t0, g0);  // exact while in the binade
+                fine1[(uint64_t)fine_slot(f) * nch + my] = __dsub_rn(t1, g1);
             }
         }
     }
@@ -604,7 +616,7 @@ __global__ void __launch_bounds__(kMapBlock)
 // 2^kFineLog amplitudes.  Returns the end value in every lane.
 template <class A>
 __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, int clog, double s, double *sp,
-                                  double *fine_abs, uint64_t *bar, uint32_t &phase) {
+                                  double *fine_abs, uint64_t fstride, uint64_t *bar, uint32_t &phase) {
     const int lane = threadIdx.x & 31;
     const int C = 1 << clog;
     const A *p = amps + ((uint64_t)chunk << clog);
@@ -636,14 +648,15 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
         for (int j = lane; j < C; j += 32) sp[j] = prob(p[j]);
     }
     __syncwarp();
-    constexpr int S = 1 << kFineLog;  // sub-block: the fine-start spacing
+    // sub-blocks of 256 amplitudes (one per lane, 16 per chunk); fine starts
+    // every 64 (kFineLog): at each sub-block start and at +64/+128/+192
+    constexpr int S = 1 << (kFineLog + 2);
+    constexpr int kSub = S >> kFineLog;  // fine starts per sub-block
     const int nsb = C / S;
     double res = s;
-    if (nsb < 2) {  // short chunk: plain sequential sum
-        if (lane == 0) {
-            if (fine_abs) fine_abs[0] = res;
+    if (nsb < 2) {  // short chunk: plain sequential sum (fine starts only for full chunks)
+        if (lane == 0)
             for (int j = 0; j < C; ++j) res = __dadd_rn(res, sp[j]);
-        }
         __syncwarp();
         return __shfl_sync(0xffffffffu, res, 0);
     }
@@ -651,8 +664,10 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
     // even / odd start g0, g1 = g0 + ulp near its guessed start (the chunk
     // start plus a plain sum of the earlier sub-blocks) is, while both
     // trajectories stay in g0's binade, the true sum's offset for a true
-    // start of that parity in that binade; lane 0 then chains the sub-blocks
-    // exactly and re-sums in order only those that leave their binade.
+    // start of that parity in that binade (so are its partial sums at +64,
+    // +128, +192: the fine starts inside the sub-block); lane 0 then chains
+    // the sub-blocks exactly and re-sums in order only those that leave their
+    // binade.
     const double *q = sp + (lane < nsb ? lane : 0) * S;
     double bs = 0.0;  // this sub-block's plain sum (for the guess only)
     if (lane < nsb)
@@ -665,6 +680,7 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
     }
     pre -= bs;
     double g0 = 0.0, d0 = 0.0, d1 = 0.0, hi = 0.0;
+    double m0[kSub - 1], m1[kSub - 1];  // partial offsets at +64, +128, +192
     int ok = 0;
     if (lane < nsb) {
         const double gg = __dadd_rn(s, pre);
@@ -672,9 +688,16 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
         const double g1 = __longlong_as_double(__double_as_longlong(g0) + 1ll);
         hi = binade_hi(g0);
         double t0 = g0, t1 = g1;
-        for (int j = 0; j < S; ++j) {
-            t0 = __dadd_rn(t0, q[j]);
-            t1 = __dadd_rn(t1, q[j]);
+#pragma unroll
+        for (int r = 0; r < kSub; ++r) {
+            for (int j = r << kFineLog; j < (r + 1) << kFineLog; ++j) {
+                t0 = __dadd_rn(t0, q[j]);
+                t1 = __dadd_rn(t1, q[j]);
+            }
+            if (r + 1 < kSub) {
+                m0[r] = __dsub_rn(t0, g0);
+                m1[r] = __dsub_rn(t1, g1);
+            }
         }
         d0 = __dsub_rn(t0, g0);
         d1 = __dsub_rn(t1, g1);
@@ -684,11 +707,24 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
         const double lg0 = __shfl_sync(0xffffffffu, g0, L), ld0 = __shfl_sync(0xffffffffu, d0, L);
         const double ld1 = __shfl_sync(0xffffffffu, d1, L), lhi = __shfl_sync(0xffffffffu, hi, L);
         const int lok = __shfl_sync(0xffffffffu, ok, L);
+        double lm0[kSub - 1], lm1[kSub - 1];
+#pragma unroll
+        for (int r = 0; r < kSub - 1; ++r) {
+            lm0[r] = __shfl_sync(0xffffffffu, m0[r], L);
+            lm1[r] = __shfl_sync(0xffffffffu, m1[r], L);
+        }
         if (lane == 0) {
-            if (fine_abs) fine_abs[L] = res;
+            if (fine_abs) fine_abs[(uint64_t)fine_slot(L * kSub) * fstride] = res;
             const bool odd = (__double_as_longlong(res) & 1ll) != 0;
             const double en = __dadd_rn(res, odd ? ld1 : ld0);
             if (lok && res >= binade_lo(lg0) && res < lhi && en < lhi) {
+                // the whole sub-block stays in the binade: its inner fine
+                // starts are the start plus the trajectory's partial offsets
+                if (fine_abs) {
+#pragma unroll
+                    for (int r = 0; r < kSub - 1; ++r)
+                        fine_abs[(uint64_t)fine_slot(L * kSub + r + 1) * fstride] = __dadd_rn(res, odd ? lm1[r] : lm0[r]);
+                }
                 res = en;
             } else {  // the sub-block leaves its binade (or the guess missed): sum it in order
                 const double *r = sp + L * S;
@@ -698,6 +734,9 @@ __device__ double warp_walk_chunk(const A *__restrict__ amps, uint64_t chunk, in
                     for (int u = 0; u < 8; ++u) pr[u] = r[j + u];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) res = __dadd_rn(res, pr[u]);
+                    const int done = j + 8;
+                    if (fine_abs && (done & ((1 << kFineLog) - 1)) == 0 && done < S)
+                        fine_abs[(uint64_t)fine_slot(L * kSub + (done >> kFineLog)) * fstride] = res;
                 }
             }
         }
@@ -849,7 +888,7 @@ __global__ void __launch_bounds__(32)
                     if (bad >= l1) break;
                     const bool record = fine0 && clog == kChunkLog;
                     s = warp_walk_chunk(amps, k0 + bad, clog, s, sprob,
-                                        record ? fine0 + (k0 + bad) * kFinePer : nullptr, &wbar, wphase);
+                                        record ? fine0 + (k0 + bad) : nullptr, nch, &wbar, wphase);
                     if (lane == 0) {
                         ++slow;
                         flags[k0 + bad] = sfl[bad] | kFlagWalked | (record ? kFlagFineAbs : 0);
@@ -1021,36 +1060,48 @@ __global__ void k_draws(const A *__restrict__ amps, uint64_t nch, int clog, uint
             uint64_t j = 0, hit = C;
             if (fine0 && clog == kChunkLog) {
                 const int f = flags[lo];
-                // the chunk's 16 fine values in 8 16-B loads issued together
-                // (a load-compare-break loop waited a latency per value); the
-                // values are non-decreasing, so the sub-block is the count of
+                // the chunk's fine starts, coarse-first: the 16 values at
+                // multiples of 256 (8 16-B loads issued together), then the
+                // 3 inside the chosen 256-block; the values are
+                // non-decreasing, so each level's pick is the count of
                 // leading values below the cut
                 const bool absf = (f & kFlagFineAbs) != 0;
                 const bool traj = !absf && (f & kFlagOk) && !(f & (kFlagExact0 | kFlagWalked));
                 if (absf || traj) {
-                    const double *fb = (absf || !(__double_as_longlong(s) & 1ll) ? fine0 : fine1) + lo * kFinePer;
-                    double fv[kFinePer];
+                    const double *fb = (absf || !(__double_as_longlong(s) & 1ll) ? fine0 : fine1) + lo;
+                    double fv[kCoarse];  // slot-major: value (lo, slot) at slot * nch + lo
 #pragma unroll
-                    for (int q = 0; q < kFinePer / 2; ++q) {
-                        const double2 x = reinterpret_cast<const double2 *>(fb)[q];
-                        fv[2 * q] = x.x;
-                        fv[2 * q + 1] = x.y;
-                    }
+                    for (int q = 0; q < kCoarse; ++q) fv[q] = fb[(uint64_t)q * nch];
                     // absolute (a walked / exact0 chunk: running values before
-                    // amplitude 256 q) or start + trajectory offset (M3, M4)
+                    // amplitude 64 i) or start + trajectory offset (M3, M4)
                     double fs = absf ? fv[0] : s;
-                    int sb = 0;
+                    int qb = 0;
                     bool go = true;
 #pragma unroll
-                    for (int q = 1; q < kFinePer; ++q) {
+                    for (int q = 1; q < kCoarse; ++q) {
                         const double v = absf ? fv[q] : __dadd_rn(s, fv[q]);
                         go = go && v < cut;
                         if (go) {
-                            sb = q;
+                            qb = q;
                             fs = v;
                         }
                     }
-                    j = (uint64_t)sb << kFineLog;
+                    const double *ff = fb + (uint64_t)(kCoarse + (kCoarseStep - 1) * qb) * nch;
+                    double fw[kCoarseStep - 1];
+#pragma unroll
+                    for (int r = 0; r < kCoarseStep - 1; ++r) fw[r] = ff[(uint64_t)r * nch];
+                    int rb = 0;
+                    go = true;
+#pragma unroll
+                    for (int r = 0; r < kCoarseStep - 1; ++r) {
+                        const double v = absf ? fw[r] : __dadd_rn(s, fw[r]);
+                        go = go && v < cut;
+                        if (go) {
+                            rb = r + 1;
+                            fs = v;
+                        }
+                    }
+                    j = (uint64_t)(qb * kCoarseStep + rb) << kFineLog;
                     s = fs;
                 }
             }
@@ -1273,7 +1324,7 @@ static int cdf_scratch(qs_state *s, int64_t k, CdfScratch &c) {
     c.pmap = (long long *)(b + 7 * nch + 2);
     c.bmap = c.pmap + 2 * nch;
     c.sblock = (double *)(c.bmap + 4 * c.nblk);
-    // fine values 64-B aligned (k_draws reads them as double2)
+    // fine values 64-B aligned
     c.fine0 = fine ? (double *)(((uintptr_t)(c.sblock + c.nblk) + 63) & ~(uintptr_t)63) : nullptr;
     c.fine1 = fine ? c.fine0 + kFinePer * nch : nullptr;
     c.flags = (int *)(b + nd);
@@ -1307,7 +1358,7 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
         if constexpr (std::is_same<A, float2>::value) {
             if (bulk)
                 k_trajectories_bulk<<<(unsigned)(c.nch / 32), 32, 0, s->stream>>>(
-                    amps, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
+                    amps, c.nch, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
         }
         if (!bulk)
             k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
