@@ -476,36 +476,6 @@ __global__ void __launch_bounds__(32)
     }
 }
 
-// sequential re-sum of one chunk from an exact start (the reference's loop)
-__device__ double walk_chunk(const double2 *__restrict__ amps, uint64_t chunk, int clog, double s) {
-    const uint64_t C = 1ull << clog;
-    const double2 *p = amps + (chunk << clog);
-    for (uint64_t j = 0; j < C; ++j) s = __dadd_rn(s, prob(p[j]));
-    return s;
-}
-__device__ double walk_chunk(const float2 *__restrict__ amps, uint64_t chunk, int clog, double s) {
-    const uint64_t C = 1ull << clog;
-    const float2 *p = amps + (chunk << clog);
-    uint64_t j = 0;
-    if (C >= 8) {
-        const float4 *q = (const float4 *)p;
-        for (; j + 8 <= C; j += 8) {
-            float4 v0 = q[(j >> 1) + 0], v1 = q[(j >> 1) + 1], v2 = q[(j >> 1) + 2],
-                   v3 = q[(j >> 1) + 3];
-            s = __dadd_rn(s, prob(make_float2(v0.x, v0.y)));
-            s = __dadd_rn(s, prob(make_float2(v0.z, v0.w)));
-            s = __dadd_rn(s, prob(make_float2(v1.x, v1.y)));
-            s = __dadd_rn(s, prob(make_float2(v1.z, v1.w)));
-            s = __dadd_rn(s, prob(make_float2(v2.x, v2.y)));
-            s = __dadd_rn(s, prob(make_float2(v2.z, v2.w)));
-            s = __dadd_rn(s, prob(make_float2(v3.x, v3.y)));
-            s = __dadd_rn(s, prob(make_float2(v3.z, v3.w)));
-        }
-    }
-    for (; j < C; ++j) s = __dadd_rn(s, prob(p[j]));
-    return s;
-}
-
 // ---- M4: resolve true chunk starts ------------------------------------------
 // Inside one binade a double's bit pattern is linear in its value (step u).
 // A chunk whose trajectory check passes moves the running value s to
