@@ -262,7 +262,7 @@ class MultiDeviceState:
 
     def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
         keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
-        return {int(k): int(c) for k, c in zip(keys, counts)}
+        return dict(zip(keys.tolist(), counts.tolist()))  # Python ints, np.unique (sorted) order
 
     def __repr__(self) -> str:
         return f"MultiDeviceState(num_qubits={self.num_qubits}, devices={self.devices})"

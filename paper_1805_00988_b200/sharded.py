@@ -877,7 +877,7 @@ class ShardedState:
 
     def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
         keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
-        return {int(k): int(c) for k, c in zip(keys, counts)}
+        return dict(zip(keys.tolist(), counts.tolist()))  # Python ints, np.unique (sorted) order
 
     def measure_collapse(self, seed=None) -> int:
         """One draw, then the register becomes |outcome> (measure.py:88-99)."""

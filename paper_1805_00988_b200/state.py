@@ -363,7 +363,7 @@ class State:
     def measure(self, samples: int = 1000, seed=None) -> dict[int, int]:
         """Non-destructive sampling: {basis index: count}."""
         keys, counts = np.unique(self.sample_outcomes(samples, seed), return_counts=True)
-        return {int(k): int(c) for k, c in zip(keys, counts)}
+        return dict(zip(keys.tolist(), counts.tolist()))  # Python ints, np.unique (sorted) order
 
     def measure_bitstrings(self, samples: int = 1000, seed=None) -> dict[str, int]:
         """Same draws keyed by the n-bit string (qubit n-1 first)."""
