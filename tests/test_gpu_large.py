@@ -258,6 +258,30 @@ class TestHighAddresses:
         st.close()
 
 
+    def test_from_basis_above_2_31(self):
+        """execute(..., initial_basis=x) on a 32-qubit register holding other
+        data: the first fused pass writes |x>'s tiles (x above 2^31); equal to
+        reset(x) + the same passes over all 2^32 amplitudes."""
+        need(70)
+        n = 32
+        x = (1 << 31) | (1 << 29) | 0x2345
+        circ = Circuit(n, build_qft(n).instructions[:200])
+        states = []
+        for folded in (False, True):
+            st = State(n)
+            for q in range(0, n, 3):
+                st.h(q)  # stale contents the folded reset must overwrite
+            if folded:
+                execute(circ, st, fuse=True, initial_basis=x)
+            else:
+                st.reset(x)
+                execute(circ, st, fuse=True)
+            states.append(st)
+        assert device_equal(view(states[0]), view(states[1]))
+        for st in states:
+            st.close()
+
+
 class TestShardedAt31:
     def test_two_virtual_shards_equal_unsharded(self):
         """A 31-qubit register as two 30-qubit shards (qubit 30 global: qubit
