@@ -331,6 +331,13 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
         }
         return true;
     };
+    // QSB_FUSED_STAGE_PAIRS=k (probe): at most k distinct pair-target bits
+    // per register stage, so a phase-heavy pass re-lays its tile more often
+    // and each stage's lanes can take bits its phases do not test
+    static const int stage_pairs = [] {
+        const char *e = std::getenv("QSB_FUSED_STAGE_PAIRS");
+        return e && *e ? std::atoi(e) : 0;
+    }();
     auto fits = [&](const std::vector<int> &rb, int f) {
         if (std::find(rb.begin(), rb.end(), f) != rb.end()) return true;
         if ((int)rb.size() >= RB) return false;
@@ -349,6 +356,9 @@ static int plan_pass(qs_state *s, uint64_t tile_mask, const qs_op *ops, int nops
                 int f = -1;
                 if (!need_of(ops[i], &f)) continue;
                 if (!fits(pl.rb, f)) break;
+                if (stage_pairs > 0 && (int)pl.rb.size() >= stage_pairs &&
+                    std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end())
+                    break;
                 if (pl.first == nops) pl.first = i;
                 if (std::find(pl.rb.begin(), pl.rb.end(), f) == pl.rb.end()) pl.rb.push_back(f);
             }
