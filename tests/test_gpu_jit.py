@@ -297,3 +297,27 @@ class TestFromBasis:
         with pytest.raises(IndexError):
             execute(build_qft(12), st, initial_basis=1 << 12)
         st.close()
+
+
+def test_from_basis_inexact_mode():
+    """initial_basis with exact=False (reordered passes, combined diagonal
+    runs): equal to reset + the same inexact run bit for bit (same programs),
+    and to the exact result within the north_star tolerance."""
+    n = 20
+    circ = Circuit(n, build_hadamard_layer(n).instructions + build_qft(n).instructions)
+    ref = State(n)
+    ref.reset(3)
+    execute(circ, ref, exact=False)
+    got = State(n)
+    got.set_amplitudes(np.ones(1 << n, np.complex64))
+    execute(circ, got, exact=False, initial_basis=3)
+    assert got.amplitudes().tobytes() == ref.amplitudes().tobytes()
+    ex = State(n)
+    ex.reset(3)
+    execute(circ, ex)
+    want = ex.amplitudes()
+    # this state concentrates its weight (|a| up to 0.64) and cancels to ~0
+    # elsewhere: the absolute floor scales with the largest amplitude
+    np.testing.assert_allclose(got.amplitudes(), want, rtol=1e-5, atol=1e-5 * float(np.abs(want).max()))
+    for s in (ref, got, ex):
+        s.close()
