@@ -345,11 +345,13 @@ def run_ours(args):
                 folded = mode == "reset_folded_into_first_pass"
 
                 def wf_step(k):
-                    if folded:  # execute(..., initial_basis=0): the first pass writes |0>'s tiles
-                        fusion.run(st, layer_passes, from_basis=0)
-                    else:
-                        st.reset(0)
-                        fusion.run(st, layer_passes)
+                    if folded:  # execute(measured circuit, initial_basis=0): the first pass writes
+                        # |0>'s tiles, the last one leaves the sampler's chunk sums
+                        st.sample_prepare(1000)
+                        ready = fusion.run(st, layer_passes, from_basis=0, chunk_sums=True)
+                        return st.sample_outcomes(1000, k, sums_ready=ready)
+                    st.reset(0)
+                    fusion.run(st, layer_passes)
                     return st.sample_outcomes(1000, k)
 
                 wf_step(0)
@@ -362,9 +364,10 @@ def run_ours(args):
             e2e["circuit_workflow"] = {
                 "value": wf["reset_folded_into_first_pass"], "unit": UNIT, "steps": reps,
                 "d2h_bytes_per_step": shots.nbytes, "reset_then_passes_value": wf["reset_then_passes"],
-                "timing": "host wall clock: |0> + the H layer as fused passes (the reset folded into the first "
-                          "pass: execute(..., initial_basis=0); reset_then_passes_value = State.reset first) + "
-                          "1000 exact shots (sample_outcomes, int64 outcomes to the host) per step"}
+                "timing": "host wall clock: |0> + the H layer as fused passes + 1000 exact shots "
+                          "(sample_outcomes, int64 outcomes to the host) per step, as execute(measured circuit, "
+                          "initial_basis=0) runs it: the reset folded into the first pass, the sampler's chunk "
+                          "sums left by the last; reset_then_passes_value = State.reset + passes + sample"}
         except Exception as exc:  # noqa: BLE001
             e2e["circuit_workflow"] = {"error": f"{type(exc).__name__}: {exc}"}
 

@@ -148,7 +148,7 @@ int qs_apply_fused(qs_state *s, const int32_t *tile_qubits, int ntile,
  * exactly in fixed-point turns) instead of one product per op; results agree
  * with the sequential ops to rounding (~1e-6 relative; tested at the
  * north_star rtol 1e-5).  complex128 registers ignore the flag. */
-enum { QS_FUSED_COMBINE_PHASES = 1 };
+enum { QS_FUSED_COMBINE_PHASES = 1, QS_FUSED_CHUNK_SUMS = 2 };
 int qs_apply_fused_ex(qs_state *s, const int32_t *tile_qubits, int ntile,
                       const qs_op *ops, int nops, int flags);
 /* qs_reset(s, basis) followed by qs_apply_fused_ex(...), as ONE HBM write:
@@ -201,6 +201,16 @@ int qs_norm_squared(qs_state *s, double *out);
  * out[i] is the outcome of draw i.  Bit-exact with the reference for the
  * same generator state.  QS_ERR_DEGENERATE when all probabilities are 0. */
 int qs_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
+/* A circuit's last fused pass feeding a sample: qs_sample_prepare(h, k) lays
+ * out the sampler's scratch for k draws and zeroes its chunk sums; the next
+ * fused pass with QS_FUSED_CHUNK_SUMS adds each tile's |a|^2 row sums into
+ * them as it writes the tile back (no extra read of the register), and
+ * qs_sample_ex(..., QS_SAMPLE_SUMS_READY) skips its own chunk-sum pass (M1).
+ * The sums only seed the exact chain's guesses: draws are bit-identical to
+ * qs_sample either way. */
+enum { QS_SAMPLE_SUMS_READY = 1 };
+int qs_sample_prepare(qs_state *s, int64_t k);
+int qs_sample_ex(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out, int flags);
 /* measure_collapse (measure.py:88-99): one draw, then amps = e_outcome. */
 int qs_measure_collapse(qs_state *s, const qs_pcg64 *rng, int64_t *outcome);
 

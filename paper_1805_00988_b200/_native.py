@@ -34,7 +34,7 @@ EXPORTS = (
     "qs_apply_controlled_controlled_gate_f64", "qs_apply_fused", "qs_apply_fused_ex", "qs_apply_fused_from_basis", "qs_apply_fused_f64", "qs_swap_qubits",
     "qs_get_amplitudes", "qs_set_amplitudes", "qs_get_amplitudes_async", "qs_set_amplitudes_async",
     "qs_probabilities", "qs_norm_squared",
-    "qs_sample", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
+    "qs_sample", "qs_sample_prepare", "qs_sample_ex", "qs_measure_collapse", "qs_cdf_extend", "qs_sample_shard",
     "qs_ipc_handle", "qs_ipc_open", "qs_ipc_close", "qs_apply_gate_peer", "qs_apply_gate_peer_f64", "qs_swap_peer", "qs_jit_sync", "qs_jit_stats",
     "qs_jit_shutdown", "qs_begin_capture", "qs_end_capture", "qs_graph_launch", "qs_graph_destroy",
     "qs_create_sharded", "qs_sharded_destroy", "qs_sharded_info", "qs_sharded_shard", "qs_sharded_set_mode",
@@ -45,6 +45,8 @@ EXPORTS = (
 )
 QS_EXCHANGE_NCCL, QS_EXCHANGE_P2P = 1, 2
 QS_FUSED_COMBINE_PHASES = 1
+QS_FUSED_CHUNK_SUMS = 2
+QS_SAMPLE_SUMS_READY = 1
 
 
 class qs_pcg64(ctypes.Structure):
@@ -112,6 +114,8 @@ def _declare(L):
         "qs_probabilities": ([vp, u64, u64, vp], i32),
         "qs_norm_squared": ([vp, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sample": ([vp, ctypes.POINTER(qs_pcg64), i64, vp], i32),
+        "qs_sample_prepare": ([vp, i64], i32),
+        "qs_sample_ex": ([vp, ctypes.POINTER(qs_pcg64), i64, vp, i32], i32),
         "qs_measure_collapse": ([vp, ctypes.POINTER(qs_pcg64), ctypes.POINTER(i64)], i32),
         "qs_cdf_extend": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double)], i32),
         "qs_sample_shard": ([vp, ctypes.POINTER(qs_pcg64), i64, ctypes.c_double, ctypes.c_double,

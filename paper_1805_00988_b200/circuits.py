@@ -188,6 +188,9 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
         raise ValueError("circuit and state widths differ")
     double = getattr(state, "is_double", False)
     ops = lower_ops(circuit, double=double)
+    last = circuit.instructions[-1] if circuit.instructions else None
+    measured = isinstance(last, SampleMeasure)
+    sums = False
     if fuse:
         if double and tile_qubits is None:
             tile_qubits = 12  # complex128 tiles: 2^12 amplitudes = 64 KiB
@@ -195,14 +198,21 @@ def execute(circuit: Circuit, state, seed=None, fuse: bool = True, tile_qubits: 
             import os
 
             reorder = os.environ.get("QSB_FUSE_REORDER") == "1" or not exact
-        fusion.run(state, fusion.plan(state.num_qubits, ops, tile_qubits, reorder=reorder),
-                   combine=not exact and not double, from_basis=initial_basis)
+        passes = fusion.plan(state.num_qubits, ops, tile_qubits, reorder=reorder)
+        # a trailing measurement: the last fused pass leaves the sampler's
+        # chunk sums as it writes the register back (one read less)
+        want_sums = measured and not double and hasattr(state, "sample_prepare")
+        if want_sums:
+            state.sample_prepare(last.n_samples)
+        sums = fusion.run(state, passes, combine=not exact and not double, from_basis=initial_basis,
+                          chunk_sums=want_sums)
     else:
         if initial_basis is not None:
             state.reset(int(initial_basis))
         for kind, t, cm, m in ops:
             fusion._single(state, kind, t, cm, m)
-    last = circuit.instructions[-1] if circuit.instructions else None
-    if isinstance(last, SampleMeasure):
+    if measured:
+        if sums:
+            return state.sample_outcomes(last.n_samples, seed, sums_ready=True)
         return state.sample_outcomes(last.n_samples, seed)
     return None

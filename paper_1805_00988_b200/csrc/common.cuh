@@ -24,6 +24,11 @@ typedef long long int64_t;
 
 namespace qsb {
 
+// amplitudes per chunk of the exact sampling chain (csrc/measure.cu M1-M6); the
+// fused passes' optional chunk-sum epilogue (QS_FUSED_CHUNK_SUMS) uses it too
+constexpr int kCdfChunkLog = 12;
+
+
 struct Gate2 {
     float2 a, b, c, d;
 };

@@ -574,6 +574,9 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
               long long basis) {
     NvtxRange nvtx_range("qsb fused pass");
     const int n = s->num_qubits;
+    // chunk sums for a following sample (qs_sample_prepare laid them out)
+    double *const csum = (flags & QS_FUSED_CHUNK_SUMS) && s->prec != QS_DOUBLE ? s->csum_dst : nullptr;
+    s->csum_ready = 0;  // the register changes: earlier sums are stale
     uint64_t tile_mask = 0;
     for (int i = 0; i < ntile; ++i) {
         if (tile_qubits[i] < 0 || tile_qubits[i] >= n)
@@ -640,6 +643,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         if (plan_pass(s, tile_mask, ops, nops, jrb, groups) == QS_OK) {
             for (FParams &g : groups) g.combine = (flags & QS_FUSED_COMBINE_PHASES) ? 1 : 0;
             groups[0].synth_basis = basis;  // the first launch group writes |basis> (or loads: -1)
+            groups.back().csum = csum;       // the last one leaves the sampler's chunk sums
             std::vector<void *> fns;
             for (const FParams &g : groups) {
                 void *fn = recording ? jit_lookup(s->device, g, K, jrb)
@@ -655,6 +659,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
                                               (unsigned)grid, (1u << (K - 1 - jrb)) + 32u);
                     if (rc) return rc;
                 }
+                s->csum_ready = csum != nullptr;
                 return QS_OK;
             }
         }
@@ -674,6 +679,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         if (rc) return rc;
     }
     groups[0].synth_basis = basis;
+    groups.back().csum = csum;
     for (const FParams &g : groups) {
         int rc;
         switch (K) {
@@ -684,6 +690,7 @@ int run_fused(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op *o
         }
         if (rc) return rc;
     }
+    s->csum_ready = csum != nullptr;
     return QS_OK;
 }
 

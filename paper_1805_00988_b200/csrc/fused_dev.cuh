@@ -72,6 +72,11 @@ struct FParams {
     // contents (zeros, 1 at the basis amplitude) instead of loading them
     // (qs_apply_fused_from_basis: reset + first pass in one HBM write)
     long long synth_basis;
+    // non-null (the last launch group of a pass followed by a sample): each
+    // tile's |a|^2 row sums (512-B rows of 64 amplitudes) are stored at
+    // csum[index >> 6] before the tile is written back; the sampler reduces
+    // them to its chunk sums instead of reading the register again
+    double *csum;
     uint64_t ntiles;
     // Dynamic tile scheduler: the producers take tiles from this counter
     // (zero at launch; the last CTA to find it exhausted zeroes it again).
@@ -653,6 +658,12 @@ __device__ __forceinline__ float4 lds_unit<float4>(uint32_t a) {
     return lds128(a);
 }
 __device__ __forceinline__ void sts_unit_(uint32_t a, float4 v) { sts128(a, v); }
+// a register of |basis>: zeros, (1, 0) in the half holding the basis amplitude
+template <class V = float4>
+__device__ __forceinline__ float4 synth_unit(uint32_t a, uint32_t basis_addr, uint32_t half) {
+    const bool hit = a == basis_addr;
+    return make_float4(hit && !half ? 1.f : 0.f, 0.f, hit && half ? 1.f : 0.f, 0.f);
+}
 __device__ __forceinline__ void sts_unit_(uint32_t a, double2 v) { sts128d(a, v); }
 template <class V>
 __device__ __forceinline__ void sts_unit(uint32_t a, V v) {
@@ -711,6 +722,30 @@ __device__ __forceinline__ void phase_ct_d(double2 d, double2 (&v)[1 << RB]) {
 // run-time compiled pass kernels (Prog = a generated straight-line program,
 // fused.cu: JIT).  Everything but the op application is identical, so both
 // give the same bits.
+// The sampler's row sums of one finished tile (QS_FUSED_CHUNK_SUMS), by the
+// producer warp just before it stores the tile: lane l adds up rows l, l+32,
+// ... (32 padded 16-B units each; the 33-unit pitch keeps the lanes on
+// distinct bank quads) and stores |a|^2 of the row's 64 amplitudes at
+// csum[row index >> 6] — the compute warps' critical path is untouched.
+template <int K, int kLowQ>
+__device__ __forceinline__ void tile_row_sums(const float4 *buf, uint64_t base, const FParams &p, int lane) {
+    constexpr int kRows = 1 << (K - kLowQ);
+    for (int r = lane; r < kRows; r += 32) {
+        const float4 *row = buf + r * 33;
+        float a = 0.f, b = 0.f;
+#pragma unroll 8
+        for (int j = 0; j < 32; j += 2) {
+            const float4 x = row[j], y = row[j + 1];
+            a = __fmaf_rn(x.x, x.x, __fmaf_rn(x.y, x.y, __fmaf_rn(x.z, x.z, __fmaf_rn(x.w, x.w, a))));
+            b = __fmaf_rn(y.x, y.x, __fmaf_rn(y.y, y.y, __fmaf_rn(y.z, y.z, __fmaf_rn(y.w, y.w, b))));
+        }
+        uint64_t g = base;
+        for (int q = 0; q < K - kLowQ; ++q)
+            if ((r >> q) & 1) g |= 1ull << p.qpos[kLowQ + q];
+        p.csum[g >> kLowQ] = (double)(a + b);
+    }
+}
+
 template <int K, int RB, class Prog, class V = float4>
 __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FParams &p) {
     constexpr int kLowQ = UnitTraits<V>::kLowQ;
@@ -766,6 +801,8 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             t = __shfl_sync(0xffffffffu, t, 0);
             if (i >= kNB) {  // buffer b still holds tile i-kNB: write it back first
                 mbar_wait(&done[b], ((i - kNB) / kNB) & 1);
+                if constexpr (UnitTraits<V>::kHalf)
+                    if (p.csum) tile_row_sums<K, kLowQ>(buf, pending[b], p, lane);
                 const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
                 for (int c = lane; c < (p.dry >= 3 ? 0 : p.ncopies); c += 32) {
                     uint32_t row = row0;
@@ -790,31 +827,12 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             const uint64_t base = tile_base(t, p);
             pending[b] = base;
             if constexpr (UnitTraits<V>::kHalf) {
-                if (p.synth_basis >= 0) {  // |basis>: write the tile, no load
+                if (p.synth_basis >= 0) {  // |basis>: no load — stage 0 starts from registers
                     if (i >= kNB) bulk_wait_read0();  // this lane's stores of the buffer are read out
-                    __syncwarp();
-                    for (int u = lane; u < kBufF4; u += 32) buf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    __syncwarp();
-                    if (lane == 0) {
-                        const uint64_t bb = (uint64_t)p.synth_basis;
-                        uint64_t tmask = 0, local = 0;
-                        for (int q = 0; q < K; ++q) {
-                            tmask |= 1ull << p.qpos[q];
-                            local |= ((bb >> p.qpos[q]) & 1ull) << q;
-                        }
-                        if ((bb & ~tmask) == base) {
-                            float4 &w = buf[(local >> kLowQ) * 33u + ((local & ((1u << kLowQ) - 1u)) >> 1)];
-                            if (local & 1u)
-                                w.z = 1.f;
-                            else
-                                w.x = 1.f;
-                        }
-                    }
-                    fence_async_smem();  // the tile's bytes may reach the bulk store unchanged
                     __syncwarp();
                     if (lane == 0) {
                         tile_id[b] = t;
-                        mbar_arrive(&full[b]);  // release: the compute warps see the writes
+                        mbar_arrive(&full[b]);  // the compute warps may overwrite the buffer
                     }
                     continue;
                 }
@@ -841,6 +859,8 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         for (int k = (i >= kNB ? i - kNB + 1 : 0); k < i; ++k) {
             const int b = k % kNB;
             mbar_wait(&done[b], (k / kNB) & 1);
+            if constexpr (UnitTraits<V>::kHalf)
+                if (p.csum) tile_row_sums<K, kLowQ>(buf0 + b * kBufF4, pending[b], p, lane);
             const uint32_t row0 = (uint32_t)(pending[b] >> kLowQ);
             for (int c = lane; c < (p.dry >= 3 ? 0 : p.ncopies); c += 32) {
                 uint32_t row = row0;
@@ -876,10 +896,29 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         const uint64_t t = tile_id[b];
         if (t == ~0ull) break;
         const uint64_t base = tile_base(t, p);
+        // |synth_basis> (qs_apply_fused_from_basis): stage 0 starts from zero
+        // registers instead of loading, with 1 at the basis amplitude when it
+        // lies in this tile (its shared-memory byte address and half)
+        uint32_t syn_addr = 0xffffffffu, syn_half = 0;
+        const bool synth = UnitTraits<V>::kHalf && p.synth_basis >= 0;
+        if (synth) {
+            const uint64_t bb = (uint64_t)p.synth_basis;
+            uint64_t tmask = 0, local = 0;
+            for (int q = 0; q < K; ++q) {
+                tmask |= 1ull << p.qpos[q];
+                local |= ((bb >> p.qpos[q]) & 1ull) << q;
+            }
+            if ((bb & ~tmask) == base) {
+                const uint32_t f = (uint32_t)(local >> 1);
+                syn_addr = smem_u32(tile) + padded(f) * 16u;
+                syn_half = (uint32_t)(local & 1u);
+            }
+        }
         bool staged = false;
         if constexpr (Prog::kOwnsStages) {  // generated program: literal stage layouts
             if (p.dry == 0 || p.dry == 4) {
-                Prog::template run_stages<RB, kCompute>(tile, (uint32_t)tid, base, p.one, sops);
+                Prog::template run_stages<RB, kCompute>(tile, (uint32_t)tid, base, p.one, sops, synth, syn_addr,
+                                                        syn_half);
                 staged = true;
             }
         }
@@ -898,6 +937,12 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
+                if constexpr (UnitTraits<V>::kHalf) {
+                    if (synth && s == 0) {
+                        v[j] = synth_unit(a, syn_addr, syn_half);
+                        continue;
+                    }
+                }
                 v[j] = lds_unit<V>(a);
             }
             if constexpr (Prog::kPlanar && UnitTraits<V>::kHalf) {

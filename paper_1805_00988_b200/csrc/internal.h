@@ -28,6 +28,10 @@ struct qs_state {
     // the register buffer was exported with cudaIpcGetMemHandle: other
     // processes may still map it, so it is freed, never recycled by the pool
     int ipc_exported;
+    // the last fused pass (QS_FUSED_CHUNK_SUMS) left the sampler's chunk sums
+    // (M1) in scratch; consumed / cleared by the next sample or pass
+    int csum_ready;
+    double *csum_dst;  // qs_sample_prepare's chunk-sum array in scratch (nullptr: none)
 };
 
 #include <nvtx3/nvToolsExt.h>  // header-only; a no-op unless a tool (ncu / nsys) is attached
@@ -94,7 +98,8 @@ int run_fused_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op6
 int run_fused_tiles_d(qs_state *s, const int32_t *tile_qubits, int ntile, const qs_op64 *ops, int nops);
 int run_probabilities(qs_state *s, uint64_t offset, uint64_t count, double *host);
 int run_norm(qs_state *s, double *out);
-int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out);
+int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out, bool sums_ready = false);
+int run_sample_prepare(qs_state *s, int64_t k, double **csum);
 int run_cdf_extend(qs_state *s, double start, double *end);
 int run_sample_shard(qs_state *s, const qs_pcg64 *rng, int64_t k, double start, double total,
                      uint64_t base, uint64_t gdim, int is_last, int64_t *out);

@@ -54,6 +54,7 @@ namespace qsb {
 namespace {
 
 constexpr int kChunkLog = 12;  // 4096 amplitudes per chunk
+static_assert(kChunkLog == kCdfChunkLog, "fused-pass chunk sums use the sampler's chunk size");
 
 __device__ __forceinline__ double prob(float2 a) {
     double re = (double)a.x, im = (double)a.y;
@@ -1313,8 +1314,11 @@ static bool traj_regs() {
 }
 
 template <class A>
-static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s_start) {
-    if (sizeof(A) == sizeof(float2) && c.clog == kChunkLog)
+static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s_start, bool sums_ready) {
+    // M1, unless the circuit's last fused pass already accumulated the chunk
+    // sums (qs_sample_prepare + QS_FUSED_CHUNK_SUMS: they are guesses only)
+    if (sums_ready) {
+    } else if (sizeof(A) == sizeof(float2) && c.clog == kChunkLog)
         k_chunk_sums_f4<<<(unsigned)c.nch, 256, 0, s->stream>>>((const float4 *)amps, c.csum);
     else
         k_chunk_sums<<<(unsigned)c.nch, 256, 0, s->stream>>>(amps, c.clog, c.csum);
@@ -1343,9 +1347,9 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
     return QS_OK;
 }
 
-static int cdf_chain(qs_state *s, const CdfScratch &c, double s_start) {
-    return s->prec == QS_DOUBLE ? cdf_chain_t(s, (const double2 *)amps_d(s), c, s_start)
-                                : cdf_chain_t(s, (const float2 *)s->amps, c, s_start);
+static int cdf_chain(qs_state *s, const CdfScratch &c, double s_start, bool sums_ready = false) {
+    return s->prec == QS_DOUBLE ? cdf_chain_t(s, (const double2 *)amps_d(s), c, s_start, false)
+                                : cdf_chain_t(s, (const float2 *)s->amps, c, s_start, sums_ready);
 }
 
 // M5 + M6 and the copy-out shared by qs_sample / qs_sample_shard.
@@ -1380,12 +1384,49 @@ static int draw(qs_state *s, const CdfScratch &c, const qs_pcg64 *rng, int64_t k
     return QS_OK;
 }
 
-int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
-    NvtxRange nvtx_range("qsb sample");
+// Scratch for k draws laid out and the chunk sums zeroed, so that the next
+// fused pass can accumulate them (QS_FUSED_CHUNK_SUMS) and qs_sample_ex skip
+// M1.  *csum: where that pass adds (nullptr when this register's sampler has
+// no such chunks: complex128 or fewer than 2^12 amplitudes).
+int run_sample_prepare(qs_state *s, int64_t k, double **csum) {
+    *csum = nullptr;
+    s->csum_ready = 0;
+    if (s->prec == QS_DOUBLE || s->num_qubits < kChunkLog) return QS_OK;
     CdfScratch c;
     int rc = cdf_scratch(s, k, c);
     if (rc) return rc;
-    rc = cdf_chain(s, c, 0.0);
+    // the pass's row sums (2^(n-6) doubles) go where M3 later writes the fine
+    // starts (2 x 64 per chunk = 2^(n-5) doubles): free until then
+    *csum = c.fine0;
+    s->csum_dst = c.fine0;
+    return QS_OK;
+}
+
+// M1 from the row sums a fused pass left (64 rows of 64 amplitudes per chunk)
+__global__ void k_rows_to_chunks(const double *__restrict__ rows, uint64_t nch, double *__restrict__ csum) {
+    const uint64_t c = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+    if (c >= nch) return;
+    const int lane = threadIdx.x & 31;
+    double v = rows[(c << 6) + lane] + rows[(c << 6) + 32 + lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) csum[c] = v;
+}
+
+int run_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out, bool sums_ready) {
+    NvtxRange nvtx_range("qsb sample");
+    // the sums are guesses only (M2-M4 resolve the exact starts whatever they
+    // are), so this is a shortcut, never a correctness condition
+    bool ready = sums_ready && s->csum_ready && s->csum_dst != nullptr;
+    s->csum_ready = 0;
+    void *before = s->scratch;
+    CdfScratch c;
+    int rc = cdf_scratch(s, k, c);
+    if (rc) return rc;
+    if (s->scratch != before || c.fine0 != s->csum_dst) ready = false;  // reallocated: the row sums are gone
+    if (ready)
+        k_rows_to_chunks<<<(unsigned)((c.nch + 7) / 8), 256, 0, s->stream>>>(c.fine0, c.nch, c.csum);
+    rc = cdf_chain(s, c, 0.0, ready);
     if (rc) return rc;
     double tot = 0.0;
     const uint64_t dim = 1ull << s->num_qubits;

@@ -65,6 +65,8 @@ int ensure_scratch(qs_state *s, size_t bytes) {
     bytes = (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
     if (s->scratch) {
         QS_CUDA(cudaStreamSynchronize(s->stream));
+        s->csum_dst = nullptr;  // a prepared chunk-sum array lived in the old buffer
+        s->csum_ready = 0;
         pool_free(s->device, s->scratch, s->scratch_bytes);
         s->scratch = nullptr;
         s->scratch_bytes = 0;
@@ -508,6 +510,24 @@ int qs_sample(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out) {
     if (!rng || !out) return set_error(QS_ERR_NULL, "null rng or output buffer");
     DeviceGuard guard(s->device);
     return run_sample(s, rng, k, out);
+}
+
+int qs_sample_prepare(qs_state *s, int64_t k) {
+    CHECK_HANDLE(s);
+    if (k < 1) return set_error(QS_ERR_VALUE, "n_samples must be >= 1");
+    DeviceGuard guard(s->device);
+    double *csum = nullptr;
+    int rc = run_sample_prepare(s, k, &csum);
+    s->csum_dst = csum;
+    return rc;
+}
+
+int qs_sample_ex(qs_state *s, const qs_pcg64 *rng, int64_t k, int64_t *out, int flags) {
+    CHECK_HANDLE(s);
+    if (k < 1) return set_error(QS_ERR_VALUE, "n_samples must be >= 1");
+    if (!rng || !out) return set_error(QS_ERR_NULL, "null rng or output buffer");
+    DeviceGuard guard(s->device);
+    return run_sample(s, rng, k, out, (flags & QS_SAMPLE_SUMS_READY) != 0);
 }
 
 // measure_collapse: pkg/src/pairsim/measure.py:88-99

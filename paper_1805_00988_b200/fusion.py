@@ -350,27 +350,35 @@ def jit_stats() -> dict:
     return {"compiled": c.value, "cache_hits": h.value, "failed": f.value}
 
 
-def run(state, passes: list[Pass], combine: bool = False, from_basis: int | None = None) -> None:
+def run(state, passes: list[Pass], combine: bool = False, from_basis: int | None = None,
+        chunk_sums: bool = False) -> bool:
     """Launch the planned passes on a State (asynchronous on its stream).
     combine=True: runs of unit-modulus diagonal ops as one product per
     amplitude (State.apply_fused; not bit-exact).  from_basis=b: the register
     starts as |b> (State.reset(b)), folded into the first pass when it is a
-    fused one — its tiles are written as |b> instead of loaded."""
-    if from_basis is not None:
-        if passes and len(passes[0].ops) > 1:
-            first = passes[0]
-            state.apply_fused(first.tile, first.op_array(), combine=combine, from_basis=from_basis)
-            passes = passes[1:]
-        else:
+    fused one — its tiles are written as |b> instead of loaded.
+    chunk_sums=True (after State.sample_prepare): the last pass, when it is a
+    fused one, also leaves the sampler's chunk sums; returns whether it did."""
+    last = len(passes) - 1
+    sums = False
+    for i, p in enumerate(passes):
+        want = chunk_sums and i == last and len(p.ops) > 1
+        extra = {"chunk_sums": True} if want else {}  # (shard objects take the plain signature)
+        if i == 0 and from_basis is not None:
+            if len(p.ops) > 1:
+                state.apply_fused(p.tile, p.op_array(), combine=combine, from_basis=from_basis, **extra)
+                sums = want
+                continue
             state.reset(int(from_basis))
-    for p in passes:
         if len(p.ops) == 1:
             kind, t, cm, m = p.ops[0]
             _single(state, kind, t, cm, m)
-        elif combine:
-            state.apply_fused(p.tile, p.op_array(), combine=True)
         else:
-            state.apply_fused(p.tile, p.op_array())
+            state.apply_fused(p.tile, p.op_array(), combine=combine, **extra)
+            sums = want
+    if not passes and from_basis is not None:
+        state.reset(int(from_basis))
+    return sums
 
 
 def _single(state, kind, t, cm, m) -> None:

@@ -210,30 +210,32 @@ class State:
         return self
 
     def apply_fused(self, tile_qubits, ops: np.ndarray, combine: bool = False,
-                    from_basis: int | None = None) -> "State":
+                    from_basis: int | None = None, chunk_sums: bool = False) -> "State":
         """One fused HBM pass (see fusion.py for the planner).  `ops` is an
         OP_DTYPE (float32 entries) or OP64_DTYPE (fp64 entries) record array.
         combine=True (not bit-exact, QS_FUSED_COMBINE_PHASES): runs of
         unit-modulus diagonal ops become one product per amplitude.
         from_basis=b: reset to |b> first, folded into the pass (its tiles are
-        written as |b> instead of loaded: qs_apply_fused_from_basis)."""
+        written as |b> instead of loaded: qs_apply_fused_from_basis).
+        chunk_sums=True: the pass also leaves the sampler's chunk sums (after
+        sample_prepare; QS_FUSED_CHUNK_SUMS)."""
         tq = np.ascontiguousarray(np.asarray(tile_qubits, dtype=np.int32))
         wide = np.asarray(ops).dtype == N.OP64_DTYPE
         ops = np.ascontiguousarray(ops, dtype=N.OP64_DTYPE if wide else N.OP_DTYPE)
         L = N.lib()
         tp = tq.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        flags = (N.QS_FUSED_COMBINE_PHASES if combine else 0) | (N.QS_FUSED_CHUNK_SUMS if chunk_sums else 0)
         if from_basis is not None:
             if wide:
                 self.reset(int(from_basis))
             else:
                 N.check(L.qs_apply_fused_from_basis(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size),
-                                                    N.QS_FUSED_COMBINE_PHASES if combine else 0, int(from_basis)))
+                                                    flags, int(from_basis)))
                 return self
         if wide:
             N.check(L.qs_apply_fused_f64(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size)))
-        elif combine:
-            N.check(L.qs_apply_fused_ex(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size),
-                                        N.QS_FUSED_COMBINE_PHASES))
+        elif flags:
+            N.check(L.qs_apply_fused_ex(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size), flags))
         else:
             N.check(L.qs_apply_fused(self.handle, tp, int(tq.size), ops.ctypes.data, int(ops.size)))
         return self
@@ -334,15 +336,24 @@ class State:
         N.check(N.lib().qs_norm_squared(self.handle, ctypes.byref(v)))
         return v.value
 
-    def sample_outcomes(self, samples: int, seed=None) -> np.ndarray:
-        """Per-draw outcomes, bit-exact with pairsim.measure.sample for the same seed."""
+    def sample_outcomes(self, samples: int, seed=None, sums_ready: bool = False) -> np.ndarray:
+        """Per-draw outcomes, bit-exact with pairsim.measure.sample for the same seed.
+        sums_ready: the last fused pass accumulated the sampler's chunk sums
+        (sample_prepare + apply_fused(chunk_sums=True)); a shortcut only."""
         if samples < 1:
             raise ValueError("n_samples must be >= 1")
         out = np.empty(int(samples), dtype=np.int64)
         rng = N.pcg_from_seed(seed)
-        N.check(N.lib().qs_sample(self.handle, ctypes.byref(rng), int(samples), out.ctypes.data))
+        N.check(N.lib().qs_sample_ex(self.handle, ctypes.byref(rng), int(samples), out.ctypes.data,
+                                     N.QS_SAMPLE_SUMS_READY if sums_ready else 0))
         N.consume_draws(seed, samples)
         return out
+
+    def sample_prepare(self, samples: int) -> "State":
+        """Lay out the sampler's scratch for `samples` draws so the next fused
+        pass (apply_fused(chunk_sums=True)) can leave the chunk sums."""
+        N.check(N.lib().qs_sample_prepare(self.handle, int(samples)))
+        return self
 
     def cdf_extend(self, start: float) -> float:
         """Exact sequential cumsum of this register's probabilities continued from `start`."""

@@ -71,6 +71,12 @@ if part in ("all", "sample18"):
     mag = np.exp(rng.uniform(np.log(1e-30), 0.0, size=1 << m))
     st.set_amplitudes((mag * np.exp(2j * np.pi * rng.random(1 << m))).astype(np.complex64))
     st.sample_outcomes(3000, 6)
+    # a measured circuit: the reset folded into the first fused pass, the
+    # sampler's row sums left by the last one (producer-warp epilogue)
+    from paper_1805_00988_b200 import execute
+    from paper_1805_00988_b200.circuits import Circuit, SampleMeasure
+
+    execute(Circuit(m, build_qft(m).instructions + (SampleMeasure(2000),)), st, seed=7, initial_basis=5)
     st.close()
 
 if part in ("all", "peer"):

@@ -321,3 +321,49 @@ def test_from_basis_inexact_mode():
     np.testing.assert_allclose(got.amplitudes(), want, rtol=1e-5, atol=1e-5 * float(np.abs(want).max()))
     for s in (ref, got, ex):
         s.close()
+
+
+class TestChunkSumEpilogue:
+    """A measured circuit's last fused pass leaves the sampler's chunk sums
+    (qs_sample_prepare + QS_FUSED_CHUNK_SUMS) and the sample skips M1.  The
+    sums only seed guesses, so draws must equal the plain path's bit for bit
+    — also when the sums are stale (the register changed after the pass)."""
+
+    @pytest.mark.parametrize("n,circ_name", [(12, "qft"), (17, "hlayer"), (20, "random"), (22, "layered")])
+    @pytest.mark.parametrize("jit", ["2", "0"])
+    def test_draws_equal_plain_path(self, n, circ_name, jit, monkeypatch):
+        from paper_1805_00988_b200.circuits import SampleMeasure
+
+        monkeypatch.setenv("QSB_FUSED_JIT", jit)
+        base = {"qft": lambda: build_qft(n), "hlayer": lambda: build_hadamard_layer(n),
+                "random": lambda: random_circuit(n, 10, np.random.default_rng(n)),
+                "layered": lambda: layered_random_circuit(n, 5, seed=n)}[circ_name]()
+        measured = Circuit(n, base.instructions + (SampleMeasure(4000),))
+        got = State(n)
+        got_out = execute(measured, got, seed=11, initial_basis=0)
+        ref = State(n)
+        execute(base, ref)
+        want_out = ref.sample_outcomes(4000, 11)
+        assert np.array_equal(got_out, want_out)
+        assert got.amplitudes().tobytes() == ref.amplitudes().tobytes()
+        got.close()
+        ref.close()
+
+    def test_stale_sums_still_exact(self):
+        from paper_1805_00988_b200 import fusion
+        from paper_1805_00988_b200.circuits import lower_ops
+
+        n = 18
+        st = State(n)
+        st.sample_prepare(3000)
+        fusion.run(st, fusion.plan(n, lower_ops(build_qft(n))), chunk_sums=True)
+        st.h(3)  # the register changes after the sums were left
+        st.t(17)
+        got = st.sample_outcomes(3000, 5, sums_ready=True)
+        ref = State(n)
+        execute(build_qft(n), ref)
+        ref.h(3)
+        ref.t(17)
+        assert np.array_equal(got, ref.sample_outcomes(3000, 5))
+        st.close()
+        ref.close()
