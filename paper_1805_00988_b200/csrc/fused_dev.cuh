@@ -68,7 +68,7 @@ struct FParams {
     float one;  // == 1.0f, read at run time (the generated programs' rsum / csub)
     int l2hint;  // TMA copies with an L2 evict_first policy
     int combine;  // generated programs: combine runs of unit-modulus diagonal ops (exact = False)
-    // >= 0: the register is |synth_basis> — the producer writes each tile's
+    // >= 0: the register is |synth_basis> — the compute warps write each tile's
     // contents (zeros, 1 at the basis amplitude) instead of loading them
     // (qs_apply_fused_from_basis: reset + first pass in one HBM write)
     long long synth_basis;
@@ -658,12 +658,7 @@ __device__ __forceinline__ float4 lds_unit<float4>(uint32_t a) {
     return lds128(a);
 }
 __device__ __forceinline__ void sts_unit_(uint32_t a, float4 v) { sts128(a, v); }
-// a register of |basis>: zeros, (1, 0) in the half holding the basis amplitude
-template <class V = float4>
-__device__ __forceinline__ float4 synth_unit(uint32_t a, uint32_t basis_addr, uint32_t half) {
-    const bool hit = a == basis_addr;
-    return make_float4(hit && !half ? 1.f : 0.f, 0.f, hit && half ? 1.f : 0.f, 0.f);
-}
+
 __device__ __forceinline__ void sts_unit_(uint32_t a, double2 v) { sts128d(a, v); }
 template <class V>
 __device__ __forceinline__ void sts_unit(uint32_t a, V v) {
@@ -827,7 +822,7 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
             const uint64_t base = tile_base(t, p);
             pending[b] = base;
             if constexpr (UnitTraits<V>::kHalf) {
-                if (p.synth_basis >= 0) {  // |basis>: no load — stage 0 starts from registers
+                if (p.synth_basis >= 0) {  // |basis>: no load — the compute warps write the tile
                     if (i >= kNB) bulk_wait_read0();  // this lane's stores of the buffer are read out
                     __syncwarp();
                     if (lane == 0) {
@@ -896,29 +891,37 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
         const uint64_t t = tile_id[b];
         if (t == ~0ull) break;
         const uint64_t base = tile_base(t, p);
-        // |synth_basis> (qs_apply_fused_from_basis): stage 0 starts from zero
-        // registers instead of loading, with 1 at the basis amplitude when it
-        // lies in this tile (its shared-memory byte address and half)
-        uint32_t syn_addr = 0xffffffffu, syn_half = 0;
-        const bool synth = UnitTraits<V>::kHalf && p.synth_basis >= 0;
-        if (synth) {
-            const uint64_t bb = (uint64_t)p.synth_basis;
-            uint64_t tmask = 0, local = 0;
-            for (int q = 0; q < K; ++q) {
-                tmask |= 1ull << p.qpos[q];
-                local |= ((bb >> p.qpos[q]) & 1ull) << q;
-            }
-            if ((bb & ~tmask) == base) {
-                const uint32_t f = (uint32_t)(local >> 1);
-                syn_addr = smem_u32(tile) + padded(f) * 16u;
-                syn_half = (uint32_t)(local & 1u);
+        // |synth_basis> (qs_apply_fused_from_basis): the producer loaded
+        // nothing; the compute warps write the tile as |basis> (zeros, 1 at
+        // the basis amplitude when it lies in this tile) and the stages
+        // proceed as after a load — the same threads write and then read, so
+        // a named barrier orders them (no producer-written shared memory)
+        if constexpr (UnitTraits<V>::kHalf) {
+            if (p.synth_basis >= 0) {
+                for (int u = tid; u < kBufF4; u += kCompute) tile[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                named_sync(1, kCompute);
+                if (tid == 0) {
+                    const uint64_t bb = (uint64_t)p.synth_basis;
+                    uint64_t tmask = 0, local = 0;
+                    for (int q = 0; q < K; ++q) {
+                        tmask |= 1ull << p.qpos[q];
+                        local |= ((bb >> p.qpos[q]) & 1ull) << q;
+                    }
+                    if ((bb & ~tmask) == base) {
+                        float4 &w = tile[padded((uint32_t)(local >> 1))];
+                        if (local & 1u)
+                            w.z = 1.f;
+                        else
+                            w.x = 1.f;
+                    }
+                }
+                named_sync(1, kCompute);
             }
         }
         bool staged = false;
         if constexpr (Prog::kOwnsStages) {  // generated program: literal stage layouts
             if (p.dry == 0 || p.dry == 4) {
-                Prog::template run_stages<RB, kCompute>(tile, (uint32_t)tid, base, p.one, sops, synth, syn_addr,
-                                                        syn_half);
+                Prog::template run_stages<RB, kCompute>(tile, (uint32_t)tid, base, p.one, sops);
                 staged = true;
             }
         }
@@ -937,12 +940,6 @@ __device__ __forceinline__ void fused_body(float4 *__restrict__ amps, const FPar
 #pragma unroll
                 for (int r = 0; r < RB; ++r)
                     if (j & (1 << r)) a += rs[r];
-                if constexpr (UnitTraits<V>::kHalf) {
-                    if (synth && s == 0) {
-                        v[j] = synth_unit(a, syn_addr, syn_half);
-                        continue;
-                    }
-                }
                 v[j] = lds_unit<V>(a);
             }
             if constexpr (Prog::kPlanar && UnitTraits<V>::kHalf) {

@@ -221,8 +221,7 @@ void emit_run_stages(std::string &src, const FParams &p, int RB, bool dbl) {
     src += "  static constexpr bool kOwnsStages = true;\n"
            "  template <int RB_, int NC>\n"
            "  static __device__ __forceinline__ void run_stages(float4 *tile, uint32_t tid, uint64_t base,\n"
-           "      float one, const FOp *ops, bool synth, uint32_t syn_addr, uint32_t syn_half) {\n"
-           "    (void)synth;\n    (void)syn_addr;\n    (void)syn_half;\n"
+           "      float one, const FOp *ops) {\n"
            "    const uint32_t lane = tid & 31u, warp = tid >> 5;\n    (void)warp;\n    const FStage st0{};\n";
     for (int k = 0; k < p.nstages; ++k) {
         const FStage &st = p.stages[k];
@@ -245,20 +244,10 @@ void emit_run_stages(std::string &src, const FParams &p, int RB, bool dbl) {
                 if (j & (1 << r)) a += (1u << st.rf[r]) + ((1u << st.rf[r]) >> 5);
             off[j] = a;
         }
-        if (k == 0 && !dbl) {  // |basis> (qs_apply_fused_from_basis): the first stage starts from registers
-            src += "      if (synth) {\n";
-            for (int j = 0; j < (1 << RB); ++j) {
-                std::snprintf(buf, sizeof buf, "        v[%d] = synth_unit(sb + %uu, syn_addr, syn_half);\n", j,
-                              16u * off[j]);
-                src += buf;
-            }
-            src += "      } else {\n";
-        }
         for (int j = 0; j < (1 << RB); ++j) {
             std::snprintf(buf, sizeof buf, "      v[%d] = %s(sb + %uu);\n", j, dbl ? "lds128d" : "lds128", 16u * off[j]);
             src += buf;
         }
-        if (k == 0 && !dbl) src += "      }\n";
         std::snprintf(buf, sizeof buf, "      run<RB_>(%d, st0, ops, tid, base, one, v);\n", k);
         src += buf;
         for (int j = 0; j < (1 << RB); ++j) {
