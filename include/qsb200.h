@@ -105,6 +105,10 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
 /* As qs_create with an explicit precision (QS_SINGLE or QS_DOUBLE); a
  * complex128 register needs 16 * 2^n bytes (memory_required, state.py:71-83). */
 int qs_create_ex(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out);
+/* qs_create_ex with the register's contents left undefined (no clear): for a
+ * circuit whose first fused pass writes its start state anyway
+ * (qs_apply_fused_from_basis).  Reading it before that is unspecified. */
+int qs_create_uninit(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out);
 int qs_precision(const qs_state *s, int *out);
 int qs_destroy(qs_state *s);
 int qs_num_qubits(const qs_state *s, int *out);

@@ -26,7 +26,7 @@ QS_SINGLE, QS_DOUBLE = 0, 1
 # Every symbol include/qsb200.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "qs_abi_version", "qs_last_error", "qs_device_count", "qs_release_cached", "qs_host_alloc", "qs_host_free",
-    "qs_create", "qs_create_ex",
+    "qs_create", "qs_create_ex", "qs_create_uninit",
     "qs_precision", "qs_destroy",
     "qs_num_qubits", "qs_device", "qs_device_pointer", "qs_stream", "qs_reset",
     "qs_synchronize", "qs_apply_gate", "qs_apply_controlled_gate",
@@ -88,6 +88,7 @@ def _declare(L):
         "qs_host_free": ([vp], i32),
         "qs_create": ([i32, i32, u64, ctypes.POINTER(vp)], i32),
         "qs_create_ex": ([i32, i32, u64, i32, ctypes.POINTER(vp)], i32),
+        "qs_create_uninit": ([i32, i32, u64, i32, ctypes.POINTER(vp)], i32),
         "qs_precision": ([vp, ctypes.POINTER(i32)], i32),
         "qs_destroy": ([vp], i32),
         "qs_num_qubits": ([vp, ctypes.POINTER(i32)], i32),

@@ -150,7 +150,22 @@ int qs_create(int num_qubits, int device, uint64_t memory_budget, qs_state **out
     return qs_create_ex(num_qubits, device, memory_budget, QS_SINGLE, out);
 }
 
+static int create_impl(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out,
+                       bool init);
+
 int qs_create_ex(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out) {
+    return create_impl(num_qubits, device, memory_budget, precision, out, true);
+}
+
+// A register whose contents are left undefined: for a circuit whose first
+// fused pass writes its start state anyway (qs_apply_fused_from_basis) —
+// pairsim's new_state + run_circuit without the separate clear.
+int qs_create_uninit(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out) {
+    return create_impl(num_qubits, device, memory_budget, precision, out, false);
+}
+
+static int create_impl(int num_qubits, int device, uint64_t memory_budget, int precision, qs_state **out,
+                       bool init) {
     if (!out) return set_error(QS_ERR_NULL, "null output pointer");
     *out = nullptr;
     if (num_qubits < 1) return set_error(QS_ERR_VALUE, "num_qubits must be >= 1");
@@ -207,7 +222,7 @@ int qs_create_ex(int num_qubits, int device, uint64_t memory_budget, int precisi
         return cuda_fail(e, "cudaStreamCreateWithFlags");
     }
     cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
-    int rc = launch_reset(s, 0);
+    int rc = init ? launch_reset(s, 0) : QS_OK;
     if (rc != QS_OK) {
         stream_release(device, s->stream);
         pool_free(device, s->amps, need_b);

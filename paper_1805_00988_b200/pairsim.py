@@ -255,6 +255,10 @@ class StateVector:
 
 def new_state(num_qubits: int, precision: Precision = Precision.SINGLE, memory_budget: int | None = None) -> StateVector:
     """|0...0> on the device; CapacityError before allocation (state.py:122-143)."""
+    return _new_state(num_qubits, precision, memory_budget, True)
+
+
+def _new_state(num_qubits: int, precision: Precision, memory_budget: int | None, init: bool) -> StateVector:
     if num_qubits < 1:
         raise ValueError("num_qubits must be >= 1")
     need = memory_required(num_qubits, precision) // 8
@@ -262,7 +266,7 @@ def new_state(num_qubits: int, precision: Precision = Precision.SINGLE, memory_b
         raise CapacityError(
             f"{num_qubits} qubits need {format_bytes(need)} ({need} bytes); "
             f"memory budget is {format_bytes(memory_budget)}")
-    dev = State(num_qubits, _device(), memory_budget=memory_budget, precision=precision.value)
+    dev = State(num_qubits, _device(), memory_budget=memory_budget, precision=precision.value, _init=init)
     return StateVector(num_qubits, _dev=dev)
 
 
@@ -377,8 +381,9 @@ def run_circuit(circuit, precision: Precision = Precision.SINGLE, seed=None, exe
     """circuits.py:171-192 on the device; returns (StateVector, histogram | None)."""
     from .circuits import execute
 
-    state = new_state(circuit.num_qubits, precision, memory_budget)
-    # the register is |0>: the first fused pass writes its tiles instead of loading them
+    # |0> is written by the circuit's first fused pass (or an explicit reset
+    # when it has none): the register is not cleared separately
+    state = _new_state(circuit.num_qubits, precision, memory_budget, False)
     outcomes = execute(circuit, state.device_state, seed=seed, fuse=fuse, initial_basis=0)
     hist = MeasurementHistogram.from_outcomes(outcomes) if outcomes is not None else None
     return state, hist

@@ -120,15 +120,17 @@ def _precision_code(precision) -> int:
 
 class State:
     def __init__(self, num_qubits: int, device: int = 0, memory_budget: int | None = None,
-                 precision="single"):
+                 precision="single", _init: bool = True):
         if not isinstance(num_qubits, (int, np.integer)):
             raise TypeError("num_qubits must be an integer")
         if num_qubits < 1:
             raise ValueError("num_qubits must be >= 1")
         prec = _precision_code(precision)
         self._h = ctypes.c_void_p()
-        N.check(N.lib().qs_create_ex(int(num_qubits), int(device), int(memory_budget or 0), prec,
-                                     ctypes.byref(self._h)))
+        # _init=False: contents undefined until the first fused pass writes its
+        # start state (execute(..., initial_basis=b) right after; qs_create_uninit)
+        create = N.lib().qs_create_ex if _init else N.lib().qs_create_uninit
+        N.check(create(int(num_qubits), int(device), int(memory_budget or 0), prec, ctypes.byref(self._h)))
         self.num_qubits = int(num_qubits)
         self.device = int(device)
         self.is_double = prec == N.QS_DOUBLE

@@ -367,3 +367,30 @@ class TestChunkSumEpilogue:
         assert np.array_equal(got, ref.sample_outcomes(3000, 5))
         st.close()
         ref.close()
+
+
+@pytest.mark.parametrize("n", [8, 14, 20])
+def test_run_circuit_on_an_uncleared_register(n):
+    """pairsim.run_circuit creates its register without the clear
+    (qs_create_uninit) and lets the first fused pass write |0> (or resets when
+    the circuit has no fused pass): results equal new_state + the sweeps, for
+    circuits with and without fused passes and for complex128."""
+    from paper_1805_00988_b200 import pairsim as ps
+    from paper_1805_00988_b200.circuits import SampleMeasure
+
+    # dirty the pool's cached buffers first, so an uncleared register would show
+    for _ in range(2):
+        junk = State(n)
+        junk.set_amplitudes(np.full(1 << n, 0.5 + 0.25j, np.complex64))
+        junk.close()
+    cases = [build_qft(n), Circuit(n, (Apply(FIXED_GATES["h"], 1),)), Circuit(n, ()),
+             Circuit(n, build_hadamard_layer(n).instructions + (SampleMeasure(500),))]
+    for circ in cases:
+        for prec in (ps.Precision.SINGLE, ps.Precision.DOUBLE):
+            got, hist = ps.run_circuit(circ, prec, seed=3)
+            ref = ps.new_state(n, prec)
+            execute(Circuit(n, tuple(i for i in circ.instructions if not isinstance(i, SampleMeasure))),
+                    ref.device_state, fuse=False)
+            assert np.array_equal(ps.probabilities(got), ps.probabilities(ref)), (circ.gate_count(), prec)
+            if hist is not None:
+                assert hist == ps.sample(ref, 500, 3)
