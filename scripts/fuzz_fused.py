@@ -2,7 +2,10 @@
 circuits — library / Haar / u1 gates, controlled and doubly-controlled, all
 gate classes — over random register sizes and tile widths, run as compiled
 pass programs (and the interpreter kernel for a share of them) and compared
-bit for bit with the unfused sweeps on the same register.  Exits non-zero on
+bit for bit with the unfused sweeps on the same register; every third case
+also as a measured circuit from a basis state (the folded reset and the
+last pass's row sums) against reset + sweeps + the plain sampler (values
+and draws).  Exits non-zero on
 the first mismatch and prints the failing case.
 
     python scripts/fuzz_fused.py [cases] [seed]
@@ -21,7 +24,8 @@ os.environ.setdefault("QSB_FUSED_JIT", "2")
 import numpy as np  # noqa: E402
 
 from paper_1805_00988_b200 import State, fusion, random_circuit  # noqa: E402
-from paper_1805_00988_b200.circuits import Circuit, ControlledControlledApply, execute, lower_ops  # noqa: E402
+from paper_1805_00988_b200.circuits import (  # noqa: E402
+    Circuit, ControlledControlledApply, SampleMeasure, execute, lower_ops)
 from paper_1805_00988_b200.gates import FIXED_GATES, random_unitary_gate  # noqa: E402
 
 
@@ -67,6 +71,28 @@ def main() -> int:
                                   "got": str(got[bad]), "want": str(want[bad])}))
                 return 1
         os.environ["QSB_FUSED_JIT"] = "2"
+        if case % 3 == 0:  # the measured-circuit path: folded reset + row sums left by the last pass
+            b = int(rng.integers(0, 1 << n))
+            shots = int(rng.integers(1, 3000))
+            ref = State(n)
+            ref.reset(b)
+            execute(circ, ref, fuse=False)
+            want_amp = ref.amplitudes()
+            want_out = ref.sample_outcomes(shots, case)
+            ref.close()
+            st = State(n)
+            st.set_amplitudes(a0)  # stale contents
+            got_out = execute(Circuit(n, circ.instructions + (SampleMeasure(shots),)), st, seed=case,
+                              tile_qubits=K, initial_basis=b)
+            got_amp = st.amplitudes()
+            st.close()
+            # values, not bytes: from a basis state the register holds exact
+            # zeros, and fused diagonal ops may flip their sign (the documented
+            # freedom: 1*x + 0*y adds +-0, same as the sweeps up to the sign of 0)
+            if not np.array_equal(got_amp, want_amp) or not np.array_equal(got_out, want_out):
+                print(json.dumps({"mismatch": True, "case": case, "n": n, "K": K, "mode": "measured", "basis": b}))
+                return 1
+            stats["measured"] = stats.get("measured", 0) + 1
         stats["cases"] += 1
         stats["ops"] += len(circ.instructions)
         stats["passes"] += len(passes)
