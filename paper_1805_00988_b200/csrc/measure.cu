@@ -365,13 +365,20 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
 
 // M3 for complex64 registers of >= 2^17 amplitudes (whole warps of 4096-
 // amplitude chunks): the same trajectories, but each warp streams its 32
-// chunks through a two-stage shared-memory ring with 1-D bulk copies (one
+// chunks through a shared-memory ring (kTbStages deep) of 1-D bulk copies (one
 // 512-B row per lane and stage, completion on an mbarrier), so a row block is
 // in flight while the previous one is summed.  The register-staged form above
 // kept only eight rows of loads in flight per warp and was memory-latency
 // bound (ncu: long_scoreboard 50% of stalls, 2.1 ms at n = 30).
-constexpr int kTbCols = 64;                  // amplitudes per row and stage (512 B)
-constexpr int kTbPitch4 = kTbCols / 2 + 1;   // padded row pitch in float4 (528 B)
+#ifndef QSB_TB_COLS
+#define QSB_TB_COLS 64
+#endif
+#ifndef QSB_TB_STAGES
+#define QSB_TB_STAGES 2
+#endif
+constexpr int kTbCols = QSB_TB_COLS;         // amplitudes per row and stage (512 B; 256-B rows x 4 stages: 1.37 -> 1.89 ms)
+constexpr int kTbStages = QSB_TB_STAGES;     // ring depth: kTbStages - 1 row blocks in flight while one is summed
+constexpr int kTbPitch4 = kTbCols / 2 + 1;   // padded row pitch in float4 (odd: lanes on distinct bank quads)
 constexpr int kTbStage4 = 32 * kTbPitch4;
 
 __device__ __forceinline__ uint32_t tb_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -410,20 +417,19 @@ __global__ void __launch_bounds__(32)
                         double *__restrict__ g0out, double *__restrict__ d0, double *__restrict__ d1,
                         double *__restrict__ hiout, int *__restrict__ flags, double *__restrict__ fine0,
                         double *__restrict__ fine1) {
-    __shared__ __align__(128) float4 ring[2][kTbStage4];
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(128) float4 ring[kTbStages][kTbStage4];
+    __shared__ __align__(8) uint64_t bar[kTbStages];
     const int lane = threadIdx.x;
     const uint64_t first = (uint64_t)blockIdx.x * 32;
     const uint64_t my = first + lane;
     const float2 *rows = amps + (first << kChunkLog);
     if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&bar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&bar[1])));
+        for (int st = 0; st < kTbStages; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tb_smem(&bar[st])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    tb_issue(rows, &bar[0], ring[0], 0, lane);
-    tb_issue(rows, &bar[1], ring[1], 1, lane);
+    for (int st = 0; st < kTbStages; ++st) tb_issue(rows, &bar[st], ring[st], st, lane);
 
     // prologue and epilogue as in k_trajectories
     const double prefix = g[my];
@@ -440,8 +446,8 @@ __global__ void __launch_bounds__(32)
     constexpr int kCols = (1 << kChunkLog) / kTbCols;
     constexpr int kFineEvery = (1 << kFineLog) / kTbCols;
     for (int c = 0; c < kCols; ++c) {
-        const int st = c & 1;
-        tb_wait(&bar[st], (uint32_t)(c >> 1) & 1u);
+        const int st = c % kTbStages;
+        tb_wait(&bar[st], (uint32_t)(c / kTbStages) & 1u);
         const float4 *row = ring[st] + lane * kTbPitch4;
 #pragma unroll 8
         for (int j = 0; j < kTbCols / 2; ++j) {
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__(32)
             t0 = __dadd_rn(t0, p1);
             t1 = __dadd_rn(t1, p1);
         }
-        if (c + 2 < kCols) tb_issue(rows, &bar[st], ring[st], c + 2, lane);
+        if (c + kTbStages < kCols) tb_issue(rows, &bar[st], ring[st], c + kTbStages, lane);
         if (fine0 && (c + 1) % kFineEvery == 0 && c + 1 < kCols) {
             const int f = (c + 1) / kFineEvery;
             if (exact0) {
