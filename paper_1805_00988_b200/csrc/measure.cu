@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kTrajWarps * 32)
 #define QSB_TB_STAGES 2
 #endif
 constexpr int kTbCols = QSB_TB_COLS;         // amplitudes per row and stage (512 B; 256-B rows x 4 stages: 1.37 -> 1.89 ms)
-constexpr int kTbStages = QSB_TB_STAGES;     // ring depth: kTbStages - 1 row blocks in flight while one is summed
+constexpr int kTbStages = QSB_TB_STAGES;     // ring depth (3 stages, 4 warps/SM: 1.67 ms vs 1.37 with 2 stages, 6 warps/SM)
 constexpr int kTbPitch4 = kTbCols / 2 + 1;   // padded row pitch in float4 (odd: lanes on distinct bank quads)
 constexpr int kTbStage4 = 32 * kTbPitch4;
 
@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(32)
                         double *__restrict__ g0out, double *__restrict__ d0, double *__restrict__ d1,
                         double *__restrict__ hiout, int *__restrict__ flags, double *__restrict__ fine0,
                         double *__restrict__ fine1) {
-    __shared__ __align__(128) float4 ring[kTbStages][kTbStage4];
+    extern __shared__ __align__(128) float4 tb_dyn[];  // kTbStages x kTbStage4 (dynamic: may exceed 48 KB)
+    float4(*ring)[kTbStage4] = reinterpret_cast<float4(*)[kTbStage4]>(tb_dyn);
     __shared__ __align__(8) uint64_t bar[kTbStages];
     const int lane = threadIdx.x;
     const uint64_t first = (uint64_t)blockIdx.x * 32;
@@ -1336,9 +1337,12 @@ static int cdf_chain_t(qs_state *s, const A *amps, const CdfScratch &c, double s
         if constexpr (std::is_same<A, float2>::value)  // QSB_TRAJ_REGS=1: the register-staged form (probes)
             bulk = c.clog == kChunkLog && c.nch % 32 == 0 && !traj_regs();
         if constexpr (std::is_same<A, float2>::value) {
-            if (bulk)
-                k_trajectories_bulk<<<(unsigned)(c.nch / 32), 32, 0, s->stream>>>(
+            if (bulk) {
+                constexpr int kRingBytes = kTbStages * kTbStage4 * 16;
+                if (int rc = ensure_smem_attr((const void *)k_trajectories_bulk, kRingBytes)) return rc;
+                k_trajectories_bulk<<<(unsigned)(c.nch / 32), 32, kRingBytes, s->stream>>>(
                     amps, c.nch, s_start, c.start, c.g0, c.d0, c.d1, c.hi, c.flags, c.fine0, c.fine1);
+            }
         }
         if (!bulk)
             k_trajectories<<<blocks, kTrajWarps * 32, 0, s->stream>>>(
